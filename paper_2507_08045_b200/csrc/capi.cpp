@@ -1,0 +1,767 @@
+// capi.cpp — the extern "C" boundary (include/krul_b200.h).
+//
+// Every entry validates on the host first (reference "validate before
+// compute"), runs device work through kb::, and maps kb::Error codes to
+// krul_status. The estimator and selector live here because they are thin:
+// their arithmetic is the K1/K2/K3 kernels in kernels.cu.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "host.hpp"
+
+using namespace kb;
+
+struct krul_ctx {
+  Ctx* c;
+};
+struct krul_conv {
+  Conv* v;
+};
+struct krul_snapshot {
+  Snapshot* s;
+};
+
+namespace kb {
+Snapshot* snapshot_compress(Ctx& c, Conv& conv, const krul_pair* pairs, int np, const int64_t* p,
+                            int64_t L, int mode);
+Snapshot* snapshot_from_host(Ctx& c, const krul_pair* pairs, int np, const int64_t* p, int64_t L,
+                             int mode, const float* const* k, const float* const* v);
+void snapshot_blob_f32(const Snapshot& s, int b, int64_t row0, int64_t rows, float* k, float* v);
+void snapshot_expand(const Snapshot& s, int layer, float* k, float* v, int64_t* start,
+                     int64_t* end);
+
+// Streaming estimator state (analysis.hpp:66-126): tracked layers, fp64
+// per-(pair, head) sums resident on the device.
+struct Est {
+  Ctx* ctx = nullptr;
+  std::vector<int> layers;
+  int H = 1;
+  DevBuf d_layers, sums, partial, D, tmp;
+  int64_t partial_cap = 0;
+  bool prefill_done = false;
+  int64_t prefill_rows = 0, decode_steps = 0;
+  int P() const { return int(layers.size() * (layers.size() - 1) / 2); }
+};
+}  // namespace kb
+
+struct krul_est {
+  Est* e;
+};
+
+namespace {
+thread_local std::string g_msg;
+thread_local int g_code = 0;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    g_code = 0;
+    return KRUL_OK;
+  } catch (const kb::Error& e) {
+    g_msg = e.what();
+    g_code = e.code;
+  } catch (const std::bad_alloc&) {
+    g_msg = "host allocation failed";
+    g_code = KRUL_E_CUDA;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    g_code = KRUL_E_CUDA;
+  }
+  return g_code;
+}
+void need(const void* p, const char* what) {
+  if (!p) fail(KRUL_E_ARG, std::string("null ") + what);
+}
+void ensure_partial(Est& e, int64_t chunks) {
+  const int64_t need_n = std::max<int64_t>(chunks, 1) * std::max(e.P(), 1) * e.H;
+  if (need_n > e.partial_cap) {
+    e.partial.ensure(size_t(need_n) * 8);
+    e.partial_cap = need_n;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int krul_abi_version(void) { return KRUL_ABI_VERSION; }
+
+int krul_last_error(char* buf, size_t n) {
+  if (buf && n) {
+    std::strncpy(buf, g_msg.c_str(), n - 1);
+    buf[n - 1] = 0;
+  }
+  return g_code;
+}
+
+// ---------------------------------------------------------------- context
+int krul_ctx_create(int device, const krul_model_desc* desc, krul_ctx** out) {
+  return guard([&] {
+    need(desc, "desc");
+    need(out, "out");
+    *out = new krul_ctx{ctx_create(device, *desc)};
+  });
+}
+int krul_ctx_destroy(krul_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    delete ctx->c;
+    delete ctx;
+  });
+}
+int krul_ctx_sync(krul_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    KB_CUDA(cudaSetDevice(ctx->c->device));
+    KB_CUDA(cudaDeviceSynchronize());
+  });
+}
+int krul_config_hash(const krul_model_desc* desc, uint64_t* out) {
+  return guard([&] {
+    need(desc, "desc");
+    krul_model_desc d = *desc;
+    if (d.max_tokens < 1) d.max_tokens = 1;
+    *out = config_hash(cfg_from_desc(d));
+  });
+}
+int krul_weights_upload_f32(krul_ctx* ctx, const float* w, int64_t n) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(w, "weights");
+    weights_upload_f32(*ctx->c, w, n);
+  });
+}
+int krul_weights_init_device(krul_ctx* ctx, uint64_t seed) {
+  return guard([&] {
+    need(ctx, "ctx");
+    weights_init_device(*ctx->c, seed);
+  });
+}
+
+// ---------------------------------------------------------------- conversations
+int krul_conv_create(krul_ctx* ctx, int64_t cap, krul_conv** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    *out = new krul_conv{conv_create(*ctx->c, cap)};
+  });
+}
+int krul_conv_destroy(krul_conv* conv) {
+  return guard([&] {
+    if (!conv) return;
+    delete conv->v;
+    delete conv;
+  });
+}
+int krul_conv_length(krul_conv* conv, int64_t* len) {
+  return guard([&] {
+    need(conv, "conv");
+    *len = conv->v->len;
+  });
+}
+int krul_conv_kv_read(krul_conv* conv, int layer, int64_t start, int64_t end, float* k, float* v) {
+  return guard([&] {
+    need(conv, "conv");
+    Conv& cv = *conv->v;
+    Ctx& c = *cv.ctx;
+    if (layer < 0 || layer >= c.cfg.N) fail(KRUL_E_CONFIG, "layer out of range");
+    if (start < 0 || end > cv.capacity || start > end) fail(KRUL_E_CONFIG, "span out of range");
+    const size_t n = size_t(c.cfg.Hkv) * size_t(end - start) * c.cfg.hd;
+    if (!n) return;
+    KB_CUDA(cudaSetDevice(c.device));
+    DevBuf tmp;
+    float* d = static_cast<float*>(tmp.ensure(2 * n * 4));
+    launch_kv_gather(c, c.s_comp, cv, layer, start, end, d, d + n);
+    KB_CUDA(cudaStreamSynchronize(c.s_comp));
+    if (k) KB_CUDA(cudaMemcpy(k, d, n * 4, cudaMemcpyDeviceToHost));
+    if (v) KB_CUDA(cudaMemcpy(v, d + n, n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+int krul_conv_kv_write(krul_conv* conv, int layer, int64_t start, int64_t end, const float* k,
+                       const float* v) {
+  return guard([&] {
+    need(conv, "conv");
+    need(k, "k");
+    need(v, "v");
+    Conv& cv = *conv->v;
+    Ctx& c = *cv.ctx;
+    if (layer < 0 || layer >= c.cfg.N) fail(KRUL_E_CONFIG, "layer out of range");
+    if (start < 0 || end > cv.capacity || start > end) fail(KRUL_E_CONFIG, "span out of range");
+    const size_t n = size_t(c.cfg.Hkv) * size_t(end - start) * c.cfg.hd;
+    if (!n) return;
+    KB_CUDA(cudaSetDevice(c.device));
+    DevBuf tmp;
+    float* d = static_cast<float*>(tmp.ensure(2 * n * 4));
+    KB_CUDA(cudaMemcpy(d, k, n * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(cudaMemcpy(d + n, v, n * 4, cudaMemcpyHostToDevice));
+    launch_kv_scatter_f32(c, c.s_comp, cv, layer, start, end, d, d + n);
+    KB_CUDA(cudaStreamSynchronize(c.s_comp));
+    cv.len = std::max(cv.len, end);
+  });
+}
+
+// ---------------------------------------------------------------- engine
+int krul_set_capture(krul_ctx* ctx, int capture_probs) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->capture_probs = capture_probs;
+  });
+}
+int krul_set_classifier_regions(krul_ctx* ctx, double ifrac, double rfrac) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (!(ifrac > 0.0) || !(rfrac > 0.0) || ifrac + rfrac >= 1.0)
+      fail(KRUL_E_CONFIG, "region fractions must be positive and sum below 1");
+    ctx->c->cap_ifrac = ifrac;
+    ctx->c->cap_rfrac = rfrac;
+  });
+}
+int krul_prefill(krul_ctx* ctx, krul_conv* conv, const int32_t* t, int64_t n, float* logits) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    if (n > 0) need(t, "tokens");
+    prefill(*ctx->c, *conv->v, t, n, logits);
+  });
+}
+int krul_prefill_new(krul_ctx* ctx, krul_conv* conv, const int32_t* t, int64_t n, float* logits) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    if (n > 0) need(t, "tokens");
+    prefill_new(*ctx->c, *conv->v, t, n, logits);
+  });
+}
+int krul_decode_step(krul_ctx* ctx, krul_conv* conv, int32_t tok, float* logits) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    decode_step(*ctx->c, *conv->v, tok, logits);
+  });
+}
+int krul_partial_recompute(krul_ctx* ctx, krul_conv* conv, const int32_t* t, int64_t n,
+                           const int64_t* p, int np) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    need(p, "recompute_len");
+    partial_recompute(*ctx->c, *conv->v, t, n, p, np);
+  });
+}
+int krul_capture_prefill(krul_ctx* ctx, int layer, int head, float* out, int64_t* rows,
+                         int64_t* width) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    if (!c.cap_valid || !c.capture_probs) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention");
+    if (layer < 0 || layer >= c.cfg.N || head < 0 || head >= c.cfg.H) fail(KRUL_E_CONFIG, "index out of range");
+    if (rows) *rows = c.cap_rows;
+    if (width) *width = c.cap_width;
+    if (out) {
+      const size_t n = size_t(c.cap_rows * c.cap_width);
+      const float* src = c.cap_probs.as<float>() + (size_t(layer) * c.cfg.H + head) * n;
+      KB_CUDA(cudaMemcpy(out, src, n * 4, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+int krul_capture_decode(krul_ctx* ctx, float* out, int64_t* width) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
+    if (width) *width = c.dec_width;
+    if (out)
+      KB_CUDA(cudaMemcpy(out, c.dec_rows.p, size_t(c.cfg.N) * c.cfg.H * c.dec_width * 4,
+                         cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---------------------------------------------------------------- analysis
+// analysis.cpp:20-63 over the masses the attention kernel reduced.
+int krul_classify(krul_ctx* ctx, double gamma, double ifrac, double rfrac, double* avg,
+                  int* is_ir) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    if (!(gamma > 0.0) || gamma > 1.0) fail(KRUL_E_CONFIG, "gamma must lie in (0, 1]");
+    if (!(ifrac > 0.0) || !(rfrac > 0.0) || ifrac + rfrac >= 1.0)
+      fail(KRUL_E_CONFIG, "region fractions must be positive and sum below 1");
+    if (!c.cap_valid || c.cap_rows == 0) fail(KRUL_E_CLASSIFICATION, "classification requires prefill attention");
+    const int64_t W = c.cap_width;
+    const int64_t il = int64_t(ifrac * double(W)), rl = int64_t(rfrac * double(W));
+    if (il < 1 || rl < 1) fail(KRUL_E_CLASSIFICATION, "sequence too short to form both attention regions");
+    if (ifrac != c.cap_ifrac || rfrac != c.cap_rfrac)
+      fail(KRUL_E_CONFIG, "classifier regions differ from those set before the prefill");
+    const int N = c.cfg.N, H = c.cfg.H;
+    const int64_t R = c.cap_rows;
+    std::vector<double> m(size_t(N) * H * R);
+    KB_CUDA(cudaMemcpy(m.data(), c.cap_mass.p, m.size() * 8, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < N; ++l) {
+      double mass = 0.0;
+      for (int h = 0; h < H; ++h) {
+        double hm = 0.0;
+        for (int64_t r = 0; r < R; ++r) hm += m[(size_t(l) * H + h) * R + r];
+        mass += hm;
+      }
+      const double a = mass / (double(H) * double(R));
+      if (avg) avg[l] = a;
+      if (is_ir) is_ir[l] = a >= gamma ? 1 : 0;
+    }
+  });
+}
+
+int krul_est_create(krul_ctx* ctx, const int* ir, int n, krul_est** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    auto* e = new Est;
+    e->ctx = ctx->c;
+    e->H = ctx->c->cfg.H;
+    e->layers.assign(ir, ir + n);
+    std::sort(e->layers.begin(), e->layers.end());
+    e->layers.erase(std::unique(e->layers.begin(), e->layers.end()), e->layers.end());
+    if (!e->layers.empty() && e->layers.front() < 0) {
+      delete e;
+      fail(KRUL_E_CONFIG, "layer indices must be non-negative");
+    }
+    KB_CUDA(cudaSetDevice(ctx->c->device));
+    const size_t nl = std::max<size_t>(e->layers.size(), 1);
+    e->d_layers.ensure(nl * 4);
+    if (!e->layers.empty())
+      KB_CUDA(cudaMemcpy(e->d_layers.p, e->layers.data(), e->layers.size() * 4, cudaMemcpyHostToDevice));
+    const size_t ns = size_t(std::max(e->P(), 1)) * e->H;
+    e->sums.ensure(ns * 8);
+    KB_CUDA(cudaMemset(e->sums.p, 0, ns * 8));
+    *out = new krul_est{e};
+  });
+}
+int krul_est_destroy(krul_est* est) {
+  return guard([&] {
+    if (!est) return;
+    delete est->e;
+    delete est;
+  });
+}
+static void fold_prefill_dev(Est& e, const float* probs, int64_t rows, int64_t W, int N) {
+  if (e.prefill_done) fail(KRUL_E_ACCOUNTING, "prefill attention folded twice");
+  if (!e.layers.empty() && e.layers.back() >= N) fail(KRUL_E_CONFIG, "record does not cover all tracked layers");
+  Ctx& c = *e.ctx;
+  ensure_partial(e, (rows * W + 511) / 512);
+  launch_fold_prefill(c.s_est, probs, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
+                      e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);
+  KB_CUDA(cudaStreamSynchronize(c.s_est));
+  e.prefill_done = true;
+  e.prefill_rows = rows;
+}
+static void fold_decode_dev(Est& e, const float* rows, int64_t W, int N) {
+  if (!e.layers.empty() && e.layers.back() >= N)
+    fail(KRUL_E_STATE_CORRUPTION, "decode rows do not cover all tracked layers");
+  Ctx& c = *e.ctx;
+  ensure_partial(e, (W + 511) / 512);
+  launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
+                     e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);
+  KB_CUDA(cudaStreamSynchronize(c.s_est));
+  ++e.decode_steps;
+}
+int krul_est_fold_prefill(krul_est* est) {
+  return guard([&] {
+    need(est, "est");
+    Est& e = *est->e;
+    Ctx& c = *e.ctx;
+    if (!c.cap_valid || !c.capture_probs) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention (krul_set_capture)");
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaStreamSynchronize(c.s_comp));
+    KB_CUDA(cudaStreamSynchronize(c.s_new));
+    fold_prefill_dev(e, c.cap_probs.as<float>(), c.cap_rows, c.cap_width, c.cfg.N);
+  });
+}
+int krul_est_fold_decode(krul_est* est) {
+  return guard([&] {
+    need(est, "est");
+    Est& e = *est->e;
+    Ctx& c = *e.ctx;
+    if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaStreamSynchronize(c.s_comp));
+    fold_decode_dev(e, c.dec_rows.as<float>(), c.dec_width, c.cfg.N);
+  });
+}
+int krul_est_fold_prefill_host(krul_est* est, const float* probs, int N, int64_t rows, int64_t W) {
+  return guard([&] {
+    need(est, "est");
+    need(probs, "probs");
+    Est& e = *est->e;
+    if (e.prefill_done) fail(KRUL_E_ACCOUNTING, "prefill attention folded twice");
+    KB_CUDA(cudaSetDevice(e.ctx->device));
+    const size_t n = size_t(N) * e.H * size_t(rows) * size_t(W);
+    float* d = static_cast<float*>(e.tmp.ensure(std::max<size_t>(n, 1) * 4));
+    KB_CUDA(cudaMemcpy(d, probs, n * 4, cudaMemcpyHostToDevice));
+    fold_prefill_dev(e, d, rows, W, N);
+  });
+}
+int krul_est_fold_decode_host(krul_est* est, const float* rows, int N, int64_t W) {
+  return guard([&] {
+    need(est, "est");
+    need(rows, "rows");
+    Est& e = *est->e;
+    KB_CUDA(cudaSetDevice(e.ctx->device));
+    const size_t n = size_t(N) * e.H * size_t(W);
+    float* d = static_cast<float*>(e.tmp.ensure(std::max<size_t>(n, 1) * 4));
+    KB_CUDA(cudaMemcpy(d, rows, n * 4, cudaMemcpyHostToDevice));
+    fold_decode_dev(e, d, W, N);
+  });
+}
+int krul_est_sums(krul_est* est, double* sums) {
+  return guard([&] {
+    need(est, "est");
+    Est& e = *est->e;
+    KB_CUDA(cudaSetDevice(e.ctx->device));
+    if (e.P() > 0) KB_CUDA(cudaMemcpy(sums, e.sums.p, size_t(e.P()) * e.H * 8, cudaMemcpyDeviceToHost));
+  });
+}
+int krul_est_finalize(krul_est* est, double* D) {
+  return guard([&] {
+    need(est, "est");
+    Est& e = *est->e;
+    if (!e.prefill_done) fail(KRUL_E_ACCOUNTING, "finalize requires the prefill part to be folded");
+    const int n = int(e.layers.size());
+    if (n == 0) return;
+    KB_CUDA(cudaSetDevice(e.ctx->device));
+    double* dD = static_cast<double*>(e.D.ensure(size_t(n) * n * 8));
+    launch_finalize(e.ctx->s_est, e.sums.as<double>(), n, e.H, dD);
+    KB_CUDA(cudaStreamSynchronize(e.ctx->s_est));
+    KB_CUDA(cudaMemcpy(D, dD, size_t(n) * n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+int krul_est_counts(krul_est* est, int64_t* pr, int64_t* ds) {
+  return guard([&] {
+    need(est, "est");
+    if (pr) *pr = est->e->prefill_done ? est->e->prefill_rows : 0;
+    if (ds) *ds = est->e->decode_steps;
+  });
+}
+
+// ---------------------------------------------------------------- selector
+int krul_quota(int n_layers, double r_l, int* out) {
+  return guard([&] { *out = quota(n_layers, r_l); });
+}
+// strategy.cpp:27-74: host assembles the (d, i, j) candidates, K3 sorts and
+// greedily matches them on the device.
+int krul_select(krul_ctx* ctx, const double* D, const int* dm_layers, int n, const int* ir,
+                int n_ir, double r_l, int n_layers, krul_pair* out, int* n_out, int* exhausted) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (r_l < 0.0 || r_l > 1.0) fail(KRUL_E_CONFIG, "r_l must lie in [0, 1]");
+    const int q = quota(n_layers, r_l);
+    *n_out = 0;
+    *exhausted = 0;
+    if (q == 0) return;
+    std::vector<int> layers(ir, ir + n_ir);
+    std::sort(layers.begin(), layers.end());
+    layers.erase(std::unique(layers.begin(), layers.end()), layers.end());
+    if (layers.size() < 2) {
+      *exhausted = 1;
+      return;
+    }
+    if (layers.back() >= 256 || layers.front() < 0) fail(KRUL_E_CONFIG, "layer index outside [0, 256)");
+    auto pos = [&](int layer) {
+      const int* it = std::lower_bound(dm_layers, dm_layers + n, layer);
+      if (it == dm_layers + n || *it != layer) fail(KRUL_E_CONFIG, "layer not tracked by the distance matrix");
+      return int(it - dm_layers);
+    };
+    std::vector<double> cd;
+    std::vector<int> ci, cj;
+    for (size_t a = 0; a < layers.size(); ++a)
+      for (size_t b = a + 1; b < layers.size(); ++b) {
+        cd.push_back(D[size_t(pos(layers[a])) * n + pos(layers[b])]);
+        ci.push_back(layers[a]);
+        cj.push_back(layers[b]);
+      }
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    const int nc = int(cd.size());
+    DevBuf buf;
+    char* p = static_cast<char*>(buf.ensure(size_t(nc) * 16 + size_t(nc) * 16 + 64));
+    double* d_cd = reinterpret_cast<double*>(p);
+    int* d_ci = reinterpret_cast<int*>(d_cd + nc);
+    int* d_cj = d_ci + nc;
+    double* d_od = reinterpret_cast<double*>(d_cj + nc);
+    int* d_oi = reinterpret_cast<int*>(d_od + nc);
+    int* d_oj = d_oi + nc;
+    int* d_on = d_oj + nc;
+    KB_CUDA(cudaMemcpy(d_cd, cd.data(), size_t(nc) * 8, cudaMemcpyHostToDevice));
+    KB_CUDA(cudaMemcpy(d_ci, ci.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(cudaMemcpy(d_cj, cj.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
+    launch_select(c.s_est, d_cd, d_ci, d_cj, nc, q, d_oi, d_oj, d_od, d_on);
+    KB_CUDA(cudaStreamSynchronize(c.s_est));
+    int np = 0;
+    KB_CUDA(cudaMemcpy(&np, d_on, 4, cudaMemcpyDeviceToHost));
+    std::vector<int> oi(size_t(std::max(np, 1))), oj(oi.size());
+    std::vector<double> od(oi.size());
+    if (np) {
+      KB_CUDA(cudaMemcpy(oi.data(), d_oi, size_t(np) * 4, cudaMemcpyDeviceToHost));
+      KB_CUDA(cudaMemcpy(oj.data(), d_oj, size_t(np) * 4, cudaMemcpyDeviceToHost));
+      KB_CUDA(cudaMemcpy(od.data(), d_od, size_t(np) * 8, cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < np; ++k) out[k] = krul_pair{oi[size_t(k)], oj[size_t(k)], od[size_t(k)]};
+    *n_out = np;
+    *exhausted = 2 * np < q ? 1 : 0;
+  });
+}
+
+// ---------------------------------------------------------------- scheduler
+int krul_build_plan(int64_t L, int N, double r_c, const krul_pair* pairs, int np, int64_t* out) {
+  return guard([&] {
+    auto p = build_plan(L, N, r_c, pairs, np);
+    std::copy(p.begin(), p.end(), out);
+  });
+}
+int krul_uniform_plan(int64_t L, int N, double r_c, int64_t* out) {
+  return guard([&] {
+    auto p = uniform_plan(L, N, r_c);
+    std::copy(p.begin(), p.end(), out);
+  });
+}
+int krul_default_rc_grid(double step, double* out, int* n) {
+  return guard([&] {
+    auto g = default_grid(step);
+    *n = int(g.size());
+    if (out) std::copy(g.begin(), g.end(), out);
+  });
+}
+int krul_calibrate_rc(const krul_cost_model* cost, int N, int64_t L, int64_t d,
+                      const krul_pair* pairs, int np, const double* grid, int ng, double* out) {
+  return guard([&] { *out = calibrate(cost_from(cost), N, L, d, pairs, np, grid, ng); });
+}
+int krul_validate_plan(int64_t L, const int64_t* p, int N, const krul_pair* pairs, int np, int* mask) {
+  return guard([&] { *mask = validate_plan(L, std::vector<int64_t>(p, p + N), pairs, np); });
+}
+int krul_blob_specs(int64_t L, const int64_t* p, int N, const krul_pair* pairs, int np,
+                    krul_blob_spec* out, int* n_out) {
+  return guard([&] {
+    auto s = blob_specs(std::vector<int64_t>(p, p + N), L, pairs, np);
+    *n_out = int(s.size());
+    if (out) std::copy(s.begin(), s.end(), out);
+  });
+}
+// scheduler.cpp:282-318
+int krul_simulate(int64_t L, const int64_t* p, int N, const krul_pair* pairs, int np,
+                  const krul_cost_model* cost, int64_t d, double* out) {
+  return guard([&] {
+    const Cost c = cost_from(cost);
+    std::vector<int64_t> pv(p, p + N);
+    double tc = 0.0, tl = 0.0;
+    for (int l = 0; l < N; ++l) tc += c.layer_flops(pv[size_t(l)], d) / c.f;
+    for (const auto& s : blob_specs(pv, L, pairs, np)) tl += c.blob_bytes(s.end - s.start, d) / c.b;
+    const double mk = std::max(tc, tl);
+    out[0] = mk;
+    out[1] = tc;
+    out[2] = tl;
+    out[3] = mk > 0 && tc > 0 ? (mk - tc) / mk : 0.0;
+    out[4] = mk > 0 && tl > 0 ? (mk - tl) / mk : 0.0;
+  });
+}
+
+// ---------------------------------------------------------------- kvstore
+int krul_snapshot_compress(krul_ctx* ctx, krul_conv* conv, const krul_pair* pairs, int np,
+                           const int64_t* p, int64_t L, int mode, krul_snapshot** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    need(p, "recompute_len");
+    Ctx& c = *ctx->c;
+    std::vector<int64_t> pv(p, p + c.cfg.N);
+    (void)blob_specs(pv, L, pairs, np);  // SnapshotError on malformed strategy
+    *out = new krul_snapshot{snapshot_compress(c, *conv->v, pairs, np, p, L, mode)};
+  });
+}
+int krul_snapshot_from_host(krul_ctx* ctx, const krul_pair* pairs, int np, const int64_t* p,
+                            int64_t L, int mode, const float* const* k, const float* const* v,
+                            krul_snapshot** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    *out = new krul_snapshot{snapshot_from_host(*ctx->c, pairs, np, p, L, mode, k, v)};
+  });
+}
+int krul_snapshot_destroy(krul_snapshot* s) {
+  return guard([&] {
+    if (!s) return;
+    delete s->s;
+    delete s;
+  });
+}
+int krul_snapshot_n_blobs(krul_snapshot* s) { return s ? int(s->s->blobs.size()) : 0; }
+int krul_snapshot_blob(krul_snapshot* s, int b, krul_blob_spec* spec, float* k, float* v) {
+  return guard([&] {
+    need(s, "snapshot");
+    const Snapshot& sn = *s->s;
+    if (b < 0 || b >= int(sn.blobs.size())) fail(KRUL_E_CONFIG, "blob index out of range");
+    const auto& bl = sn.blobs[size_t(b)];
+    if (spec) *spec = krul_blob_spec{{bl.owners[0], bl.owners[1]}, bl.start, bl.end};
+    if (k || v) snapshot_blob_f32(sn, b, 0, bl.end - bl.start, k, v);
+  });
+}
+// kvstore.cpp:345-358 (the reference accounts f32 rows; bf16 halves it).
+int krul_snapshot_storage(krul_snapshot* s, uint64_t* full, uint64_t* stored) {
+  return guard([&] {
+    need(s, "snapshot");
+    const Snapshot& sn = *s->s;
+    const uint64_t row = 2ull * uint64_t(sn.Hkv) * uint64_t(sn.hd) * uint64_t(sn.ctx->esz);
+    *full = uint64_t(sn.N) * uint64_t(sn.L) * row;
+    *stored = 0;
+    for (const auto& b : sn.blobs) *stored += uint64_t(b.end - b.start) * row;
+  });
+}
+int krul_snapshot_plan(krul_snapshot* s, int64_t* p, int64_t* L) {
+  return guard([&] {
+    need(s, "snapshot");
+    if (p) std::copy(s->s->p.begin(), s->s->p.end(), p);
+    if (L) *L = s->s->L;
+  });
+}
+int krul_snapshot_set_plan(krul_snapshot* s, const int64_t* p) {
+  return guard([&] {
+    need(s, "snapshot");
+    std::copy(p, p + s->s->N, s->s->p.begin());
+  });
+}
+int krul_expand(krul_snapshot* s, int layer, float* k, float* v, int64_t* start, int64_t* end) {
+  return guard([&] {
+    need(s, "snapshot");
+    snapshot_expand(*s->s, layer, k, v, start, end);
+  });
+}
+
+// ---------------------------------------------------------------- restore
+int krul_restore(krul_ctx* ctx, krul_conv* conv, krul_snapshot* snap, const int32_t* hist,
+                 int64_t L, krul_restore_stats* st) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    need(snap, "snapshot");
+    if (L > 0) need(hist, "history");
+    restore(*ctx->c, *conv->v, *snap->s, hist, L, st, nullptr, 0, nullptr, nullptr);
+  });
+}
+int krul_restore_and_prefill(krul_ctx* ctx, krul_conv* conv, krul_snapshot* snap,
+                             const int32_t* hist, int64_t L, const int32_t* nt, int64_t n_new,
+                             float* logits, krul_restore_stats* st, double* ttft_ms) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    need(snap, "snapshot");
+    need(nt, "new tokens");
+    if (L > 0) need(hist, "history");
+    restore(*ctx->c, *conv->v, *snap->s, hist, L, st, nt, n_new, logits, ttft_ms);
+  });
+}
+
+// Measured stream rates (calibrate_rc_measured, scheduler.cpp:402-443, as
+// device rates rather than a wall-clock grid): pinned H2D bytes/s over a
+// 256 MiB copy and recompute flop/s of one full layer at 2048 rows.
+int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps, double* flops) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    if (h2d_bps) {
+      const size_t n = size_t(256) << 20;
+      PinnedBuf hb;
+      DevBuf db;
+      void* h = hb.ensure(n);
+      void* d = db.ensure(n);
+      std::memset(h, 1, n);
+      cudaEvent_t a, b;
+      KB_CUDA(cudaEventCreate(&a));
+      KB_CUDA(cudaEventCreate(&b));
+      float best = 1e30f;
+      for (int i = 0; i < 4; ++i) {
+        KB_CUDA(cudaEventRecord(a, c.s_load));
+        KB_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, c.s_load));
+        KB_CUDA(cudaEventRecord(b, c.s_load));
+        KB_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        KB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        best = std::min(best, ms);
+      }
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      *h2d_bps = double(n) / (double(best) * 1e-3);
+    }
+    if (flops) {
+      need(scratch, "scratch conversation");
+      Conv& cv = *scratch->v;
+      const int64_t rows = std::min<int64_t>(2048, cv.capacity);
+      WS w = ws_get(c, 0, rows);
+      std::vector<int32_t> tok(static_cast<size_t>(rows));
+      for (int64_t i = 0; i < rows; ++i) tok[size_t(i)] = int32_t((i * 7919) % c.cfg.V);
+      int32_t* d_tok = upload_tokens(c, c.s_comp, tok.data(), rows, c.ws_tok);
+      launch_embed(c, c.s_comp, d_tok, rows, w.h);
+      cudaEvent_t a, b;
+      KB_CUDA(cudaEventCreate(&a));
+      KB_CUDA(cudaEventCreate(&b));
+      float best = 1e30f;
+      for (int i = 0; i < 3; ++i) {
+        KB_CUDA(cudaEventRecord(a, c.s_comp));
+        layer_forward(c, c.s_comp, w, cv, 0, w.h, rows, 0, rows, w.h2, nullptr);
+        KB_CUDA(cudaEventRecord(b, c.s_comp));
+        KB_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        KB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        best = std::min(best, ms);
+      }
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      Cost cm;
+      cm.kv_dim = c.cfg.kvd();
+      cm.q_dim = c.cfg.qd();
+      cm.ffn_hidden = c.cfg.F;
+      cm.ffn_kind = c.cfg.ffn_kind;
+      *flops = cm.layer_flops(rows, c.cfg.d) / (double(best) * 1e-3);
+    }
+  });
+}
+
+int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A,
+                    const float* B, const float* bias, int epi, float* Cout) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t s = c.s_comp;
+    DevBuf a32, b32, a, b, out, outc, bb;
+    float* da = static_cast<float*>(a32.ensure(size_t(M * K) * 4));
+    float* db = static_cast<float*>(b32.ensure(size_t(N * K) * 4));
+    KB_CUDA(cudaMemcpy(da, A, size_t(M * K) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(cudaMemcpy(db, B, size_t(N * K) * 4, cudaMemcpyHostToDevice));
+    void* ca = a.ensure(size_t(M * K) * c.esz);
+    void* cb = b.ensure(size_t(N * K) * c.esz);
+    launch_cvt_from_f32(c, s, da, ca, M * K);
+    launch_cvt_from_f32(c, s, db, cb, N * K);
+    const int64_t ncols = epi == Epi::SWIGLU ? N / 2 : N;
+    float* o = static_cast<float*>(out.ensure(size_t(M * ncols) * 4 + 16));
+    Epi e;
+    e.kind = epi;
+    e.ldo = ncols;
+    if (bias) {
+      float* dbias = static_cast<float*>(bb.ensure(size_t(N) * 4));
+      KB_CUDA(cudaMemcpy(dbias, bias, size_t(N) * 4, cudaMemcpyHostToDevice));
+      e.bias = dbias;
+    }
+    if (epi == Epi::F32 || epi == Epi::RESID) {
+      e.out = o;
+      if (epi == Epi::RESID) {
+        KB_CUDA(cudaMemcpy(o, Cout, size_t(M * N) * 4, cudaMemcpyHostToDevice));
+        e.resid = o;
+        e.ldr = N;
+      }
+    } else {
+      e.out = outc.ensure(size_t(M * ncols) * c.esz + 16);
+    }
+    gemm(c, s, M, N, K, ca, K, cb, K, e);
+    if (epi == Epi::TANH || epi == Epi::SWIGLU || epi == Epi::CDT) launch_cvt_to_f32(c, s, e.out, o, M * ncols);
+    KB_CUDA(cudaStreamSynchronize(s));
+    KB_CUDA(cudaMemcpy(Cout, o, size_t(M * ncols) * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// host.hpp — host-side building blocks shared by the C ABI translation units.
+#pragma once
+#include <vector>
+
+#include "kb.hpp"
+
+namespace kb {
+
+struct WS {  // per-stream activation workspace
+  float *h = nullptr, *h2 = nullptr, *qkv = nullptr, *hmid = nullptr;
+  void *xn = nullptr, *q = nullptr, *attn = nullptr, *hmidc = nullptr, *act = nullptr;
+};
+
+Ctx* ctx_create(int device, const krul_model_desc& desc);
+void weights_upload_f32(Ctx& c, const float* w, int64_t n);
+void weights_init_device(Ctx& c, uint64_t seed);
+Conv* conv_create(Ctx& c, int64_t capacity);
+WS ws_get(Ctx& c, int set, int64_t rows);
+void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const float* h_in,
+                   int64_t rows, int64_t pos0, int64_t out_rows, float* h_out,
+                   const AttnArgs* cap);
+void check_tokens(const Ctx& c, const int32_t* t, int64_t n);
+int32_t* upload_tokens(Ctx& c, cudaStream_t s, const int32_t* t, int64_t n, DevBuf& buf);
+void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_tok, int64_t n,
+                  int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits);
+void prefill(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, float* logits);
+void prefill_new(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, float* logits);
+void decode_step(Ctx& c, Conv& conv, int32_t tok, float* logits);
+void enqueue_partial(Ctx& c, cudaStream_t s, Conv& conv, const int32_t* d_tok,
+                     const std::vector<int64_t>& p, bool full_last, cudaEvent_t* ev);
+void check_plan_shape(const Ctx& c, int64_t n, const int64_t* p, int np);
+void partial_recompute(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, const int64_t* p,
+                       int np);
+
+// ---- scheduler arithmetic (scheduler.cpp) ----------------------------------
+struct Cost {
+  double f = 312e12, b = 139e9, ffn_mult = 4.0;
+  int64_t kv_dim = 0, q_dim = 0, ffn_hidden = 0;
+  double bpe = 4.0;
+  int ffn_kind = 0;
+  double layer_flops(int64_t p, int64_t d) const;
+  double blob_bytes(int64_t span, int64_t d) const;
+};
+Cost cost_from(const krul_cost_model* m);
+int quota(int n_layers, double r_l);
+std::vector<krul_blob_spec> blob_specs(const std::vector<int64_t>& p, int64_t L,
+                                       const krul_pair* pairs, int np);
+std::vector<int64_t> build_plan(int64_t L, int N, double r_c, const krul_pair* pairs, int np);
+std::vector<int64_t> uniform_plan(int64_t L, int N, double r_c);
+double calibrate(const Cost& c, int N, int64_t L, int64_t d, const krul_pair* pairs, int np,
+                 const double* grid, int ng);
+std::vector<double> default_grid(double step);
+int validate_plan(int64_t L, const std::vector<int64_t>& p, const krul_pair* pairs, int np);
+
+// ---- compressed KV store ---------------------------------------------------
+struct Snapshot {
+  Ctx* ctx = nullptr;
+  uint64_t config_hash = 0;
+  int N = 0, Hkv = 0, hd = 0;
+  int64_t L = 0;
+  int mode = 0;
+  std::vector<krul_pair> pairs;
+  std::vector<int64_t> p;
+  struct Blob {
+    int owners[2];
+    int64_t start, end;
+    size_t off;    // byte offset in `host`
+    size_t bytes;
+  };
+  std::vector<Blob> blobs;
+  PinnedBuf host;  // all blobs, compute dtype, [K: Hkv][rows][hd][V: ...]
+  size_t total = 0;
+};
+int validate_plan_snapshot(const std::vector<int64_t>& p, int64_t L, const Snapshot& s);
+void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
+             krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
+             double* ttft_ms);
+
+}  // namespace kb

@@ -1,0 +1,121 @@
+// host_ctx.cpp — device context, weights, paged KV pool, conversations.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "kb.hpp"
+
+namespace kb {
+
+void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+void* DevBuf::ensure(size_t n) {
+  if (n > bytes) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    KB_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  return p;
+}
+PinnedBuf::~PinnedBuf() {
+  if (p) cudaFreeHost(p);
+}
+void* PinnedBuf::ensure(size_t n) {
+  if (n > bytes) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    KB_CUDA(cudaMallocHost(&p, n));
+    bytes = n;
+  }
+  return p;
+}
+
+// engine.cpp:10-25 (+ GQA / ffn_kind checks of the extensions).
+Cfg cfg_from_desc(const krul_model_desc& d) {
+  Cfg c;
+  c.N = d.n_layers;
+  c.H = d.n_heads;
+  c.Hkv = d.n_kv_heads > 0 ? d.n_kv_heads : d.n_heads;
+  c.hd = d.head_dim;
+  c.d = d.d_model;
+  c.V = d.vocab_size;
+  c.ffn_mult = d.ffn_mult;
+  c.ffn_kind = d.ffn_kind;
+  c.seed = d.seed;
+  c.theta = d.rope_theta > 0 ? d.rope_theta : 1e4;
+  c.dtype = d.dtype;
+  c.max_tokens = d.max_tokens;
+  if (c.N < 2) fail(KRUL_E_CONFIG, "n_layers must be >= 2");
+  if (c.H < 1) fail(KRUL_E_CONFIG, "n_heads must be >= 1");
+  if (c.hd < 1) fail(KRUL_E_CONFIG, "head_dim must be >= 1");
+  if (c.d != c.H * c.hd) fail(KRUL_E_CONFIG, "d_model must equal n_heads * head_dim");
+  if (c.V < 2) fail(KRUL_E_CONFIG, "vocab_size must be >= 2");
+  c.F = int(std::lround(c.ffn_mult * float(c.d)));
+  if (!(c.ffn_mult > 0.f) || c.F < 1) fail(KRUL_E_CONFIG, "ffn_mult must yield a positive hidden width");
+  if (c.H % c.Hkv != 0) fail(KRUL_E_CONFIG, "n_heads must be a multiple of n_kv_heads");
+  if (c.ffn_kind != KRUL_FFN_TANH && c.ffn_kind != KRUL_FFN_SWIGLU) fail(KRUL_E_CONFIG, "unknown ffn_kind");
+  if (c.dtype != KRUL_F32 && c.dtype != KRUL_BF16) fail(KRUL_E_CONFIG, "unknown dtype");
+  if (c.max_tokens < 1) fail(KRUL_E_CONFIG, "max_tokens must be >= 1");
+  return c;
+}
+
+static uint64_t fnv(const void* p, size_t n, uint64_t h) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+// ModelConfig::hash (engine.cpp:27-36): FNV-1a over the fields in order;
+// extension fields fold in only when they leave the reference architecture.
+uint64_t config_hash(const Cfg& c) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  h = fnv(&c.N, sizeof c.N, h);
+  h = fnv(&c.H, sizeof c.H, h);
+  h = fnv(&c.hd, sizeof c.hd, h);
+  h = fnv(&c.d, sizeof c.d, h);
+  h = fnv(&c.V, sizeof c.V, h);
+  h = fnv(&c.ffn_mult, sizeof c.ffn_mult, h);
+  h = fnv(&c.seed, sizeof c.seed, h);
+  if (c.Hkv != c.H || c.ffn_kind != 0 || c.theta != 1e4) {
+    h = fnv(&c.Hkv, sizeof c.Hkv, h);
+    h = fnv(&c.ffn_kind, sizeof c.ffn_kind, h);
+    h = fnv(&c.theta, sizeof c.theta, h);
+  }
+  return h;
+}
+
+Ctx::~Ctx() {
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  for (auto s : {s_comp, s_load, s_new, s_est})
+    if (s) cudaStreamDestroy(s);
+}
+
+cudaEvent_t Ctx::event() {
+  if (ev_next == ev_pool.size()) {
+    cudaEvent_t e;
+    KB_CUDA(cudaEventCreate(&e));
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_next++];
+}
+
+Conv::~Conv() {
+  if (ctx) {
+    for (int p : pages) ctx->free_pages.push_back(p);
+  }
+  if (d_pt) cudaFree(d_pt);
+}
+
+}  // namespace kb

@@ -1,0 +1,264 @@
+// host_restore.cpp — compressed KV store (pinned host blobs) and the
+// two-stream restoration DAG.
+//
+// Restore (scheduler.cpp:320-400, re-designed for the GPU): the reference runs
+// the whole prefix recompute on the caller thread while one loader thread
+// expands blobs, then splices per layer. Here both streams write disjoint
+// position ranges of the same paged cache, so there is no splice:
+//   load stream    : per blob (service order = shallowest owner):
+//                    cudaMemcpyAsync pinned -> staging (K4),
+//                    expand kernel staging -> pages of each owner (K5),
+//                    event loaded[owner]
+//   compute stream : pyramid prefix recompute layer by layer (K6),
+//                    event computed[l]
+//   new stream     : (restore_and_prefill) new-input prefill of layer l waits
+//                    on computed[l] and loaded[l] only (K7), so it overlaps the
+//                    remaining restore instead of trailing it.
+#include <algorithm>
+#include <cstring>
+
+#include "host.hpp"
+
+namespace kb {
+
+static float bf16_to_f32(uint16_t b) {
+  uint32_t u = uint32_t(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+static uint16_t f32_to_bf16(float f) {  // round to nearest even (== __float2bfloat16_rn)
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+// Layout blobs of a snapshot from (strategy, plan).
+static void layout_blobs(Ctx& c, Snapshot& s) {
+  const auto specs = blob_specs(s.p, s.L, s.pairs.data(), int(s.pairs.size()));
+  size_t off = 0;
+  s.blobs.clear();
+  for (const auto& sp : specs) {
+    Snapshot::Blob b;
+    b.owners[0] = sp.owners[0];
+    b.owners[1] = sp.owners[1];
+    b.start = sp.start;
+    b.end = sp.end;
+    b.off = off;
+    b.bytes = size_t(2) * c.cfg.Hkv * size_t(sp.end - sp.start) * c.cfg.hd * c.esz;
+    off += (b.bytes + 255) & ~size_t(255);
+    s.blobs.push_back(b);
+  }
+  s.total = off;
+  s.host.ensure(std::max<size_t>(off, 256));
+}
+
+static Snapshot* new_snapshot(Ctx& c, const krul_pair* pairs, int np, const int64_t* p, int64_t L,
+                              int mode) {
+  auto* s = new Snapshot;
+  s->ctx = &c;
+  s->config_hash = config_hash(c.cfg);
+  s->N = c.cfg.N;
+  s->Hkv = c.cfg.Hkv;
+  s->hd = c.cfg.hd;
+  s->L = L;
+  s->mode = mode;
+  s->pairs.assign(pairs, pairs + np);
+  s->p.assign(p, p + c.cfg.N);
+  return s;
+}
+
+// kvstore.cpp:243-314 on the device (K8): gather + mean-merge into a device
+// staging image of all blobs, one D2H into pinned host memory.
+Snapshot* snapshot_compress(Ctx& c, Conv& conv, const krul_pair* pairs, int np, const int64_t* p,
+                            int64_t L, int mode) {
+  if (mode != KRUL_MERGE_MEAN && mode != KRUL_MERGE_KEEP_DEEPER) fail(KRUL_E_CONFIG, "unknown merge mode");
+  if (conv.len != L) fail(KRUL_E_SNAPSHOT, "cache span does not cover the plan's history");
+  std::unique_ptr<Snapshot> s(new_snapshot(c, pairs, np, p, L, mode));
+  layout_blobs(c, *s);
+  KB_CUDA(cudaSetDevice(c.device));
+  cudaStream_t st = c.s_load;
+  char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(s->total, 256)));
+  for (const auto& b : s->blobs) {
+    const bool pair = b.owners[1] >= 0;
+    const int deep = pair ? b.owners[1] : b.owners[0];
+    const int shallow = pair && mode == KRUL_MERGE_MEAN ? b.owners[0] : -1;
+    const int64_t merge_from = pair ? p[b.owners[0]] : L;
+    launch_compress(c, st, conv, deep, shallow, b.start, L, merge_from, stg + b.off);
+  }
+  if (s->total) KB_CUDA(cudaMemcpyAsync(s->host.p, stg, s->total, cudaMemcpyDeviceToHost, st));
+  KB_CUDA(cudaStreamSynchronize(st));
+  return s.release();
+}
+
+Snapshot* snapshot_from_host(Ctx& c, const krul_pair* pairs, int np, const int64_t* p, int64_t L,
+                             int mode, const float* const* k, const float* const* v) {
+  std::unique_ptr<Snapshot> s(new_snapshot(c, pairs, np, p, L, mode));
+  layout_blobs(c, *s);
+  for (size_t bi = 0; bi < s->blobs.size(); ++bi) {
+    const auto& b = s->blobs[bi];
+    const size_t n = size_t(c.cfg.Hkv) * size_t(b.end - b.start) * c.cfg.hd;
+    char* dst = static_cast<char*>(s->host.p) + b.off;
+    for (int kv = 0; kv < 2; ++kv) {
+      const float* src = kv == 0 ? k[bi] : v[bi];
+      if (c.esz == 4) {
+        std::memcpy(dst + kv * n * 4, src, n * 4);
+      } else {
+        uint16_t* o = reinterpret_cast<uint16_t*>(dst) + kv * n;
+        for (size_t i = 0; i < n; ++i) o[i] = f32_to_bf16(src[i]);
+      }
+    }
+  }
+  return s.release();
+}
+
+void snapshot_blob_f32(const Snapshot& s, int b, int64_t row0, int64_t rows, float* k, float* v) {
+  const auto& bl = s.blobs[size_t(b)];
+  const int64_t brows = bl.end - bl.start;
+  const size_t esz = s.ctx->esz;
+  const char* base = static_cast<const char*>(s.host.p) + bl.off;
+  for (int kv = 0; kv < 2; ++kv) {
+    float* out = kv == 0 ? k : v;
+    if (!out) continue;
+    for (int g = 0; g < s.Hkv; ++g)
+      for (int64_t r = 0; r < rows; ++r)
+        for (int t = 0; t < s.hd; ++t) {
+          const size_t src = ((size_t(kv) * s.Hkv + g) * size_t(brows) + size_t(row0 + r)) * s.hd + t;
+          const size_t dst = (size_t(g) * size_t(rows) + size_t(r)) * s.hd + t;
+          out[dst] = esz == 4 ? reinterpret_cast<const float*>(base)[src]
+                              : bf16_to_f32(reinterpret_cast<const uint16_t*>(base)[src]);
+        }
+  }
+}
+
+// kvstore.cpp:316-343 (host view of the pinned store).
+void snapshot_expand(const Snapshot& s, int layer, float* k, float* v, int64_t* start,
+                     int64_t* end) {
+  int found = -1;
+  for (size_t b = 0; b < s.blobs.size() && found < 0; ++b)
+    if (s.blobs[b].owners[0] == layer || (s.blobs[b].owners[1] == layer && layer >= 0))
+      found = int(b);
+  if (found < 0)
+    fail(KRUL_E_RESTORATION_GAP, "layer " + std::to_string(layer) + " is not covered by any stored blob");
+  const auto& bl = s.blobs[size_t(found)];
+  const int64_t ws = s.p[size_t(layer)], we = s.L;
+  if (ws < bl.start || we != bl.end) fail(KRUL_E_RESTORATION_GAP, "stored span does not cover the load span");
+  *start = ws;
+  *end = we;
+  snapshot_blob_f32(s, found, ws - bl.start, we - ws, k, v);
+}
+
+// scheduler.cpp:320-336 checks, then the DAG.
+void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
+             krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
+             double* ttft_ms) {
+  const Cfg& g = c.cfg;
+  if (snap.config_hash != config_hash(g)) fail(KRUL_E_SNAPSHOT, "snapshot was taken under a different model config");
+  if (L != snap.L) fail(KRUL_E_RESTORATION_GAP, "history length does not match the snapshot");
+  const std::vector<int64_t>& p = snap.p;
+  const int m = validate_plan_snapshot(p, L, snap);
+  if (m) {
+    const int base = validate_plan(L, p, snap.pairs.data(), int(snap.pairs.size()));
+    if (base & 7) fail(KRUL_E_PLAN_INVALID, "plan violation (bounds/monotonicity)");
+    if (base & 8) fail(KRUL_E_RESTORATION_GAP, "coverage: pair blob span misses the shallow member's load span");
+    fail(KRUL_E_RESTORATION_GAP, "coverage: stored span does not cover its load span");
+  }
+  check_tokens(c, hist, L);
+  if (new_tok) {
+    if (n_new <= 0) fail(KRUL_E_RESTORATION_GAP, "prefill over preloaded history requires new input tokens");
+    check_tokens(c, new_tok, n_new);
+  }
+  if (L + std::max<int64_t>(n_new, 0) > conv.capacity) fail(KRUL_E_CONFIG, "history exceeds the conversation capacity");
+  KB_CUDA(cudaSetDevice(c.device));
+
+  c.reset_events();
+  cudaEvent_t ev0 = c.event(), ev_c_end = c.event(), ev_l_end = c.event(), ev_end = c.event();
+  std::vector<cudaEvent_t> computed(size_t(g.N)), loaded(size_t(g.N));
+  for (auto& e : computed) e = c.event();
+  for (auto& e : loaded) e = c.event();
+
+  cudaStream_t sc = c.s_comp, sl = c.s_load;
+  char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(snap.total, 256)));
+  // tokens of the recomputed prefix (pinned bounce keeps the copy async)
+  int32_t* d_tok = upload_tokens(c, sc, hist, std::max<int64_t>(p[0], 0), c.ws_tok);
+  float* d_logits = static_cast<float*>(c.ws_logits.ensure(size_t(g.V) * 4));
+  int32_t* d_new = nullptr;
+
+  KB_CUDA(cudaEventRecord(ev0, sc));
+  KB_CUDA(cudaStreamWaitEvent(sl, ev0, 0));
+  // ---- load stream: K4 (H2D) + K5 (expand) per blob in service order
+  double h2d = 0, expand_bytes = 0;
+  for (const auto& b : snap.blobs) {
+    if (b.bytes) {
+      KB_CUDA(cudaMemcpyAsync(stg + b.off, static_cast<char*>(snap.host.p) + b.off, b.bytes,
+                              cudaMemcpyHostToDevice, sl));
+      h2d += double(b.bytes);
+    }
+    for (int o : b.owners) {
+      if (o < 0) continue;
+      launch_expand(c, sl, stg + b.off, b.start, L, conv, o, p[size_t(o)]);
+      expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;
+      KB_CUDA(cudaEventRecord(loaded[size_t(o)], sl));
+    }
+  }
+  KB_CUDA(cudaEventRecord(ev_l_end, sl));
+  // ---- compute stream: K6 pyramid recompute
+  if (p[0] > 0) {
+    enqueue_partial(c, sc, conv, d_tok, p, false, computed.data());
+  } else {
+    for (auto& e : computed) KB_CUDA(cudaEventRecord(e, sc));
+  }
+  KB_CUDA(cudaEventRecord(ev_c_end, sc));
+  // ---- new-input prefill (K7) layer-wise behind both streams
+  if (new_tok) {
+    cudaStream_t sn = c.s_new;
+    KB_CUDA(cudaStreamWaitEvent(sn, ev0, 0));
+    d_new = upload_tokens(c, sn, new_tok, n_new, c.ws_tok2);
+    std::vector<cudaEvent_t> waits;
+    waits.insert(waits.end(), computed.begin(), computed.end());
+    waits.insert(waits.end(), loaded.begin(), loaded.end());
+    conv.len = L;
+    forward_rows(c, sn, 1, conv, d_new, n_new, L, d_logits, &waits);
+    KB_CUDA(cudaEventRecord(ev_end, sn));
+    KB_CUDA(cudaStreamWaitEvent(sc, ev_end, 0));
+    KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end, 0));
+    conv.len = L + n_new;
+  } else {
+    KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end, 0));
+    KB_CUDA(cudaEventRecord(ev_end, sc));
+    conv.len = L;
+  }
+  if (logits && new_tok)
+    KB_CUDA(cudaMemcpyAsync(logits, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sc));
+  KB_CUDA(cudaStreamSynchronize(sc));
+  KB_CUDA(cudaStreamSynchronize(sl));
+
+  float tc = 0, tl = 0, te = 0;
+  KB_CUDA(cudaEventElapsedTime(&tc, ev0, ev_c_end));
+  KB_CUDA(cudaEventElapsedTime(&tl, ev0, ev_l_end));
+  KB_CUDA(cudaEventElapsedTime(&te, ev0, ev_end));
+  if (ttft_ms) *ttft_ms = te;
+  if (st) {
+    Cost cm;
+    cm.kv_dim = g.kvd();
+    cm.q_dim = g.qd();
+    cm.ffn_hidden = g.F;
+    cm.ffn_kind = g.ffn_kind;
+    cm.bpe = double(c.esz);
+    double fl = 0;
+    for (int64_t x : p) fl += cm.layer_flops(x, g.d);
+    const double mk = std::max(tc, tl);
+    st->compute_ms = tc;
+    st->load_ms = tl;
+    st->restore_ms = mk;
+    st->bubble_compute = mk > 0 && p[0] > 0 ? (mk - tc) / mk : 0.0;
+    st->bubble_load = mk > 0 && h2d > 0 ? (mk - tl) / mk : 0.0;
+    st->h2d_bytes = h2d;
+    st->expand_bytes = expand_bytes;
+    st->recompute_flops = fl;
+  }
+}
+
+}  // namespace kb

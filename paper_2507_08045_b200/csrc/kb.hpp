@@ -1,0 +1,226 @@
+// kb.hpp — internal types of the B200 Krul library (not part of the ABI).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/krul_b200.h"
+
+namespace kb {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+
+#define KB_CUDA(x)                                                           \
+  do {                                                                       \
+    cudaError_t e_ = (x);                                                    \
+    if (e_ != cudaSuccess)                                                   \
+      ::kb::fail(KRUL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define KB_LAUNCH() KB_CUDA(cudaGetLastError())
+
+constexpr int kPageTokens = 64;  // tokens per KV page
+
+// Model configuration (engine.hpp:17-29 + extensions).
+struct Cfg {
+  int N = 0, H = 0, Hkv = 0, hd = 0, d = 0, V = 0, F = 0;
+  float ffn_mult = 4.f;
+  int ffn_kind = 0;
+  uint64_t seed = 0;
+  double theta = 1e4;
+  int dtype = KRUL_F32;
+  int64_t max_tokens = 0;
+  int qd() const { return H * hd; }
+  int kvd() const { return Hkv * hd; }
+  int nqkv() const { return (H + 2 * Hkv) * hd; }
+};
+Cfg cfg_from_desc(const krul_model_desc& d);
+uint64_t config_hash(const Cfg& c);  // engine.cpp:27-36 (+ extension fold)
+
+// Owning device allocation that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+  void* ensure(size_t n);  // grows (contents not preserved)
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf();
+  void* ensure(size_t n);
+};
+
+// Per-layer device weights, compute dtype (f32 or bf16). All projection
+// matrices are stored transposed ([out][in], K-major) for the GEMM's B
+// operand. SwiGLU gate/up rows are interleaved in 64-row blocks.
+struct LayerW {
+  void* wqkv = nullptr;  // [(H + 2 Hkv) hd][d]
+  void* wo = nullptr;    // [d][H hd]
+  void* w1 = nullptr;    // tanh: [F][d]; swiglu: [2F][d] interleaved
+  void* w2 = nullptr;    // [d][F]
+  float* b1 = nullptr;   // [F] (tanh only)
+  float* b2 = nullptr;   // [d] (tanh only)
+};
+
+struct Ctx;
+
+// A conversation: page table into the ctx KV pool plus its length.
+struct Conv {
+  Ctx* ctx = nullptr;
+  int64_t len = 0;
+  int64_t capacity = 0;
+  int max_pages = 0;
+  std::vector<int> pages;  // host copy [N][max_pages]
+  int* d_pt = nullptr;     // device page table [N][max_pages]
+  ~Conv();
+};
+
+struct Est;
+
+struct Ctx {
+  int device = 0;
+  Cfg cfg;
+  size_t esz = 4;  // compute element size
+  cudaStream_t s_comp = nullptr, s_load = nullptr, s_new = nullptr, s_est = nullptr;
+  int sm_count = 0;
+
+  // weights
+  DevBuf wbuf;  // one arena
+  std::vector<LayerW> L;
+  void* embed = nullptr;     // [V][d]
+  void* unembedT = nullptr;  // [V][d]
+  float* rope_cos = nullptr; // [max_tokens][hd/2] (host double -> float)
+  float* rope_sin = nullptr;
+  DevBuf rope;
+  bool weights_ready = false;
+
+  // KV page pool: page = [K: Hkv][P][hd] then [V^T: Hkv][hd][P]
+  DevBuf pool;
+  int pool_pages = 0;
+  std::vector<int> free_pages;
+  size_t page_elems() const { return size_t(2) * cfg.Hkv * kPageTokens * cfg.hd; }
+
+  // workspaces (grown on demand)
+  DevBuf ws_h, ws_h2, ws_xn, ws_qkv, ws_q, ws_attn, ws_hmid, ws_hmidc, ws_act, ws_y;
+  DevBuf ws_tok, ws_tok2, ws_logits;
+  DevBuf ws_new_h, ws_new_h2;  // new-input prefill stream
+  // second workspace set for the concurrent new-input prefill stream
+  DevBuf ws2_xn, ws2_qkv, ws2_q, ws2_attn, ws2_hmid, ws2_hmidc, ws2_act, ws2_y;
+
+  // capture
+  int capture_probs = 0;
+  DevBuf cap_probs;       // [N][H][rows][W] f32 (when capture_probs)
+  int64_t cap_rows = 0, cap_width = 0, cap_first_q = 0;
+  bool cap_valid = false;
+  DevBuf cap_mass;        // [N][H][rows] f64 region masses (classifier)
+  double cap_ifrac = 0.1, cap_rfrac = 0.1;
+  int64_t cap_il = 0, cap_rs = 0;
+  DevBuf dec_rows;        // [N][H][W] f32 last decode step
+  int64_t dec_width = 0;
+  bool dec_valid = false;
+
+  // restore staging
+  DevBuf staging;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+
+  ~Ctx();
+  cudaEvent_t event();  // recycled timing-capable events
+  void reset_events() { ev_next = 0; }
+};
+
+// ---- kernels (launch wrappers, .cu) ---------------------------------------
+struct Epi {  // GEMM epilogue
+  enum Kind { F32 = 0, CDT = 1, RESID = 2, TANH = 3, SWIGLU = 4 };
+  int kind = F32;
+  void* out = nullptr;        // F32/RESID: float*, CDT/TANH/SWIGLU: cdt*
+  int64_t ldo = 0;
+  const float* bias = nullptr;
+  const float* resid = nullptr;  // RESID: out = acc + bias + resid
+  int64_t ldr = 0;
+  void* out2 = nullptr;          // RESID: optional cdt copy of out
+  int64_t ldo2 = 0;
+};
+
+// C = A[M,K] * B[N,K]^T with epilogue; A,B in compute dtype.
+void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K,
+          const void* A, int64_t lda, const void* B, int64_t ldb, const Epi& e);
+
+void launch_embed(const Ctx& c, cudaStream_t s, const int32_t* tok, int64_t n, float* h);
+void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, void* xn);
+// qkv f32 [rows][(H+2Hkv)hd] -> rope, K/V^T into pages at [pos0, pos0+rows),
+// Q (roped, cdt) for rows < q_rows.
+void launch_rope_scatter(const Ctx& c, cudaStream_t s, const float* qkv, int64_t rows,
+                         int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer);
+struct AttnArgs {
+  const void* q = nullptr;  // [rows][H*hd] cdt
+  int64_t rows = 0, pos0 = 0;
+  void* out = nullptr;      // [rows][H*hd] cdt
+  float* probs = nullptr;   // optional [H][rows][ld_probs]
+  int64_t ld_probs = 0;
+  int64_t probs_row0 = 0;   // row offset into the capture
+  int64_t probs_rows = 0;   // rows per head in the capture
+  double* mass = nullptr;   // optional [H][mass_rows] region mass
+  int64_t mass_rows = 0;
+  int64_t il = 0, rs = 0;   // classifier regions [0,il) U [rs, W)
+};
+void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
+                      const AttnArgs& a);
+void launch_bias_act(const Ctx& c, cudaStream_t s, const float* in, int64_t rows, int64_t F,
+                     const float* b1, int kind, void* out);  // tanh(x+b) or swiglu pairs
+void launch_resid_add(const Ctx& c, cudaStream_t s, const float* y, const float* bias,
+                      const float* resid, int64_t rows, int64_t d, float* out, void* outc);
+void launch_logits(const Ctx& c, cudaStream_t s, const float* h_last, float* logits);
+void launch_convert_weights(const Ctx& c, cudaStream_t s, const float* src, void* dst,
+                            int64_t rows, int64_t cols, int transpose, int interleave64);
+void launch_init_uniform(const Ctx& c, cudaStream_t s, void* dst, int64_t n, uint64_t seed,
+                         uint64_t stream_id, float bound);
+void launch_init_uniform_f32(cudaStream_t s, float* dst, int64_t n, uint64_t seed,
+                             uint64_t stream_id, float bound);
+
+// KV page transfer helpers (f32 host views)
+void launch_kv_gather(const Ctx& c, cudaStream_t s, const Conv& conv, int layer, int64_t start,
+                      int64_t end, float* k, float* v);  // -> [Hkv][rows][hd] f32 device
+void launch_kv_scatter_f32(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
+                           int64_t start, int64_t end, const float* k, const float* v);
+// Blob (cdt [2][Hkv][rows][hd], rows = [blob_start, L)) -> pages of `layer`
+// for positions [from, L).
+void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start,
+                   int64_t L, const Conv& conv, int layer, int64_t from);
+// Pages -> blob (compress, K8); mean-merge rows [merge_from, L) with `other`.
+void launch_compress(const Ctx& c, cudaStream_t s, const Conv& conv, int deep, int shallow,
+                     int64_t blob_start, int64_t L, int64_t merge_from, void* blob);
+void launch_cvt_to_f32(const Ctx& c, cudaStream_t s, const void* src, float* dst, int64_t n);
+void launch_cvt_from_f32(const Ctx& c, cudaStream_t s, const float* src, void* dst, int64_t n);
+
+// estimator kernels
+void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, const int* d_layers,
+                        int n, double* sums, double* partial, int64_t partial_cap);
+void launch_fold_prefill(cudaStream_t s, const float* probs, int64_t rows, int64_t W, int H,
+                         const int* d_layers, int n, double* sums, double* partial,
+                         int64_t partial_cap);
+void launch_finalize(cudaStream_t s, const double* sums, int n, int H, double* D);
+// selector: candidates sorted on device then greedily matched
+void launch_select(cudaStream_t s, const double* cand_d, const int* cand_i, const int* cand_j,
+                   int n_cand, int quota, int* out_i, int* out_j, double* out_d, int* out_n);
+
+}  // namespace kb

@@ -1,0 +1,715 @@
+// kernels.cu — elementwise, attention, KV paging, estimator and selector
+// kernels of the B200 Krul hot path. Templated on the compute dtype T
+// (float = parity mode, __nv_bfloat16 = perf mode). GEMMs live in
+// gemm_simt.cu / gemm_sm100.cu.
+#include <cfloat>
+#include <cmath>
+
+#include "kb.hpp"
+#include "dev.cuh"
+
+namespace kb {
+
+// ---------------------------------------------------------------- embed
+// engine.cpp:195-207 (token range is validated on the host first).
+template <class T>
+__global__ void k_embed(const int32_t* tok, int64_t n, const T* emb, int d, float* h) {
+  const int64_t r = blockIdx.x;
+  const T* src = emb + int64_t(tok[r]) * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) h[r * d + j] = tof(src[j]);
+}
+void launch_embed(const Ctx& c, cudaStream_t s, const int32_t* tok, int64_t n, float* h) {
+  if (n <= 0) return;
+  if (c.cfg.dtype == KRUL_BF16)
+    k_embed<<<unsigned(n), 256, 0, s>>>(tok, n, (const bf16*)c.embed, c.cfg.d, h);
+  else
+    k_embed<<<unsigned(n), 256, 0, s>>>(tok, n, (const float*)c.embed, c.cfg.d, h);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- rmsnorm
+// engine.cpp:117-124: xn = x / sqrt(mean(x^2) + 1e-6), no gain.
+template <class T>
+__global__ void k_rmsnorm(const float* h, int d, T* out) {
+  const int64_t r = blockIdx.x;
+  const float* x = h + r * d;
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) ss += x[j] * x[j];
+  ss = block_sum(ss);
+  const float denom = sqrtf(ss / float(d) + 1e-6f);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) out[r * d + j] = fromf<T>(x[j] / denom);
+}
+void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, void* xn) {
+  if (rows <= 0) return;
+  if (c.cfg.dtype == KRUL_BF16)
+    k_rmsnorm<<<unsigned(rows), 256, 0, s>>>(h, c.cfg.d, (bf16*)xn);
+  else
+    k_rmsnorm<<<unsigned(rows), 256, 0, s>>>(h, c.cfg.d, (float*)xn);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- paging
+struct PageView {
+  const int* pt;   // [max_pages] for one layer
+  char* pool;
+  int64_t page_bytes;
+  int Hkv, hd, esz;
+  __device__ __forceinline__ char* page(int64_t pos) const {
+    return pool + int64_t(pt[pos / kPageTokens]) * page_bytes;
+  }
+  // element offsets inside a page
+  __device__ __forceinline__ int64_t k_off(int g, int64_t pos, int t) const {
+    return (int64_t(g) * kPageTokens + pos % kPageTokens) * hd + t;
+  }
+  __device__ __forceinline__ int64_t v_off(int g, int64_t pos, int t) const {  // V^T
+    return int64_t(Hkv) * kPageTokens * hd + (int64_t(g) * hd + t) * kPageTokens + pos % kPageTokens;
+  }
+};
+static PageView page_view(const Ctx& c, const Conv& conv, int layer) {
+  PageView v;
+  v.pt = conv.d_pt + int64_t(layer) * conv.max_pages;
+  v.pool = static_cast<char*>(c.pool.p);
+  v.page_bytes = int64_t(c.page_elems() * c.esz);
+  v.Hkv = c.cfg.Hkv;
+  v.hd = c.cfg.hd;
+  v.esz = int(c.esz);
+  return v;
+}
+
+// ---------------------------------------------------------------- rope + scatter
+// engine.cpp:128-143 (interleaved pairs, odd trailing dim passes through) and
+// :162-170 (K/V of every block row appended before attention).
+template <class T>
+__global__ void k_rope_scatter(const float* qkv, int64_t pos0, int64_t q_rows, T* q, PageView pv,
+                               const float* cosT, const float* sinT, int H) {
+  const int64_t r = blockIdx.x;
+  const int hd = pv.hd, Hkv = pv.Hkv, half = hd / 2;
+  const int64_t pos = pos0 + r;
+  const int nq = H * hd, nkv = Hkv * hd;
+  const float* row = qkv + r * int64_t(nq + 2 * nkv);
+  const float* cs = cosT + pos * half;
+  const float* sn = sinT + pos * half;
+  T* page = reinterpret_cast<T*>(pv.page(pos));
+  // rotate Q (only the leading q_rows rows need Q)
+  if (r < q_rows) {
+    for (int e = threadIdx.x; e < nq; e += blockDim.x) {
+      const int t = e % hd;
+      float y;
+      if (t < 2 * half) {
+        const int i = t >> 1;
+        const float x0 = row[e - (t & 1)], x1 = row[e - (t & 1) + 1];
+        y = (t & 1) ? (x0 * sn[i] + x1 * cs[i]) : (x0 * cs[i] - x1 * sn[i]);
+      } else {
+        y = row[e];
+      }
+      q[r * nq + e] = fromf<T>(y);
+    }
+  }
+  for (int e = threadIdx.x; e < nkv; e += blockDim.x) {
+    const int g = e / hd, t = e % hd;
+    const float* kr = row + nq;
+    float y;
+    if (t < 2 * half) {
+      const int i = t >> 1;
+      const float x0 = kr[e - (t & 1)], x1 = kr[e - (t & 1) + 1];
+      y = (t & 1) ? (x0 * sn[i] + x1 * cs[i]) : (x0 * cs[i] - x1 * sn[i]);
+    } else {
+      y = kr[e];
+    }
+    page[pv.k_off(g, pos, t)] = fromf<T>(y);
+    page[pv.v_off(g, pos, t)] = fromf<T>(row[nq + nkv + e]);
+  }
+}
+void launch_rope_scatter(const Ctx& c, cudaStream_t s, const float* qkv, int64_t rows,
+                         int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer) {
+  if (rows <= 0) return;
+  PageView pv = page_view(c, conv, layer);
+  if (c.cfg.dtype == KRUL_BF16)
+    k_rope_scatter<<<unsigned(rows), 128, 0, s>>>(qkv, pos0, q_rows, (bf16*)q, pv, c.rope_cos,
+                                                  c.rope_sin, c.cfg.H);
+  else
+    k_rope_scatter<<<unsigned(rows), 128, 0, s>>>(qkv, pos0, q_rows, (float*)q, pv, c.rope_cos,
+                                                  c.rope_sin, c.cfg.H);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- attention (SIMT)
+// engine.cpp:174-188: per head, scores = q K^T * (1/sqrt(hd)), causal width
+// pos0 + r + 1, softmax with max subtraction, ctx = P V. One CTA per
+// (row, head); the score row lives in shared memory. Optionally emits the
+// normalised probabilities (capture) and the classifier region mass
+// (analysis.cpp:46-54) accumulated in double.
+template <class T>
+__global__ void k_attn_simt(const T* q, int64_t pos0, PageView pv, int H, float scale, T* out,
+                            float* probs, int64_t ld_probs, int64_t probs_row0, int64_t probs_rows,
+                            double* mass, int64_t mass_rows, int64_t il, int64_t rs) {
+  extern __shared__ float sm[];
+  const int64_t r = blockIdx.x;
+  const int h = blockIdx.y;
+  const int hd = pv.hd;
+  const int g = h / (H / pv.Hkv);
+  const int64_t W = pos0 + r + 1;
+  float* qs = sm;            // [hd]
+  float* sc = sm + hd;       // [W]
+  for (int t = threadIdx.x; t < hd; t += blockDim.x) qs[t] = tof(q[(r * H + h) * hd + t]);
+  __syncthreads();
+  float mx = -FLT_MAX;
+  for (int64_t k = threadIdx.x; k < W; k += blockDim.x) {
+    const T* kr = reinterpret_cast<const T*>(pv.page(k)) + pv.k_off(g, k, 0);
+    float dot = 0.f;
+    for (int t = 0; t < hd; ++t) dot += qs[t] * tof(kr[t]);
+    const float sv = dot * scale;
+    sc[k] = sv;
+    mx = fmaxf(mx, sv);
+  }
+  mx = block_max(mx);
+  float sum = 0.f;
+  for (int64_t k = threadIdx.x; k < W; k += blockDim.x) {
+    const float e = expf(sc[k] - mx);
+    sc[k] = e;
+    sum += e;
+  }
+  sum = block_sum(sum);
+  double ms = 0.0;
+  for (int64_t k = threadIdx.x; k < W; k += blockDim.x) {
+    const float p = sc[k] / sum;
+    sc[k] = p;
+    if (probs) probs[(int64_t(h) * probs_rows + probs_row0 + r) * ld_probs + k] = p;
+    if (mass && (k < il || k >= rs)) ms += double(p);
+  }
+  if (mass) {
+    ms = block_sum_d(ms);
+    if (threadIdx.x == 0) mass[int64_t(h) * mass_rows + probs_row0 + r] = ms;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < hd; t += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t k = 0; k < W; ++k) {
+      const T* vr = reinterpret_cast<const T*>(pv.page(k));
+      acc += sc[k] * tof(vr[pv.v_off(g, k, t)]);
+    }
+    out[(r * H + h) * hd + t] = fromf<T>(acc);
+  }
+}
+
+void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
+                      const AttnArgs& a) {
+  if (a.rows <= 0) return;
+  PageView pv = page_view(c, conv, layer);
+  const float scale = 1.0f / sqrtf(float(c.cfg.hd));
+  const size_t smem = sizeof(float) * size_t(c.cfg.hd + a.pos0 + a.rows);
+  dim3 grid(unsigned(a.rows), unsigned(c.cfg.H));
+  if (c.cfg.dtype == KRUL_BF16) {
+    auto k = k_attn_simt<bf16>;
+    KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    k<<<grid, 128, smem, s>>>((const bf16*)a.q, a.pos0, pv, c.cfg.H, scale, (bf16*)a.out, a.probs,
+                              a.ld_probs, a.probs_row0, a.probs_rows, a.mass, a.mass_rows, a.il,
+                              a.rs);
+  } else {
+    auto k = k_attn_simt<float>;
+    KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    k<<<grid, 128, smem, s>>>((const float*)a.q, a.pos0, pv, c.cfg.H, scale, (float*)a.out,
+                              a.probs, a.ld_probs, a.probs_row0, a.probs_rows, a.mass,
+                              a.mass_rows, a.il, a.rs);
+  }
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- FFN pieces (SIMT path)
+template <class T>
+__global__ void k_bias_act(const float* in, int64_t rows, int64_t F, const float* b1, int kind,
+                           T* out) {
+  const int64_t n = rows * F;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / F, j = i % F;
+    float y;
+    if (kind == 0) {
+      y = tanhf(in[i] + b1[j]);  // engine.cpp:191
+    } else {  // gate/up interleaved per column pair
+      const float g = in[r * 2 * F + 2 * j], u = in[r * 2 * F + 2 * j + 1];
+      y = g / (1.0f + expf(-g)) * u;
+    }
+    out[i] = fromf<T>(y);
+  }
+}
+void launch_bias_act(const Ctx& c, cudaStream_t s, const float* in, int64_t rows, int64_t F,
+                     const float* b1, int kind, void* out) {
+  if (rows <= 0) return;
+  const unsigned blocks = unsigned(std::min<int64_t>((rows * F + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16)
+    k_bias_act<<<blocks, 256, 0, s>>>(in, rows, F, b1, kind, (bf16*)out);
+  else
+    k_bias_act<<<blocks, 256, 0, s>>>(in, rows, F, b1, kind, (float*)out);
+  KB_LAUNCH();
+}
+
+template <class T>
+__global__ void k_resid_add(const float* y, const float* bias, const float* resid, int64_t rows,
+                            int64_t d, float* out, T* outc) {
+  const int64_t n = rows * d;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float v = resid[i] + (bias ? y[i] + bias[i % d] : y[i]);
+    out[i] = v;
+    if (outc) outc[i] = fromf<T>(v);
+  }
+}
+void launch_resid_add(const Ctx& c, cudaStream_t s, const float* y, const float* bias,
+                      const float* resid, int64_t rows, int64_t d, float* out, void* outc) {
+  if (rows <= 0) return;
+  const unsigned blocks = unsigned(std::min<int64_t>((rows * d + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16)
+    k_resid_add<<<blocks, 256, 0, s>>>(y, bias, resid, rows, d, out, (bf16*)outc);
+  else
+    k_resid_add<<<blocks, 256, 0, s>>>(y, bias, resid, rows, d, out, (float*)outc);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- logits
+// engine.cpp:338 / :444 — last row times the unembedding (stored [V][d]).
+template <class T>
+__global__ void k_logits(const float* h, const T* wT, int d, int V, float* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int v = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (v >= V) return;
+  const T* w = wT + int64_t(v) * d;
+  float acc = 0.f;
+  for (int k = lane; k < d; k += 32) acc += h[k] * tof(w[k]);
+  acc = warp_sum(acc);
+  if (lane == 0) out[v] = acc;
+}
+void launch_logits(const Ctx& c, cudaStream_t s, const float* h_last, float* logits) {
+  const int V = c.cfg.V;
+  const unsigned blocks = unsigned((V + 7) / 8);
+  if (c.cfg.dtype == KRUL_BF16)
+    k_logits<<<blocks, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, c.cfg.d, V, logits);
+  else
+    k_logits<<<blocks, 256, 0, s>>>(h_last, (const float*)c.unembedT, c.cfg.d, V, logits);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- weights
+// dst[(j * rstride + roff)][i] = src[i][j] (transpose) or dst[i][j] = src[i][j]
+template <class T>
+__global__ void k_convert(const float* src, T* dst, int64_t rows, int64_t cols, int transpose,
+                          int64_t rstride, int64_t roff, int64_t dcols) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e % cols;
+    if (transpose)
+      dst[(j * rstride + roff) * dcols + i] = fromf<T>(src[e]);
+    else
+      dst[e] = fromf<T>(src[e]);
+  }
+}
+void launch_convert_weights(const Ctx& c, cudaStream_t s, const float* src, void* dst,
+                            int64_t rows, int64_t cols, int transpose, int interleave) {
+  // interleave: 0 -> plain; 1 -> even rows (gate); 2 -> odd rows (up)
+  const int64_t rstride = interleave ? 2 : 1, roff = interleave == 2 ? 1 : 0;
+  const unsigned blocks = unsigned(std::min<int64_t>((rows * cols + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16)
+    k_convert<<<blocks, 256, 0, s>>>(src, (bf16*)dst, rows, cols, transpose, rstride, roff, rows);
+  else
+    k_convert<<<blocks, 256, 0, s>>>(src, (float*)dst, rows, cols, transpose, rstride, roff, rows);
+  KB_LAUNCH();
+}
+
+// Counter-based uniform in [-bound, bound) (splitmix64 of (seed, stream, i));
+// perf configs only — parity configs upload the reference UniformStream.
+__device__ __forceinline__ float hash_uniform(uint64_t seed, uint64_t stream, uint64_t i) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + stream * 0xD1B54A32D192ED03ull + i;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return float(uint32_t(z >> 40)) * (1.0f / 16777216.0f);
+}
+template <class T>
+__global__ void k_init(T* dst, int64_t n, uint64_t seed, uint64_t stream, float bound) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = fromf<T>(-bound + 2.f * bound * hash_uniform(seed, stream, uint64_t(i)));
+}
+void launch_init_uniform(const Ctx& c, cudaStream_t s, void* dst, int64_t n, uint64_t seed,
+                         uint64_t stream, float bound) {
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 64));
+  if (c.cfg.dtype == KRUL_BF16)
+    k_init<<<blocks, 256, 0, s>>>((bf16*)dst, n, seed, stream, bound);
+  else
+    k_init<<<blocks, 256, 0, s>>>((float*)dst, n, seed, stream, bound);
+  KB_LAUNCH();
+}
+void launch_init_uniform_f32(cudaStream_t s, float* dst, int64_t n, uint64_t seed,
+                             uint64_t stream, float bound) {
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 64));
+  k_init<<<blocks, 256, 0, s>>>(dst, n, seed, stream, bound);
+  KB_LAUNCH();
+}
+
+template <class S, class D>
+__global__ void k_cvt(const S* src, D* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = fromf<D>(tof(src[i]));
+}
+void launch_cvt_to_f32(const Ctx& c, cudaStream_t s, const void* src, float* dst, int64_t n) {
+  if (n <= 0) return;
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16) k_cvt<<<blocks, 256, 0, s>>>((const bf16*)src, dst, n);
+  else k_cvt<<<blocks, 256, 0, s>>>((const float*)src, dst, n);
+  KB_LAUNCH();
+}
+void launch_cvt_from_f32(const Ctx& c, cudaStream_t s, const float* src, void* dst, int64_t n) {
+  if (n <= 0) return;
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16) k_cvt<<<blocks, 256, 0, s>>>(src, (bf16*)dst, n);
+  else k_cvt<<<blocks, 256, 0, s>>>(src, (float*)dst, n);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- KV <-> f32 views
+template <class T>
+__global__ void k_kv_gather(PageView pv, int64_t start, int64_t rows, float* k, float* v) {
+  const int64_t n = int64_t(pv.Hkv) * rows * pv.hd;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int t = int(e % pv.hd);
+    const int64_t r = (e / pv.hd) % rows;
+    const int g = int(e / (int64_t(pv.hd) * rows));
+    const int64_t pos = start + r;
+    const T* page = reinterpret_cast<const T*>(pv.page(pos));
+    k[e] = tof(page[pv.k_off(g, pos, t)]);
+    v[e] = tof(page[pv.v_off(g, pos, t)]);
+  }
+}
+template <class T>
+__global__ void k_kv_scatter(PageView pv, int64_t start, int64_t rows, const float* k,
+                             const float* v) {
+  const int64_t n = int64_t(pv.Hkv) * rows * pv.hd;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int t = int(e % pv.hd);
+    const int64_t r = (e / pv.hd) % rows;
+    const int g = int(e / (int64_t(pv.hd) * rows));
+    const int64_t pos = start + r;
+    T* page = reinterpret_cast<T*>(pv.page(pos));
+    page[pv.k_off(g, pos, t)] = fromf<T>(k[e]);
+    page[pv.v_off(g, pos, t)] = fromf<T>(v[e]);
+  }
+}
+void launch_kv_gather(const Ctx& c, cudaStream_t s, const Conv& conv, int layer, int64_t start,
+                      int64_t end, float* k, float* v) {
+  const int64_t rows = end - start;
+  if (rows <= 0) return;
+  PageView pv = page_view(c, conv, layer);
+  const unsigned blocks = unsigned(std::min<int64_t>((rows * pv.Hkv * pv.hd + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16) k_kv_gather<bf16><<<blocks, 256, 0, s>>>(pv, start, rows, k, v);
+  else k_kv_gather<float><<<blocks, 256, 0, s>>>(pv, start, rows, k, v);
+  KB_LAUNCH();
+}
+void launch_kv_scatter_f32(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
+                           int64_t start, int64_t end, const float* k, const float* v) {
+  const int64_t rows = end - start;
+  if (rows <= 0) return;
+  PageView pv = page_view(c, conv, layer);
+  const unsigned blocks = unsigned(std::min<int64_t>((rows * pv.Hkv * pv.hd + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16) k_kv_scatter<bf16><<<blocks, 256, 0, s>>>(pv, start, rows, k, v);
+  else k_kv_scatter<float><<<blocks, 256, 0, s>>>(pv, start, rows, k, v);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- expand (K5)
+// kvstore.cpp:316-343 + the splice of scheduler.cpp:368-393: a staged blob
+// [K: Hkv][rows][hd] [V: Hkv][rows][hd] covering [blob_start, L) is written
+// into `layer`'s pages for positions [from, L). One CTA per (page tile,
+// kv head): K rows copy with 16-byte vectors; V is transposed through shared
+// memory into the page's V^T block so PV reads stay K-major.
+template <class T>
+__global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView pv,
+                         int64_t from) {
+  extern __shared__ unsigned char smraw[];
+  T* tile = reinterpret_cast<T*>(smraw);  // [kPageTokens][hd + pad]
+  const int hd = pv.hd, Hkv = pv.Hkv;
+  const int g = blockIdx.y;
+  const int64_t p0 = (from / kPageTokens + blockIdx.x) * kPageTokens;
+  const int64_t lo = p0 > from ? p0 : from, hi = p0 + kPageTokens < L ? p0 + kPageTokens : L;
+  if (lo >= hi) return;
+  const int64_t rows_blob = L - blob_start;
+  const T* kb = blob + (int64_t(g) * rows_blob) * hd;
+  const T* vb = blob + (int64_t(Hkv + g) * rows_blob) * hd;
+  T* page = reinterpret_cast<T*>(pv.page(lo));
+  const int n = int(hi - lo);
+  const int ldt = hd + 8;
+  // K: straight row copy (contiguous [rows][hd] on both sides)
+  const int64_t krow0 = lo - blob_start;
+  T* kdst = page + pv.k_off(g, lo, 0);
+  const int elems = n * hd;
+  if ((hd * int(sizeof(T))) % 16 == 0) {
+    const int vec = 16 / int(sizeof(T));
+    const int4* src = reinterpret_cast<const int4*>(kb + krow0 * hd);
+    int4* dst = reinterpret_cast<int4*>(kdst);
+    for (int i = threadIdx.x; i < elems / vec; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (int i = threadIdx.x; i < elems; i += blockDim.x) kdst[i] = kb[krow0 * hd + i];
+  }
+  // V: stage [n][hd] then write V^T [hd][pos%P]
+  for (int i = threadIdx.x; i < elems; i += blockDim.x) {
+    const int r = i / hd, t = i % hd;
+    tile[r * ldt + t] = vb[(krow0 + r) * hd + t];
+  }
+  __syncthreads();
+  const int off = int(lo % kPageTokens);
+  for (int i = threadIdx.x; i < hd * n; i += blockDim.x) {
+    const int t = i / n, r = i % n;
+    page[pv.v_off(g, lo + r, t) - 0] = tile[r * ldt + t];
+  }
+  (void)off;
+}
+void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,
+                   const Conv& conv, int layer, int64_t from) {
+  if (from >= L) return;
+  PageView pv = page_view(c, conv, layer);
+  const int64_t tiles = (L - 1) / kPageTokens - from / kPageTokens + 1;
+  dim3 grid(unsigned(tiles), unsigned(c.cfg.Hkv));
+  const size_t smem = size_t(kPageTokens) * (c.cfg.hd + 8) * c.esz;
+  if (c.cfg.dtype == KRUL_BF16) {
+    KB_CUDA(cudaFuncSetAttribute(k_expand<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    k_expand<bf16><<<grid, 256, smem, s>>>((const bf16*)blob, blob_start, L, pv, from);
+  } else {
+    KB_CUDA(cudaFuncSetAttribute(k_expand<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    k_expand<float><<<grid, 256, smem, s>>>((const float*)blob, blob_start, L, pv, from);
+  }
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- compress (K8)
+// kvstore.cpp:243-314: blob rows = deep member over [blob_start, L); with
+// the mean merge, rows [merge_from, L) become 0.5f * (shallow + deep).
+template <class T>
+__global__ void k_compress(PageView deep, PageView shal, int use_shallow, int64_t blob_start,
+                           int64_t L, int64_t merge_from, T* blob) {
+  const int hd = deep.hd, Hkv = deep.Hkv;
+  const int64_t rows = L - blob_start;
+  const int64_t n = int64_t(Hkv) * rows * hd;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int t = int(e % hd);
+    const int64_t r = (e / hd) % rows;
+    const int g = int(e / (int64_t(hd) * rows));
+    const int64_t pos = blob_start + r;
+    const T* dp = reinterpret_cast<const T*>(deep.page(pos));
+    float k = tof(dp[deep.k_off(g, pos, t)]);
+    float v = tof(dp[deep.v_off(g, pos, t)]);
+    if (use_shallow && pos >= merge_from) {
+      const T* sp = reinterpret_cast<const T*>(shal.page(pos));
+      k = 0.5f * (tof(sp[shal.k_off(g, pos, t)]) + k);
+      v = 0.5f * (tof(sp[shal.v_off(g, pos, t)]) + v);
+    }
+    blob[e] = fromf<T>(k);
+    blob[n + e] = fromf<T>(v);
+  }
+}
+void launch_compress(const Ctx& c, cudaStream_t s, const Conv& conv, int deep, int shallow,
+                     int64_t blob_start, int64_t L, int64_t merge_from, void* blob) {
+  const int64_t rows = L - blob_start;
+  if (rows <= 0) return;
+  PageView dp = page_view(c, conv, deep);
+  PageView sp = page_view(c, conv, shallow >= 0 ? shallow : deep);
+  const unsigned blocks =
+      unsigned(std::min<int64_t>((rows * c.cfg.Hkv * c.cfg.hd + 255) / 256, 65535));
+  if (c.cfg.dtype == KRUL_BF16)
+    k_compress<<<blocks, 256, 0, s>>>(dp, sp, shallow >= 0, blob_start, L, merge_from,
+                                      (bf16*)blob);
+  else
+    k_compress<<<blocks, 256, 0, s>>>(dp, sp, shallow >= 0, blob_start, L, merge_from,
+                                      (float*)blob);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- estimator (K1/K2)
+// Pair p enumerates (a < b) over the sorted tracked layers, as
+// analysis.cpp:84-93. Stage 1: one CTA per (head, column chunk) loads the
+// chunk of every tracked layer's row into shared memory once (coalesced
+// 128-bit loads) and one warp per pair reduces sum((f32 a - f32 b)^2) in
+// double (analysis.cpp:146-147) with warp shuffles. Stage 2 adds the chunk
+// partials in a fixed order (deterministic, no fp atomics).
+constexpr int kFoldChunk = 512;
+__global__ void k_fold_stage1(const float* rows, int64_t layer_stride, int64_t head_stride,
+                              int64_t total, int H, const int* layers, int n, double* partial) {
+  extern __shared__ float fs[];  // [n][kFoldChunk]
+  const int h = blockIdx.y;
+  const int64_t c0 = int64_t(blockIdx.x) * kFoldChunk;
+  const int cw = int(total - c0 < kFoldChunk ? total - c0 : kFoldChunk);
+  for (int a = 0; a < n; ++a) {
+    const float* src = rows + int64_t(layers[a]) * layer_stride + int64_t(h) * head_stride + c0;
+    float* dst = fs + a * kFoldChunk;
+    if ((cw & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+      for (int i = threadIdx.x; i < cw / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+    } else {
+      for (int i = threadIdx.x; i < cw; i += blockDim.x) dst[i] = src[i];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int P = n * (n - 1) / 2;
+  for (int p = warp; p < P; p += nw) {
+    // decode p -> (a, b), a < b
+    int a = 0, rem = p;
+    while (rem >= n - 1 - a) {
+      rem -= n - 1 - a;
+      ++a;
+    }
+    const int b = a + 1 + rem;
+    const float* x = fs + a * kFoldChunk;
+    const float* y = fs + b * kFoldChunk;
+    double acc = 0.0;
+    for (int i = lane; i < cw; i += 32) {
+      const double d = double(x[i] - y[i]);
+      acc += d * d;
+    }
+    acc = warp_sum_d(acc);
+    if (lane == 0) partial[(int64_t(blockIdx.x) * P + p) * H + h] = acc;
+  }
+}
+__global__ void k_fold_stage2(const double* partial, int chunks, int PH, double* sums) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= PH) return;
+  double acc = 0.0;
+  for (int ch = 0; ch < chunks; ++ch) acc += partial[int64_t(ch) * PH + i];
+  sums[i] += acc;
+}
+static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
+                        int64_t head_stride, int64_t total, int H, const int* d_layers, int n,
+                        double* sums, double* partial, int64_t partial_cap) {
+  if (n < 2 || total <= 0) return;
+  const int P = n * (n - 1) / 2;
+  const int chunks = int((total + kFoldChunk - 1) / kFoldChunk);
+  if (int64_t(chunks) * P * H > partial_cap) fail(KRUL_E_CUDA, "fold partial buffer too small");
+  const size_t smem = size_t(n) * kFoldChunk * sizeof(float);
+  KB_CUDA(cudaFuncSetAttribute(k_fold_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  k_fold_stage1<<<dim3(unsigned(chunks), unsigned(H)), 256, smem, s>>>(
+      rows, layer_stride, head_stride, total, H, d_layers, n, partial);
+  KB_LAUNCH();
+  k_fold_stage2<<<unsigned((P * H + 255) / 256), 256, 0, s>>>(partial, chunks, P * H, sums);
+  KB_LAUNCH();
+}
+void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, const int* d_layers,
+                        int n, double* sums, double* partial, int64_t partial_cap) {
+  fold_common(s, rows, int64_t(H) * W, W, W, H, d_layers, n, sums, partial, partial_cap);
+}
+// Prefill fold over the full [rows x W] rectangle per (pair, head): the
+// direct sum of squared differences in double; the reference's expanded
+// a^2 + b^2 - 2ab form (analysis.hpp:37-50) agrees within 1e-12 relative.
+void launch_fold_prefill(cudaStream_t s, const float* probs, int64_t rows, int64_t W, int H,
+                         const int* d_layers, int n, double* sums, double* partial,
+                         int64_t partial_cap) {
+  fold_common(s, probs, int64_t(H) * rows * W, rows * W, rows * W, H, d_layers, n, sums, partial,
+              partial_cap);
+}
+
+// analysis.cpp:153-179 — D(i,j) = mean over heads of sqrt(sums).
+__global__ void k_finalize(const double* sums, int n, int H, double* D) {
+  const int P = n * (n - 1) / 2;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) D[i] = 0.0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    int a = 0, rem = p;
+    while (rem >= n - 1 - a) {
+      rem -= n - 1 - a;
+      ++a;
+    }
+    const int b = a + 1 + rem;
+    double m = 0.0;
+    for (int h = 0; h < H; ++h) m += sqrt(sums[int64_t(p) * H + h]);
+    m /= double(H);
+    D[a * n + b] = m;
+    D[b * n + a] = m;
+  }
+}
+void launch_finalize(cudaStream_t s, const double* sums, int n, int H, double* D) {
+  k_finalize<<<1, 256, 0, s>>>(sums, n, H, D);
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- selector (K3)
+// strategy.cpp:44-69: candidates sorted lexicographically by (d, i, j) with a
+// shared-memory bitonic sort, then one thread walks the ranking accepting
+// disjoint pairs until |shared| >= quota. Bit-exact with std::sort + the
+// greedy loop on identical D (a strict total order on distinct (i, j)).
+__device__ __forceinline__ bool cand_less(double da, int ia, int ja, double db, int ib, int jb) {
+  if (da != db) return da < db;
+  if (ia != ib) return ia < ib;
+  return ja < jb;
+}
+__global__ void k_select(const double* cd, const int* ci, const int* cj, int n_cand, int cap,
+                         int quota, int* out_i, int* out_j, double* out_d, int* out_n) {
+  extern __shared__ unsigned char sraw[];
+  double* d = reinterpret_cast<double*>(sraw);
+  int* I = reinterpret_cast<int*>(d + cap);
+  int* J = I + cap;
+  for (int t = threadIdx.x; t < cap; t += blockDim.x) {
+    if (t < n_cand) {
+      d[t] = cd[t];
+      I[t] = ci[t];
+      J[t] = cj[t];
+    } else {
+      d[t] = INFINITY;
+      I[t] = 0x7fffffff;
+      J[t] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= cap; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < cap; t += blockDim.x) {
+        const int u = t ^ j;
+        if (u > t) {
+          const bool up = (t & k) == 0;
+          const bool gt = cand_less(d[u], I[u], J[u], d[t], I[t], J[t]);
+          if (gt == up) {
+            const double td = d[t]; d[t] = d[u]; d[u] = td;
+            const int ti = I[t]; I[t] = I[u]; I[u] = ti;
+            const int tj = J[t]; J[t] = J[u]; J[u] = tj;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long taken[4] = {0, 0, 0, 0};  // layers < 256
+    int shared = 0, np = 0;
+    for (int t = 0; t < n_cand; ++t) {
+      if (shared >= quota) break;
+      const int i = I[t], j = J[t];
+      const bool ti = (taken[i >> 6] >> (i & 63)) & 1ull;
+      const bool tj = (taken[j >> 6] >> (j & 63)) & 1ull;
+      if (ti || tj) continue;
+      taken[i >> 6] |= 1ull << (i & 63);
+      taken[j >> 6] |= 1ull << (j & 63);
+      out_i[np] = i;
+      out_j[np] = j;
+      out_d[np] = d[t];
+      ++np;
+      shared += 2;
+    }
+    *out_n = np;
+  }
+}
+void launch_select(cudaStream_t s, const double* cand_d, const int* cand_i, const int* cand_j,
+                   int n_cand, int quota, int* out_i, int* out_j, double* out_d, int* out_n) {
+  int cap = 1;
+  while (cap < n_cand) cap <<= 1;
+  const size_t smem = size_t(cap) * (sizeof(double) + 2 * sizeof(int));
+  KB_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k_select<<<1, 1024, smem, s>>>(cand_d, cand_i, cand_j, n_cand, cap, quota, out_i, out_j, out_d,
+                                 out_n);
+  KB_LAUNCH();
+}
+
+}  // namespace kb

@@ -1,0 +1,585 @@
+"""ctypes binding of include/krul_b200.h — the Python mirror of the
+reference's hot-path interface (/root/reference/proj/include/krul/*.hpp).
+
+Names follow the reference (classify_layers, StreamingEstimator,
+select_strategy, build_plan, calibrate_rc, compress_and_snapshot, expand,
+execute_restore, ...). Every call goes through libkrul_b200.so; there is no
+CPU fallback: importing this module on a machine without the built library
+raises, and any device entry fails loudly with CudaError when no GPU exists.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libkrul_b200.so")
+
+KRUL_F32, KRUL_BF16 = 0, 1
+FFN_TANH, FFN_SWIGLU = 0, 1
+MERGE_MEAN, MERGE_KEEP_DEEPER = 0, 1
+
+
+# ---- reference exception types (common.hpp:25-63) ---------------------------
+class KrulError(RuntimeError):
+    code = -1
+
+
+class ConfigError(KrulError):
+    code = 1
+
+
+class RestorationGapError(KrulError):
+    code = 2
+
+
+class StateCorruptionError(KrulError):
+    code = 3
+
+
+class AccountingError(KrulError):
+    code = 4
+
+
+class PlanInvalidError(KrulError):
+    code = 5
+
+
+class ClassificationError(KrulError):
+    code = 6
+
+
+class SnapshotError(KrulError):
+    code = 7
+
+
+class SnapshotLoadError(KrulError):
+    code = 8
+
+
+class CudaError(KrulError):
+    code = 9
+
+
+class ArgError(KrulError):
+    code = 10
+
+
+_ERRORS = {c.code: c for c in (ConfigError, RestorationGapError, StateCorruptionError,
+                               AccountingError, PlanInvalidError, ClassificationError,
+                               SnapshotError, SnapshotLoadError, CudaError, ArgError)}
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int), ("n_heads", C.c_int), ("n_kv_heads", C.c_int),
+        ("head_dim", C.c_int), ("d_model", C.c_int), ("vocab_size", C.c_int),
+        ("ffn_mult", C.c_float), ("ffn_kind", C.c_int), ("seed", C.c_uint64),
+        ("rope_theta", C.c_double), ("dtype", C.c_int), ("max_tokens", C.c_int64),
+    ]
+
+
+class Pair(C.Structure):
+    _fields_ = [("shallow", C.c_int), ("deep", C.c_int), ("distance", C.c_double)]
+
+
+class CostModelC(C.Structure):
+    _fields_ = [("f_peak", C.c_double), ("b_peak", C.c_double), ("ffn_mult", C.c_double),
+                ("kv_dim", C.c_int64), ("q_dim", C.c_int64), ("ffn_hidden", C.c_int64),
+                ("bytes_per_elem", C.c_double), ("ffn_kind", C.c_int)]
+
+
+class BlobSpecC(C.Structure):
+    _fields_ = [("owners", C.c_int * 2), ("start", C.c_int64), ("end", C.c_int64)]
+
+
+class RestoreStats(C.Structure):
+    _fields_ = [("restore_ms", C.c_double), ("compute_ms", C.c_double), ("load_ms", C.c_double),
+                ("bubble_compute", C.c_double), ("bubble_load", C.c_double),
+                ("h2d_bytes", C.c_double), ("expand_bytes", C.c_double),
+                ("recompute_flops", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Loads the B200 library; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                              "(the CUDA extension is required; there is no CPU path)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.krul_snapshot_n_blobs.argtypes = [C.c_void_p]
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        buf = C.create_string_buffer(1024)
+        lib().krul_last_error(buf, 1024)
+        raise _ERRORS.get(rc, KrulError)(buf.value.decode())
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _pairs(pairs):
+    pairs = list(pairs or [])
+    arr = (Pair * max(1, len(pairs)))()
+    for i, p in enumerate(pairs):
+        arr[i] = Pair(int(p[0]), int(p[1]), float(p[2]) if len(p) > 2 else 0.0)
+    return arr, len(pairs)
+
+
+@dataclass
+class ModelConfig:
+    """engine.hpp:17-29 ModelConfig + extensions (n_kv_heads, ffn_kind, rope_theta)."""
+    n_layers: int = 4
+    n_heads: int = 2
+    head_dim: int = 8
+    d_model: int = 16
+    vocab_size: int = 64
+    ffn_mult: float = 4.0
+    seed: int = 0
+    n_kv_heads: int = 0
+    ffn_kind: int = FFN_TANH
+    rope_theta: float = 10000.0
+    dtype: int = KRUL_F32
+    max_tokens: int = 1024
+
+    def desc(self):
+        return ModelDesc(self.n_layers, self.n_heads, self.n_kv_heads, self.head_dim, self.d_model,
+                         self.vocab_size, self.ffn_mult, self.ffn_kind, self.seed, self.rope_theta,
+                         self.dtype, self.max_tokens)
+
+    @property
+    def kv_heads(self):
+        return self.n_kv_heads or self.n_heads
+
+    def ffn_hidden(self):
+        return int(np.round(np.float32(self.ffn_mult) * np.float32(self.d_model)))
+
+    def hash(self):
+        out = C.c_uint64()
+        d = self.desc()
+        _check(lib().krul_config_hash(C.byref(d), C.byref(out)))
+        return out.value
+
+
+# ---- context / conversations -------------------------------------------------
+
+class Context:
+    """One CUDA device + weights + streams (krul_ctx)."""
+
+    def __init__(self, cfg: ModelConfig, device: int = 0):
+        self.cfg = cfg
+        h = C.c_void_p()
+        d = cfg.desc()
+        _check(lib().krul_ctx_create(device, C.byref(d), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().krul_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload_weights(self, w: np.ndarray):
+        w = np.ascontiguousarray(w, np.float32)
+        _check(lib().krul_weights_upload_f32(self.h, _p(w), C.c_int64(w.size)))
+
+    def init_weights(self, seed: int):
+        _check(lib().krul_weights_init_device(self.h, C.c_uint64(seed)))
+
+    def conversation(self, capacity=None) -> "Conversation":
+        return Conversation(self, capacity or self.cfg.max_tokens)
+
+    def set_capture(self, probs: bool):
+        _check(lib().krul_set_capture(self.h, int(bool(probs))))
+
+    def set_classifier_regions(self, initial_frac=0.1, recent_frac=0.1):
+        _check(lib().krul_set_classifier_regions(self.h, C.c_double(initial_frac),
+                                                  C.c_double(recent_frac)))
+
+    def sync(self):
+        _check(lib().krul_ctx_sync(self.h))
+
+    # -- engine (engine.hpp:106-139)
+    def prefill(self, conv, tokens):
+        t = np.ascontiguousarray(tokens, np.int32)
+        out = np.empty(self.cfg.vocab_size, np.float32)
+        _check(lib().krul_prefill(self.h, conv.h, _p(t), C.c_int64(t.size), _p(out)))
+        return out
+
+    def prefill_new(self, conv, tokens):
+        t = np.ascontiguousarray(tokens, np.int32)
+        out = np.empty(self.cfg.vocab_size, np.float32)
+        _check(lib().krul_prefill_new(self.h, conv.h, _p(t), C.c_int64(t.size), _p(out)))
+        return out
+
+    def decode_step(self, conv, token: int):
+        out = np.empty(self.cfg.vocab_size, np.float32)
+        _check(lib().krul_decode_step(self.h, conv.h, C.c_int32(int(token)), _p(out)))
+        return out
+
+    def partial_prefix_recompute(self, conv, tokens, recompute_len):
+        t = np.ascontiguousarray(tokens, np.int32)
+        p = np.ascontiguousarray(recompute_len, np.int64)
+        _check(lib().krul_partial_recompute(self.h, conv.h, _p(t), C.c_int64(t.size), _p(p),
+                                            len(p)))
+
+    def captured_prefill(self):
+        """[N, H, rows, width] f32 of the last prefill (capture must be on)."""
+        cfg = self.cfg
+        r, w = C.c_int64(), C.c_int64()
+        _check(lib().krul_capture_prefill(self.h, 0, 0, None, C.byref(r), C.byref(w)))
+        out = np.empty((cfg.n_layers, cfg.n_heads, r.value, w.value), np.float32)
+        for l in range(cfg.n_layers):
+            for hh in range(cfg.n_heads):
+                buf = np.empty((r.value, w.value), np.float32)
+                _check(lib().krul_capture_prefill(self.h, l, hh, _p(buf), None, None))
+                out[l, hh] = buf
+        return out
+
+    def captured_decode(self):
+        w = C.c_int64()
+        _check(lib().krul_capture_decode(self.h, None, C.byref(w)))
+        cfg = self.cfg
+        out = np.empty((cfg.n_layers, cfg.n_heads, w.value), np.float32)
+        _check(lib().krul_capture_decode(self.h, _p(out), None))
+        return out
+
+    def classify_layers(self, gamma=0.5, initial_frac=0.1, recent_frac=0.1):
+        """analysis.cpp:20-63 over the last prefill -> (avg_weight_sum, ir, non_ir)."""
+        N = self.cfg.n_layers
+        avg = np.empty(N, np.float64)
+        ir = np.empty(N, np.int32)
+        _check(lib().krul_classify(self.h, C.c_double(gamma), C.c_double(initial_frac),
+                                   C.c_double(recent_frac), _p(avg), _p(ir)))
+        return avg, [l for l in range(N) if ir[l]], [l for l in range(N) if not ir[l]]
+
+    def measure_rates(self, scratch):
+        b, f = C.c_double(), C.c_double()
+        _check(lib().krul_measure_rates(self.h, scratch.h, C.byref(b), C.byref(f)))
+        return b.value, f.value
+
+    # -- restore (scheduler.cpp:320-400)
+    def execute_restore(self, conv, history, snapshot):
+        t = np.ascontiguousarray(history, np.int32)
+        st = RestoreStats()
+        _check(lib().krul_restore(self.h, conv.h, snapshot.h, _p(t), C.c_int64(t.size),
+                                  C.byref(st)))
+        return st.as_dict()
+
+    def restore_and_prefill(self, conv, history, snapshot, new_tokens):
+        t = np.ascontiguousarray(history, np.int32)
+        n = np.ascontiguousarray(new_tokens, np.int32)
+        out = np.empty(self.cfg.vocab_size, np.float32)
+        st = RestoreStats()
+        ttft = C.c_double()
+        _check(lib().krul_restore_and_prefill(self.h, conv.h, snapshot.h, _p(t),
+                                              C.c_int64(t.size), _p(n), C.c_int64(n.size),
+                                              _p(out), C.byref(st), C.byref(ttft)))
+        return out, st.as_dict(), ttft.value
+
+
+class Conversation:
+    """Paged KV cache of one conversation (krul_conv)."""
+
+    def __init__(self, ctx: Context, capacity: int):
+        self.ctx = ctx
+        h = C.c_void_p()
+        _check(lib().krul_conv_create(ctx.h, C.c_int64(capacity), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().krul_conv_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        n = C.c_int64()
+        _check(lib().krul_conv_length(self.h, C.byref(n)))
+        return n.value
+
+    def kv(self, layer, start, end):
+        cfg = self.ctx.cfg
+        k = np.zeros((cfg.kv_heads, max(0, end - start), cfg.head_dim), np.float32)
+        v = np.zeros_like(k)
+        _check(lib().krul_conv_kv_read(self.h, layer, C.c_int64(start), C.c_int64(end), _p(k),
+                                       _p(v)))
+        return k, v
+
+    def write_kv(self, layer, start, end, k, v):
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        _check(lib().krul_conv_kv_write(self.h, layer, C.c_int64(start), C.c_int64(end), _p(k),
+                                        _p(v)))
+
+
+# ---- analysis: streaming estimator (analysis.hpp:96-126) ---------------------
+
+class StreamingEstimator:
+    def __init__(self, ctx: Context, ir_layers):
+        self.ctx = ctx
+        ir = np.ascontiguousarray(list(ir_layers) or [0], np.int32)
+        h = C.c_void_p()
+        _check(lib().krul_est_create(ctx.h, _p(ir), len(list(ir_layers)), C.byref(h)))
+        self.h = h
+        self.layers = sorted(set(int(x) for x in ir_layers))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().krul_est_destroy(self.h)
+
+    def fold_prefill(self):
+        _check(lib().krul_est_fold_prefill(self.h))
+
+    def fold_decode(self):
+        _check(lib().krul_est_fold_decode(self.h))
+
+    def fold_prefill_rows(self, probs):
+        p = np.ascontiguousarray(probs, np.float32)
+        N, H, R, W = p.shape
+        _check(lib().krul_est_fold_prefill_host(self.h, _p(p), N, C.c_int64(R), C.c_int64(W)))
+
+    def fold_decode_rows(self, rows):
+        r = np.ascontiguousarray(rows, np.float32)
+        N, H, W = r.shape
+        _check(lib().krul_est_fold_decode_host(self.h, _p(r), N, C.c_int64(W)))
+
+    def sums(self):
+        n = len(self.layers)
+        out = np.zeros(max(1, n * (n - 1) // 2 * self.ctx.cfg.n_heads), np.float64)
+        _check(lib().krul_est_sums(self.h, _p(out)))
+        return out[: n * (n - 1) // 2 * self.ctx.cfg.n_heads]
+
+    def finish(self):
+        n = len(self.layers)
+        D = np.zeros((max(n, 1), max(n, 1)), np.float64)
+        _check(lib().krul_est_finalize(self.h, _p(D)))
+        return D[:n, :n]
+
+    def counts(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().krul_est_counts(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+# ---- strategy (strategy.hpp:37-44) -------------------------------------------
+
+@dataclass
+class CompressionStrategy:
+    pairs: list = field(default_factory=list)  # [(shallow, deep, distance)]
+    exhausted_before_quota: bool = False
+
+    @property
+    def shared(self):
+        return sorted({x for p in self.pairs for x in p[:2]})
+
+
+def shared_layer_quota(n_layers, r_l):
+    out = C.c_int()
+    _check(lib().krul_quota(n_layers, C.c_double(r_l), C.byref(out)))
+    return out.value
+
+
+def select_strategy(ctx: Context, D, dm_layers, ir_layers, r_l, n_layers) -> CompressionStrategy:
+    """K3 on the device: sort (d, i, j) + greedy disjoint matching."""
+    D = np.ascontiguousarray(D, np.float64)
+    dl = np.ascontiguousarray(list(dm_layers) or [0], np.int32)
+    ir = np.ascontiguousarray(list(ir_layers) or [0], np.int32)
+    out = (Pair * max(1, len(list(ir_layers))))()
+    n, ex = C.c_int(), C.c_int()
+    _check(lib().krul_select(ctx.h, _p(D), _p(dl), len(list(dm_layers)), _p(ir),
+                             len(list(ir_layers)), C.c_double(r_l), n_layers, out, C.byref(n),
+                             C.byref(ex)))
+    return CompressionStrategy([(out[i].shallow, out[i].deep, out[i].distance)
+                                for i in range(n.value)], bool(ex.value))
+
+
+# ---- scheduler (scheduler.hpp:14-112) ----------------------------------------
+
+@dataclass
+class CostModel:
+    f_peak: float = 312e12
+    b_peak: float = 139e9
+    ffn_mult: float = 4.0
+    kv_dim: int = 0
+    q_dim: int = 0
+    ffn_hidden: int = 0
+    bytes_per_elem: float = 0.0
+    ffn_kind: int = 0
+
+    def c(self):
+        return CostModelC(self.f_peak, self.b_peak, self.ffn_mult, self.kv_dim, self.q_dim,
+                          self.ffn_hidden, self.bytes_per_elem, self.ffn_kind)
+
+    @staticmethod
+    def for_model(cfg: ModelConfig, f_peak, b_peak):
+        """Cost model with the model's real KV width, FFN and storage dtype."""
+        return CostModel(f_peak, b_peak, cfg.ffn_mult, cfg.kv_heads * cfg.head_dim,
+                         cfg.n_heads * cfg.head_dim, cfg.ffn_hidden(),
+                         2.0 if cfg.dtype == KRUL_BF16 else 4.0, cfg.ffn_kind)
+
+
+def build_plan(L, N, r_c, pairs=()):
+    arr, n = _pairs(pairs)
+    out = np.empty(N, np.int64)
+    _check(lib().krul_build_plan(C.c_int64(L), N, C.c_double(r_c), arr, n, _p(out)))
+    return out
+
+
+def uniform_plan(L, N, r_c):
+    out = np.empty(N, np.int64)
+    _check(lib().krul_uniform_plan(C.c_int64(L), N, C.c_double(r_c), _p(out)))
+    return out
+
+
+def default_rc_grid(step=0.05):
+    n = C.c_int()
+    _check(lib().krul_default_rc_grid(C.c_double(step), None, C.byref(n)))
+    out = np.empty(n.value, np.float64)
+    _check(lib().krul_default_rc_grid(C.c_double(step), _p(out), C.byref(n)))
+    return out
+
+
+def calibrate_rc(cost: CostModel, N, L, d, pairs=(), grid=None):
+    arr, n = _pairs(pairs)
+    g = np.ascontiguousarray(default_rc_grid() if grid is None else grid, np.float64)
+    out = C.c_double()
+    cm = cost.c()
+    _check(lib().krul_calibrate_rc(C.byref(cm), N, C.c_int64(L), C.c_int64(d), arr, n, _p(g),
+                                   len(g), C.byref(out)))
+    return out.value
+
+
+def validate_plan(L, p, pairs=()):
+    arr, n = _pairs(pairs)
+    pp = np.ascontiguousarray(p, np.int64)
+    m = C.c_int()
+    _check(lib().krul_validate_plan(C.c_int64(L), _p(pp), len(pp), arr, n, C.byref(m)))
+    return m.value
+
+
+def plan_blob_specs(L, p, pairs=()):
+    arr, n = _pairs(pairs)
+    pp = np.ascontiguousarray(p, np.int64)
+    out = (BlobSpecC * max(1, len(pp)))()
+    cnt = C.c_int()
+    _check(lib().krul_blob_specs(C.c_int64(L), _p(pp), len(pp), arr, n, out, C.byref(cnt)))
+    res = []
+    for i in range(cnt.value):
+        o = [out[i].owners[0]] + ([out[i].owners[1]] if out[i].owners[1] >= 0 else [])
+        res.append((o, (out[i].start, out[i].end)))
+    return res
+
+
+def simulate_pipeline(L, p, pairs, cost: CostModel, d):
+    arr, n = _pairs(pairs)
+    pp = np.ascontiguousarray(p, np.int64)
+    out = np.empty(5, np.float64)
+    cm = cost.c()
+    _check(lib().krul_simulate(C.c_int64(L), _p(pp), len(pp), arr, n, C.byref(cm), C.c_int64(d),
+                               _p(out)))
+    return dict(makespan=out[0], compute_finish=out[1], load_finish=out[2],
+                bubble_compute=out[3], bubble_load=out[4])
+
+
+# ---- kvstore (kvstore.hpp:16-89) -----------------------------------------------
+
+class KVSnapshot:
+    """Compressed KV store: pinned host blobs + plan + strategy."""
+
+    def __init__(self, h, ctx):
+        self.h = h
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().krul_snapshot_destroy(self.h)
+
+    @classmethod
+    def compress(cls, ctx: Context, conv: Conversation, pairs, recompute_len, L, mode=MERGE_MEAN):
+        """compress_and_snapshot (kvstore.cpp:243-314), K8 on the device."""
+        arr, n = _pairs(pairs)
+        p = np.ascontiguousarray(recompute_len, np.int64)
+        h = C.c_void_p()
+        _check(lib().krul_snapshot_compress(ctx.h, conv.h, arr, n, _p(p), C.c_int64(L), mode,
+                                            C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_blobs(cls, ctx: Context, pairs, recompute_len, L, mode, blobs):
+        """blobs: list of (K[kvh,rows,hd], V[kvh,rows,hd]) in service order."""
+        arr, n = _pairs(pairs)
+        p = np.ascontiguousarray(recompute_len, np.int64)
+        ks = [np.ascontiguousarray(b[0], np.float32) for b in blobs]
+        vs = [np.ascontiguousarray(b[1], np.float32) for b in blobs]
+        kp = (C.c_void_p * max(1, len(ks)))(*[k.ctypes.data for k in ks])
+        vp = (C.c_void_p * max(1, len(vs)))(*[v.ctypes.data for v in vs])
+        h = C.c_void_p()
+        _check(lib().krul_snapshot_from_host(ctx.h, arr, n, _p(p), C.c_int64(L), mode, kp, vp,
+                                             C.byref(h)))
+        return cls(h, ctx)
+
+    def n_blobs(self):
+        return lib().krul_snapshot_n_blobs(self.h)
+
+    def blob(self, b):
+        spec = BlobSpecC()
+        _check(lib().krul_snapshot_blob(self.h, b, C.byref(spec), None, None))
+        cfg = self.ctx.cfg
+        rows = spec.end - spec.start
+        k = np.empty((cfg.kv_heads, rows, cfg.head_dim), np.float32)
+        v = np.empty_like(k)
+        _check(lib().krul_snapshot_blob(self.h, b, C.byref(spec), _p(k), _p(v)))
+        o = [spec.owners[0]] + ([spec.owners[1]] if spec.owners[1] >= 0 else [])
+        return o, (spec.start, spec.end), k, v
+
+    def storage_report(self):
+        f, s = C.c_uint64(), C.c_uint64()
+        _check(lib().krul_snapshot_storage(self.h, C.byref(f), C.byref(s)))
+        return f.value, s.value
+
+    def plan(self):
+        N = self.ctx.cfg.n_layers
+        p = np.empty(N, np.int64)
+        L = C.c_int64()
+        _check(lib().krul_snapshot_plan(self.h, _p(p), C.byref(L)))
+        return p, L.value
+
+    def set_plan(self, p):
+        pp = np.ascontiguousarray(p, np.int64)
+        _check(lib().krul_snapshot_set_plan(self.h, _p(pp)))
+
+    def expand(self, layer):
+        cfg = self.ctx.cfg
+        p, L = self.plan()
+        rows = max(0, L - int(p[layer])) if 0 <= layer < len(p) else L
+        k = np.empty((cfg.kv_heads, max(rows, 1), cfg.head_dim), np.float32)
+        v = np.empty_like(k)
+        s, e = C.c_int64(), C.c_int64()
+        _check(lib().krul_expand(self.h, layer, _p(k), _p(v), C.byref(s), C.byref(e)))
+        r = e.value - s.value
+        return (s.value, e.value), k[:, :r], v[:, :r]

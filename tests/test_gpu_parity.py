@@ -1,0 +1,338 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.
+
+Tolerances (stated per SURVEY.md §8c):
+  * f32 parity mode: K/V and logits max-abs <= 1e-4, probabilities <= 1e-5,
+    estimator sums rel <= 1e-6, D rel <= 1e-6; pairs, plans and blob layouts
+    bit-exact.
+  * bf16 perf mode: per-layer relative Frobenius error <= 2e-2 vs the f32
+    oracle on identical weights; the selector bit-exact on identical D.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2507_08045_b200 import native
+    native.lib()
+    return native
+
+
+def make_pair(K, O, dtype, **kw):
+    base = dict(n_layers=3, n_heads=2, head_dim=4, d_model=8, vocab_size=17, ffn_mult=2.0, seed=5)
+    base.update(kw)
+    ocfg = O.ModelConfig(**base)
+    om = O.Model(ocfg)
+    cfg = K.ModelConfig(**base, dtype=dtype, max_tokens=1024)
+    ctx = K.Context(cfg, 0)
+    ctx.upload_weights(om.weights())
+    return ocfg, om, cfg, ctx
+
+
+def rel_fro(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-30))
+
+
+# ----------------------------------------------------------------- GEMM unit
+
+@pytest.mark.parametrize("M,N,Kd", [(1, 16, 8), (7, 40, 24), (128, 128, 64), (200, 300, 136),
+                                    (256, 2048, 512), (513, 4096, 1024), (64, 6144, 4096)])
+def test_gemm_bf16_tcgen05(K, oracle, M, N, Kd):
+    from paper_2507_08045_b200.native import _p, lib
+    import ctypes as C
+    cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
+                        dtype=K.KRUL_BF16, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(M * 7 + N)
+    A = rng.uniform(-1, 1, (M, Kd)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, Kd)).astype(np.float32)
+    Ab = A.astype(np.float32)
+    # reference on bf16-rounded inputs
+    def bf(x):
+        u = x.view(np.uint32).astype(np.uint64)
+        u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16
+        return u.astype(np.uint32).view(np.float32)
+    ref = bf(Ab).astype(np.float64) @ bf(B).astype(np.float64).T
+    out = np.zeros((M, N), np.float32)
+    rc = lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A), _p(B),
+                               None, 0, _p(out))
+    assert rc == 0
+    err = np.abs(out - ref).max() / max(np.abs(ref).max(), 1)
+    assert err < 1e-4, err
+
+
+def test_gemm_epilogues_f32(K):
+    from paper_2507_08045_b200.native import _p, lib
+    import ctypes as C
+    for dtype in (K.KRUL_F32, K.KRUL_BF16):
+        cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
+                            dtype=dtype, max_tokens=64)
+        ctx = K.Context(cfg, 0)
+        rng = np.random.default_rng(1)
+        M, N, Kd = 130, 256, 64
+        A = rng.uniform(-.5, .5, (M, Kd)).astype(np.float32)
+        B = rng.uniform(-.5, .5, (N, Kd)).astype(np.float32)
+        bias = rng.uniform(-.5, .5, N).astype(np.float32)
+        acc = A.astype(np.float64) @ B.astype(np.float64).T
+        tol = 1e-5 if dtype == K.KRUL_F32 else 3e-2
+        out = np.zeros((M, N), np.float32)
+        assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                     _p(B), _p(bias), 3, _p(out)) == 0
+        assert np.abs(out - np.tanh(acc + bias)).max() < tol
+        out = np.zeros((M, N // 2), np.float32)
+        assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                     _p(B), None, 4, _p(out)) == 0
+        g, u = acc[:, 0::2], acc[:, 1::2]
+        assert np.abs(out - g / (1 + np.exp(-g)) * u).max() < tol
+        resid = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+        out = resid.copy()
+        assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                     _p(B), _p(bias), 2, _p(out)) == 0
+        assert np.abs(out - (resid + acc + bias)).max() < tol
+
+
+# ----------------------------------------------------------------- engine
+
+@pytest.mark.parametrize("kw", [dict(), dict(head_dim=5, d_model=10),
+                                dict(n_layers=4, n_heads=4, head_dim=64, d_model=256,
+                                     vocab_size=256, ffn_mult=4.0, seed=7),
+                                dict(n_layers=3, n_heads=4, n_kv_heads=2, head_dim=16, d_model=64,
+                                     vocab_size=50, ffn_kind=1, rope_theta=500000.0)])
+def test_prefill_f32_matches_oracle(K, oracle, kw):
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
+    toks = oracle.tokens(40, 3, ocfg.vocab_size)
+    ctx.set_capture(True)
+    conv = ctx.conversation(128)
+    logits = ctx.prefill(conv, toks)
+    opf = om.prefill(toks)
+    assert np.abs(logits - opf.logits()).max() < 1e-4
+    assert np.abs(ctx.captured_prefill() - opf.attn_all()).max() < 1e-5
+    okv = opf.take_kv()
+    for l in range(ocfg.n_layers):
+        k, v = conv.kv(l, 0, 40)
+        ok, ov = okv.layer(l)
+        assert np.abs(k - ok).max() < 1e-4 and np.abs(v - ov).max() < 1e-4
+
+
+def test_decode_f32_matches_oracle(K, oracle):
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, n_layers=4, n_heads=4, head_dim=64,
+                                   d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    toks = oracle.tokens(33, 4, 256)
+    conv = ctx.conversation(128)
+    ctx.prefill(conv, toks[:-1])
+    okv = om.prefill(toks[:-1]).take_kv()
+    for step in range(3):
+        t = int(toks[-1]) if step == 0 else step
+        lg = ctx.decode_step(conv, t)
+        olg, orows = om.decode(okv, t)
+        assert np.abs(lg - olg).max() < 1e-4
+        assert np.abs(ctx.captured_decode() - orows).max() < 1e-5
+    assert len(conv) == 35
+
+
+def test_partial_recompute_f32(K, oracle):
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32)
+    toks = oracle.tokens(16, 7, 17)
+    conv = ctx.conversation(64)
+    ctx.partial_prefix_recompute(conv, toks, [12, 9, 4])
+    opk = om.partial(toks, [12, 9, 4])
+    for l, p in enumerate([12, 9, 4]):
+        k, v = conv.kv(l, 0, p)
+        ok, ov = opk.layer(l)
+        assert np.abs(k - ok).max() < 1e-5 and np.abs(v - ov).max() < 1e-5
+    with pytest.raises(K.PlanInvalidError):
+        ctx.partial_prefix_recompute(conv, toks, [4, 6, 2])
+    with pytest.raises(K.PlanInvalidError):
+        ctx.partial_prefix_recompute(conv, toks, [4, 2])
+
+
+def test_prefill_bf16_close_to_oracle(K, oracle):
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, **kw)
+    toks = oracle.tokens(300, 3, 256)
+    conv = ctx.conversation(512)
+    ctx.set_capture(True)
+    logits = ctx.prefill(conv, toks)
+    opf = om.prefill(toks)
+    assert rel_fro(logits, opf.logits()) < 2e-2
+    okv = opf.take_kv()
+    for l in range(4):
+        k, v = conv.kv(l, 0, 300)
+        ok, ov = okv.layer(l)
+        assert rel_fro(k, ok) < 2e-2 and rel_fro(v, ov) < 2e-2
+
+
+# ----------------------------------------------------------------- estimator
+
+def test_estimator_folds_match_oracle(K, oracle):
+    cfg = K.ModelConfig(n_layers=8, n_heads=3, head_dim=4, d_model=12, vocab_size=5,
+                        dtype=K.KRUL_F32, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(0)
+    N, H, s = 8, 3, 700
+    tracked = [0, 2, 3, 5, 7]
+    pre = rng.dirichlet(np.ones(s), (N, H, 20)).astype(np.float32)
+    est = K.StreamingEstimator(ctx, tracked)
+    acc = oracle.Accumulator(tracked, H)
+    est.fold_prefill_rows(pre)
+    acc.fold_prefill(pre)
+    for t in range(5):
+        rows = rng.dirichlet(np.ones(s + t), (N, H)).astype(np.float32)
+        est.fold_decode_rows(rows)
+        acc.fold_decode(rows)
+    assert np.allclose(est.sums(), acc.sums(), rtol=1e-9, atol=1e-12)
+    D, Do = est.finish(), acc.finalize()
+    assert np.allclose(D, Do, rtol=1e-9, atol=1e-12)
+    assert est.counts() == (20, 5)
+    with pytest.raises(K.AccountingError):
+        est.fold_prefill_rows(pre)
+    e2 = K.StreamingEstimator(ctx, tracked)
+    with pytest.raises(K.AccountingError):
+        e2.finish()
+
+
+def test_estimator_on_engine_capture(K, oracle):
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
+    toks = oracle.tokens(64, 9, 256)
+    ctx.set_capture(True)
+    conv = ctx.conversation(256)
+    ctx.prefill(conv, toks)
+    avg, ir, _ = ctx.classify_layers(gamma=0.1)
+    opf = om.prefill(toks)
+    oavg, oir = opf.classify(gamma=0.1)
+    assert np.allclose(avg, oavg, atol=1e-6) and ir == oir
+    est = K.StreamingEstimator(ctx, [0, 1, 2, 3])
+    est.fold_prefill()
+    acc = oracle.Accumulator([0, 1, 2, 3], 4)
+    acc.fold_prefill_handle(opf)
+    okv = opf.take_kv()
+    for t in range(4):
+        ctx.decode_step(conv, t + 1)
+        est.fold_decode()
+        _, rows = om.decode(okv, t + 1)
+        acc.fold_decode(rows)
+    assert np.allclose(est.finish(), acc.finalize(), rtol=1e-5, atol=1e-7)
+
+
+# ----------------------------------------------------------------- selector
+
+def test_selector_bit_exact(K, oracle):
+    cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
+                        dtype=K.KRUL_F32, max_tokens=16)
+    ctx = K.Context(cfg, 0)
+    D = np.array([[0, 3, 1, 4], [3, 0, 5, 2], [1, 5, 0, 6], [4, 2, 6, 0]], np.float64)
+    s = K.select_strategy(ctx, D, [0, 1, 2, 3], [0, 1, 2, 3], 1.0, 4)
+    assert s.pairs == [(0, 2, 1.0), (1, 3, 2.0)] and not s.exhausted_before_quota
+    s = K.select_strategy(ctx, np.ones((6, 6)) - np.eye(6), range(6), range(6), 1.0, 6)
+    assert s.pairs == [(0, 1, 1.0), (2, 3, 1.0), (4, 5, 1.0)]
+    rng = np.random.default_rng(303)
+    for trial in range(300):
+        N = 2 + int(rng.integers(80))
+        n_ir = int(rng.integers(0, min(N, 40) + 1))
+        ir = sorted(rng.permutation(N)[:n_ir].tolist())
+        D = np.zeros((n_ir, n_ir))
+        iu = np.triu_indices(n_ir, 1)
+        vals = rng.uniform(0, 2, len(iu[0]))
+        if trial % 3 == 0:
+            vals = np.round(vals, 1)  # ties
+        D[iu] = vals
+        D = D + D.T
+        r_l = 0.25 * int(rng.integers(5))
+        got = K.select_strategy(ctx, D, ir, list(rng.permutation(ir)) if ir else [], r_l, N)
+        want = oracle.select_strategy(D, ir, ir, r_l, N)
+        assert got.pairs == want.pairs and got.exhausted_before_quota == want.exhausted
+
+
+# ----------------------------------------------------------------- kvstore + restore
+
+def test_snapshot_compress_matches_oracle(K, oracle):
+    kw = dict(n_layers=4, n_heads=2, head_dim=4, d_model=8, vocab_size=13, seed=21)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
+    hist = oracle.tokens(70, 77, 13)
+    conv = ctx.conversation(128)
+    ctx.prefill(conv, hist)
+    okv = om.prefill(hist).take_kv()
+    pairs = [(1, 3, 0.25)]
+    p = K.build_plan(70, 4, 0.4, pairs)
+    for mode in (0, 1):
+        snap = K.KVSnapshot.compress(ctx, conv, pairs, p, 70, mode)
+        osnap = oracle.Snapshot(okv, ocfg, oracle.Strategy(pairs), p, 70, mode=mode)
+        assert snap.n_blobs() == osnap.n_blobs()
+        for b in range(snap.n_blobs()):
+            o1, s1, k1, v1 = snap.blob(b)
+            o2, s2, k2, v2 = osnap.blob(b)
+            assert o1 == o2 and tuple(s1) == tuple(s2)
+            assert np.abs(k1 - k2).max() < 1e-5 and np.abs(v1 - v2).max() < 1e-5
+        assert snap.storage_report() == osnap.storage()
+        for l in range(4):
+            (a, e), k, v = snap.expand(l)
+            (a2, e2), k2, v2 = osnap.expand(l)
+            assert (a, e) == (a2, e2) and np.abs(k - k2).max() < 1e-5
+        with pytest.raises(K.RestorationGapError):
+            snap.expand(4)
+
+
+@pytest.mark.parametrize("r_c", [0.0, 0.25, 0.5, 0.75, 1.0])
+def test_lossless_restore(K, oracle, r_c):  # test_scheduler.cpp:353-400
+    kw = dict(n_layers=4, n_heads=2, head_dim=4, d_model=8, vocab_size=13, seed=21)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
+    hist = oracle.tokens(24, 77, 13)
+    conv = ctx.conversation(64)
+    ctx.prefill(conv, hist)
+    p = K.build_plan(24, 4, r_c)
+    snap = K.KVSnapshot.compress(ctx, conv, [], p, 24, K.MERGE_KEEP_DEEPER)
+    conv2 = ctx.conversation(64)
+    st = ctx.execute_restore(conv2, hist, snap)
+    for l in range(4):
+        k1, v1 = conv.kv(l, 0, 24)
+        k2, v2 = conv2.kv(l, 0, 24)
+        assert np.abs(k1 - k2).max() < 1e-6 and np.abs(v1 - v2).max() < 1e-6
+    a = ctx.decode_step(conv2, int(hist[-1]))
+    b = ctx.decode_step(conv, int(hist[-1]))
+    assert np.abs(a - b).max() < 1e-5
+    assert st["restore_ms"] >= 0
+
+
+def test_restore_and_prefill_matches_oracle(K, oracle):
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    for dtype, tol in ((K.KRUL_F32, 1e-4), (K.KRUL_BF16, None)):
+        ocfg, om, cfg, ctx = make_pair(K, oracle, dtype, **kw)
+        hist = oracle.tokens(512, 11, 256)
+        new = oracle.tokens(64, 12, 256)
+        conv = ctx.conversation(1024)
+        ctx.prefill(conv, hist)
+        pairs = [(1, 2, 0.5)]
+        p = K.build_plan(512, 4, 0.3, pairs)
+        snap = K.KVSnapshot.compress(ctx, conv, pairs, p, 512, K.MERGE_MEAN)
+        conv2 = ctx.conversation(1024)
+        logits, st, ttft = ctx.restore_and_prefill(conv2, hist, snap, new)
+        okv = om.prefill(hist).take_kv()
+        osnap = oracle.Snapshot(okv, ocfg, oracle.Strategy(pairs), p, 512, mode=0)
+        rest = om.restore(hist, osnap)
+        want = om.prefill(np.concatenate([hist, new]), preload=rest.suffix([0] * 4)).logits()
+        if tol:
+            assert np.abs(logits - want).max() < tol
+        else:
+            assert rel_fro(logits, want) < 3e-2
+        assert ttft > 0 and len(conv2) == 576
+
+
+def test_restore_rejects_mismatch(K, oracle):  # test_scheduler.cpp:402-430
+    kw = dict(n_layers=2, n_heads=1, head_dim=4, d_model=4, vocab_size=7)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
+    hist = np.array([1, 2, 3, 4, 5, 6], np.int32)
+    conv = ctx.conversation(16)
+    ctx.prefill(conv, hist)
+    snap = K.KVSnapshot.compress(ctx, conv, [], K.build_plan(6, 2, 0.5), 6, 1)
+    c2 = ctx.conversation(16)
+    with pytest.raises(K.RestorationGapError):
+        ctx.execute_restore(c2, np.append(hist, 1), snap)
+    snap.set_plan([2, 1])
+    with pytest.raises(K.RestorationGapError):
+        ctx.execute_restore(c2, hist, snap)
+    with pytest.raises(K.ConfigError):
+        ctx.prefill(c2, np.array([0, 7], np.int32))
