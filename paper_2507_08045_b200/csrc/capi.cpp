@@ -173,8 +173,8 @@ int krul_conv_kv_read(krul_conv* conv, int layer, int64_t start, int64_t end, fl
     float* d = static_cast<float*>(tmp.ensure(2 * n * 4));
     launch_kv_gather(c, c.s_comp, cv, layer, start, end, d, d + n);
     KB_CUDA(cudaStreamSynchronize(c.s_comp));
-    if (k) KB_CUDA(cudaMemcpy(k, d, n * 4, cudaMemcpyDeviceToHost));
-    if (v) KB_CUDA(cudaMemcpy(v, d + n, n * 4, cudaMemcpyDeviceToHost));
+    if (k) KB_CUDA(kb_memcpy_sync(k, d, n * 4, cudaMemcpyDeviceToHost));
+    if (v) KB_CUDA(kb_memcpy_sync(v, d + n, n * 4, cudaMemcpyDeviceToHost));
   });
 }
 int krul_conv_kv_write(krul_conv* conv, int layer, int64_t start, int64_t end, const float* k,
@@ -192,8 +192,8 @@ int krul_conv_kv_write(krul_conv* conv, int layer, int64_t start, int64_t end, c
     KB_CUDA(cudaSetDevice(c.device));
     DevBuf tmp;
     float* d = static_cast<float*>(tmp.ensure(2 * n * 4));
-    KB_CUDA(cudaMemcpy(d, k, n * 4, cudaMemcpyHostToDevice));
-    KB_CUDA(cudaMemcpy(d + n, v, n * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d, k, n * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d + n, v, n * 4, cudaMemcpyHostToDevice));
     launch_kv_scatter_f32(c, c.s_comp, cv, layer, start, end, d, d + n);
     KB_CUDA(cudaStreamSynchronize(c.s_comp));
     cv.len = std::max(cv.len, end);
@@ -260,7 +260,7 @@ int krul_capture_prefill(krul_ctx* ctx, int layer, int head, float* out, int64_t
     if (out) {
       const size_t n = size_t(c.cap_rows * c.cap_width);
       const float* src = c.cap_probs.as<float>() + (size_t(layer) * c.cfg.H + head) * n;
-      KB_CUDA(cudaMemcpy(out, src, n * 4, cudaMemcpyDeviceToHost));
+      KB_CUDA(kb_memcpy_sync(out, src, n * 4, cudaMemcpyDeviceToHost));
     }
   });
 }
@@ -271,7 +271,7 @@ int krul_capture_decode(krul_ctx* ctx, float* out, int64_t* width) {
     if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
     if (width) *width = c.dec_width;
     if (out)
-      KB_CUDA(cudaMemcpy(out, c.dec_rows.p, size_t(c.cfg.N) * c.cfg.H * c.dec_width * 4,
+      KB_CUDA(kb_memcpy_sync(out, c.dec_rows.p, size_t(c.cfg.N) * c.cfg.H * c.dec_width * 4,
                          cudaMemcpyDeviceToHost));
   });
 }
@@ -295,7 +295,7 @@ int krul_classify(krul_ctx* ctx, double gamma, double ifrac, double rfrac, doubl
     const int N = c.cfg.N, H = c.cfg.H;
     const int64_t R = c.cap_rows;
     std::vector<double> m(size_t(N) * H * R);
-    KB_CUDA(cudaMemcpy(m.data(), c.cap_mass.p, m.size() * 8, cudaMemcpyDeviceToHost));
+    KB_CUDA(kb_memcpy_sync(m.data(), c.cap_mass.p, m.size() * 8, cudaMemcpyDeviceToHost));
     for (int l = 0; l < N; ++l) {
       double mass = 0.0;
       for (int h = 0; h < H; ++h) {
@@ -327,10 +327,10 @@ int krul_est_create(krul_ctx* ctx, const int* ir, int n, krul_est** out) {
     const size_t nl = std::max<size_t>(e->layers.size(), 1);
     e->d_layers.ensure(nl * 4);
     if (!e->layers.empty())
-      KB_CUDA(cudaMemcpy(e->d_layers.p, e->layers.data(), e->layers.size() * 4, cudaMemcpyHostToDevice));
+      KB_CUDA(kb_memcpy_sync(e->d_layers.p, e->layers.data(), e->layers.size() * 4, cudaMemcpyHostToDevice));
     const size_t ns = size_t(std::max(e->P(), 1)) * e->H;
     e->sums.ensure(ns * 8);
-    KB_CUDA(cudaMemset(e->sums.p, 0, ns * 8));
+    KB_CUDA(kb_memset_sync(e->sums.p, 0, ns * 8));
     *out = new krul_est{e};
   });
 }
@@ -394,7 +394,7 @@ int krul_est_fold_prefill_host(krul_est* est, const float* probs, int N, int64_t
     KB_CUDA(cudaSetDevice(e.ctx->device));
     const size_t n = size_t(N) * e.H * size_t(rows) * size_t(W);
     float* d = static_cast<float*>(e.tmp.ensure(std::max<size_t>(n, 1) * 4));
-    KB_CUDA(cudaMemcpy(d, probs, n * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d, probs, n * 4, cudaMemcpyHostToDevice));
     fold_prefill_dev(e, d, rows, W, N);
   });
 }
@@ -406,7 +406,7 @@ int krul_est_fold_decode_host(krul_est* est, const float* rows, int N, int64_t W
     KB_CUDA(cudaSetDevice(e.ctx->device));
     const size_t n = size_t(N) * e.H * size_t(W);
     float* d = static_cast<float*>(e.tmp.ensure(std::max<size_t>(n, 1) * 4));
-    KB_CUDA(cudaMemcpy(d, rows, n * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d, rows, n * 4, cudaMemcpyHostToDevice));
     fold_decode_dev(e, d, W, N);
   });
 }
@@ -415,7 +415,7 @@ int krul_est_sums(krul_est* est, double* sums) {
     need(est, "est");
     Est& e = *est->e;
     KB_CUDA(cudaSetDevice(e.ctx->device));
-    if (e.P() > 0) KB_CUDA(cudaMemcpy(sums, e.sums.p, size_t(e.P()) * e.H * 8, cudaMemcpyDeviceToHost));
+    if (e.P() > 0) KB_CUDA(kb_memcpy_sync(sums, e.sums.p, size_t(e.P()) * e.H * 8, cudaMemcpyDeviceToHost));
   });
 }
 int krul_est_finalize(krul_est* est, double* D) {
@@ -429,7 +429,7 @@ int krul_est_finalize(krul_est* est, double* D) {
     double* dD = static_cast<double*>(e.D.ensure(size_t(n) * n * 8));
     launch_finalize(e.ctx->s_est, e.sums.as<double>(), n, e.H, dD);
     KB_CUDA(cudaStreamSynchronize(e.ctx->s_est));
-    KB_CUDA(cudaMemcpy(D, dD, size_t(n) * n * 8, cudaMemcpyDeviceToHost));
+    KB_CUDA(kb_memcpy_sync(D, dD, size_t(n) * n * 8, cudaMemcpyDeviceToHost));
   });
 }
 int krul_est_counts(krul_est* est, int64_t* pr, int64_t* ds) {
@@ -488,19 +488,19 @@ int krul_select(krul_ctx* ctx, const double* D, const int* dm_layers, int n, con
     int* d_oi = reinterpret_cast<int*>(d_od + nc);
     int* d_oj = d_oi + nc;
     int* d_on = d_oj + nc;
-    KB_CUDA(cudaMemcpy(d_cd, cd.data(), size_t(nc) * 8, cudaMemcpyHostToDevice));
-    KB_CUDA(cudaMemcpy(d_ci, ci.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
-    KB_CUDA(cudaMemcpy(d_cj, cj.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d_cd, cd.data(), size_t(nc) * 8, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d_ci, ci.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(d_cj, cj.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
     launch_select(c.s_est, d_cd, d_ci, d_cj, nc, q, d_oi, d_oj, d_od, d_on);
     KB_CUDA(cudaStreamSynchronize(c.s_est));
     int np = 0;
-    KB_CUDA(cudaMemcpy(&np, d_on, 4, cudaMemcpyDeviceToHost));
+    KB_CUDA(kb_memcpy_sync(&np, d_on, 4, cudaMemcpyDeviceToHost));
     std::vector<int> oi(size_t(std::max(np, 1))), oj(oi.size());
     std::vector<double> od(oi.size());
     if (np) {
-      KB_CUDA(cudaMemcpy(oi.data(), d_oi, size_t(np) * 4, cudaMemcpyDeviceToHost));
-      KB_CUDA(cudaMemcpy(oj.data(), d_oj, size_t(np) * 4, cudaMemcpyDeviceToHost));
-      KB_CUDA(cudaMemcpy(od.data(), d_od, size_t(np) * 8, cudaMemcpyDeviceToHost));
+      KB_CUDA(kb_memcpy_sync(oi.data(), d_oi, size_t(np) * 4, cudaMemcpyDeviceToHost));
+      KB_CUDA(kb_memcpy_sync(oj.data(), d_oj, size_t(np) * 4, cudaMemcpyDeviceToHost));
+      KB_CUDA(kb_memcpy_sync(od.data(), d_od, size_t(np) * 8, cudaMemcpyDeviceToHost));
     }
     for (int k = 0; k < np; ++k) out[k] = krul_pair{oi[size_t(k)], oj[size_t(k)], od[size_t(k)]};
     *n_out = np;
@@ -731,8 +731,8 @@ int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float*
     DevBuf a32, b32, a, b, out, outc, bb;
     float* da = static_cast<float*>(a32.ensure(size_t(M * K) * 4));
     float* db = static_cast<float*>(b32.ensure(size_t(N * K) * 4));
-    KB_CUDA(cudaMemcpy(da, A, size_t(M * K) * 4, cudaMemcpyHostToDevice));
-    KB_CUDA(cudaMemcpy(db, B, size_t(N * K) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(da, A, size_t(M * K) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(db, B, size_t(N * K) * 4, cudaMemcpyHostToDevice));
     void* ca = a.ensure(size_t(M * K) * c.esz);
     void* cb = b.ensure(size_t(N * K) * c.esz);
     launch_cvt_from_f32(c, s, da, ca, M * K);
@@ -744,13 +744,13 @@ int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float*
     e.ldo = ncols;
     if (bias) {
       float* dbias = static_cast<float*>(bb.ensure(size_t(N) * 4));
-      KB_CUDA(cudaMemcpy(dbias, bias, size_t(N) * 4, cudaMemcpyHostToDevice));
+      KB_CUDA(kb_memcpy_sync(dbias, bias, size_t(N) * 4, cudaMemcpyHostToDevice));
       e.bias = dbias;
     }
     if (epi == Epi::F32 || epi == Epi::RESID) {
       e.out = o;
       if (epi == Epi::RESID) {
-        KB_CUDA(cudaMemcpy(o, Cout, size_t(M * N) * 4, cudaMemcpyHostToDevice));
+        KB_CUDA(kb_memcpy_sync(o, Cout, size_t(M * N) * 4, cudaMemcpyHostToDevice));
         e.resid = o;
         e.ldr = N;
       }
@@ -760,7 +760,7 @@ int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float*
     gemm(c, s, M, N, K, ca, K, cb, K, e);
     if (epi == Epi::TANH || epi == Epi::SWIGLU || epi == Epi::CDT) launch_cvt_to_f32(c, s, e.out, o, M * ncols);
     KB_CUDA(cudaStreamSynchronize(s));
-    KB_CUDA(cudaMemcpy(Cout, o, size_t(M * ncols) * 4, cudaMemcpyDeviceToHost));
+    KB_CUDA(kb_memcpy_sync(Cout, o, size_t(M * ncols) * 4, cudaMemcpyDeviceToHost));
   });
 }
 

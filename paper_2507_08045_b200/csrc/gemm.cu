@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   }
+  __syncwarp();
   tc::fence_before();
   __syncthreads();
   if (warp == 1) {

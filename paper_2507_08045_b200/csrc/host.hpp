@@ -9,6 +9,7 @@ namespace kb {
 struct WS {  // per-stream activation workspace
   float *h = nullptr, *h2 = nullptr, *qkv = nullptr, *hmid = nullptr;
   void *xn = nullptr, *q = nullptr, *attn = nullptr, *hmidc = nullptr, *act = nullptr;
+  DevBuf* part = nullptr;
 };
 
 Ctx* ctx_create(int device, const krul_model_desc& desc);

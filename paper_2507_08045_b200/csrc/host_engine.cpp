@@ -41,14 +41,17 @@ Ctx* ctx_create(int device, const krul_model_desc& desc) {
     c->rope.ensure(2 * cs.size() * sizeof(float));
     c->rope_cos = c->rope.as<float>();
     c->rope_sin = c->rope_cos + cs.size();
-    KB_CUDA(cudaMemcpy(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
-    KB_CUDA(cudaMemcpy(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
     // KV page pool: room for KRUL_KV_POOL_CONVS conversations of max_tokens.
     int convs = 2;
     if (const char* v = std::getenv("KRUL_KV_POOL_CONVS")) convs = std::max(1, std::atoi(v));
     const int64_t pages_per_layer = (cfg.max_tokens + kPageTokens - 1) / kPageTokens;
     c->pool_pages = int(pages_per_layer * cfg.N * convs);
     c->pool.ensure(size_t(c->pool_pages) * c->page_elems() * c->esz);
+    // zeroed once so never-written positions of a page are finite (masked
+    // keys still multiply V inside the tensor-core P V product)
+    KB_CUDA(kb_memset_sync(c->pool.p, 0, size_t(c->pool_pages) * c->page_elems() * c->esz));
     c->free_pages.resize(size_t(c->pool_pages));
     for (int i = 0; i < c->pool_pages; ++i) c->free_pages[size_t(i)] = c->pool_pages - 1 - i;
   } catch (...) {
@@ -79,7 +82,7 @@ static void carve_weights(Ctx& c) {
   const size_t un_off = total;
   total = align(total + size_t(g.V) * d * c.esz);
   char* base = static_cast<char*>(c.wbuf.ensure(total));
-  KB_CUDA(cudaMemset(base, 0, total));
+  KB_CUDA(kb_memset_sync(base, 0, total));
   c.L.assign(size_t(g.N), LayerW{});
   for (int l = 0; l < g.N; ++l) {
     char* p = base + off[size_t(2 * l)];
@@ -118,7 +121,7 @@ void weights_upload_f32(Ctx& c, const float* w, int64_t n) {
   auto upload = [&](int64_t rows, int64_t cols) -> float* {
     float* p = static_cast<float*>(tmp.ensure(size_t(rows * cols) * 4));
     KB_CUDA(cudaStreamSynchronize(s));
-    KB_CUDA(cudaMemcpy(p, src, size_t(rows * cols) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(kb_memcpy_sync(p, src, size_t(rows * cols) * 4, cudaMemcpyHostToDevice));
     src += rows * cols;
     return p;
   };
@@ -135,10 +138,10 @@ void weights_upload_f32(Ctx& c, const float* w, int64_t n) {
     launch_convert_weights(c, s, upload(qd, d), lw.wo, qd, d, 1, 0);
     if (g.ffn_kind == KRUL_FFN_TANH) {
       launch_convert_weights(c, s, upload(d, F), lw.w1, d, F, 1, 0);
-      KB_CUDA(cudaMemcpy(lw.b1, src, size_t(F) * 4, cudaMemcpyHostToDevice));
+      KB_CUDA(kb_memcpy_sync(lw.b1, src, size_t(F) * 4, cudaMemcpyHostToDevice));
       src += F;
       launch_convert_weights(c, s, upload(F, d), lw.w2, F, d, 1, 0);
-      KB_CUDA(cudaMemcpy(lw.b2, src, size_t(d) * 4, cudaMemcpyHostToDevice));
+      KB_CUDA(kb_memcpy_sync(lw.b2, src, size_t(d) * 4, cudaMemcpyHostToDevice));
       src += d;
     } else {
       launch_convert_weights(c, s, upload(d, F), lw.w1, d, F, 1, 1);  // gate -> even rows
@@ -195,7 +198,7 @@ Conv* conv_create(Ctx& c, int64_t capacity) {
   }
   KB_CUDA(cudaSetDevice(c.device));
   KB_CUDA(cudaMalloc(&v->d_pt, need * sizeof(int)));
-  KB_CUDA(cudaMemcpy(v->d_pt, v->pages.data(), need * sizeof(int), cudaMemcpyHostToDevice));
+  KB_CUDA(kb_memcpy_sync(v->d_pt, v->pages.data(), need * sizeof(int), cudaMemcpyHostToDevice));
   return v;
 }
 
@@ -222,6 +225,7 @@ WS ws_get(Ctx& c, int set, int64_t rows) {
   w.hmid = static_cast<float*>(hm->ensure(r * g.d * 4));
   w.hmidc = hc->ensure(r * g.d * c.esz);
   w.act = act->ensure(r * g.F * c.esz);
+  w.part = set == 0 ? &c.ws_part : &c.ws2_part;
   return w;
 }
 
@@ -243,6 +247,7 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
   launch_rope_scatter(c, s, w.qkv, rows, pos0, out_rows, w.q, conv, l);
   if (out_rows <= 0) return;
   AttnArgs a = cap ? *cap : AttnArgs{};
+  a.part = w.part;
   a.q = w.q;
   a.rows = out_rows;
   a.pos0 = pos0;

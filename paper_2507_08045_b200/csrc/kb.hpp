@@ -28,6 +28,25 @@ struct Error : std::runtime_error {
   } while (0)
 #define KB_LAUNCH() KB_CUDA(cudaGetLastError())
 
+// Blocking copies/memsets that are ordered against the library's
+// non-blocking streams: plain cudaMemcpy/cudaMemset run on the legacy stream,
+// which does not synchronise with cudaStreamNonBlocking streams, and a
+// pageable H2D cudaMemcpy may return before its DMA lands.
+inline cudaError_t kb_memcpy_sync(void* d, const void* s, size_t n, cudaMemcpyKind k) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(d, s, n, k);
+  if (e != cudaSuccess) return e;
+  return cudaDeviceSynchronize();
+}
+inline cudaError_t kb_memset_sync(void* d, int v, size_t n) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(d, v, n);
+  if (e != cudaSuccess) return e;
+  return cudaDeviceSynchronize();
+}
+
 constexpr int kPageTokens = 64;  // tokens per KV page
 
 // Model configuration (engine.hpp:17-29 + extensions).
@@ -123,6 +142,7 @@ struct Ctx {
   DevBuf ws_h, ws_h2, ws_xn, ws_qkv, ws_q, ws_attn, ws_hmid, ws_hmidc, ws_act, ws_y;
   DevBuf ws_tok, ws_tok2, ws_logits;
   DevBuf ws_new_h, ws_new_h2;  // new-input prefill stream
+  DevBuf ws_part, ws2_part;    // split-KV attention partials per stream
   // second workspace set for the concurrent new-input prefill stream
   DevBuf ws2_xn, ws2_qkv, ws2_q, ws2_attn, ws2_hmid, ws2_hmidc, ws2_act, ws2_y;
 
@@ -171,6 +191,7 @@ void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, 
 // Q (roped, cdt) for rows < q_rows.
 void launch_rope_scatter(const Ctx& c, cudaStream_t s, const float* qkv, int64_t rows,
                          int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer);
+struct DevBuf;
 struct AttnArgs {
   const void* q = nullptr;  // [rows][H*hd] cdt
   int64_t rows = 0, pos0 = 0;
@@ -182,9 +203,13 @@ struct AttnArgs {
   double* mass = nullptr;   // optional [H][mass_rows] region mass
   int64_t mass_rows = 0;
   int64_t il = 0, rs = 0;   // classifier regions [0,il) U [rs, W)
+  DevBuf* part = nullptr;   // split-KV scratch owned by the calling stream
 };
 void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                       const AttnArgs& a);
+bool attention_tc_supported(const Ctx& c, const AttnArgs& a);
+void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
+                         const AttnArgs& a, DevBuf& scratch);
 void launch_bias_act(const Ctx& c, cudaStream_t s, const float* in, int64_t rows, int64_t F,
                      const float* b1, int kind, void* out);  // tanh(x+b) or swiglu pairs
 void launch_resid_add(const Ctx& c, cudaStream_t s, const float* y, const float* bias,

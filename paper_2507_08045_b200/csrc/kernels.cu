@@ -195,19 +195,23 @@ __global__ void k_attn_simt(const T* q, int64_t pos0, PageView pv, int H, float 
 void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                       const AttnArgs& a) {
   if (a.rows <= 0) return;
+  if (a.part && attention_tc_supported(c, a)) {
+    launch_attention_tc(c, s, conv, layer, a, *a.part);
+    return;
+  }
   PageView pv = page_view(c, conv, layer);
   const float scale = 1.0f / sqrtf(float(c.cfg.hd));
   const size_t smem = sizeof(float) * size_t(c.cfg.hd + a.pos0 + a.rows);
   dim3 grid(unsigned(a.rows), unsigned(c.cfg.H));
   if (c.cfg.dtype == KRUL_BF16) {
     auto k = k_attn_simt<bf16>;
-    KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     k<<<grid, 128, smem, s>>>((const bf16*)a.q, a.pos0, pv, c.cfg.H, scale, (bf16*)a.out, a.probs,
                               a.ld_probs, a.probs_row0, a.probs_rows, a.mass, a.mass_rows, a.il,
                               a.rs);
   } else {
     auto k = k_attn_simt<float>;
-    KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     k<<<grid, 128, smem, s>>>((const float*)a.q, a.pos0, pv, c.cfg.H, scale, (float*)a.out,
                               a.probs, a.ld_probs, a.probs_row0, a.probs_rows, a.mass,
                               a.mass_rows, a.il, a.rs);
@@ -537,6 +541,7 @@ void launch_compress(const Ctx& c, cudaStream_t s, const Conv& conv, int deep, i
 // double (analysis.cpp:146-147) with warp shuffles. Stage 2 adds the chunk
 // partials in a fixed order (deterministic, no fp atomics).
 constexpr int kFoldChunk = 512;
+template <bool kExactDiff>
 __global__ void k_fold_stage1(const float* rows, int64_t layer_stride, int64_t head_stride,
                               int64_t total, int H, const int* layers, int n, double* partial) {
   extern __shared__ float fs[];  // [n][kFoldChunk]
@@ -568,7 +573,10 @@ __global__ void k_fold_stage1(const float* rows, int64_t layer_stride, int64_t h
     const float* y = fs + b * kFoldChunk;
     double acc = 0.0;
     for (int i = lane; i < cw; i += 32) {
-      const double d = double(x[i] - y[i]);
+      // decode rows: f32 difference (analysis.cpp:146-147); prefill: the
+      // reference's expanded double form is exact in the operands, so the
+      // difference is taken in double.
+      const double d = kExactDiff ? double(x[i]) - double(y[i]) : double(x[i] - y[i]);
       acc += d * d;
     }
     acc = warp_sum_d(acc);
@@ -582,6 +590,7 @@ __global__ void k_fold_stage2(const double* partial, int chunks, int PH, double*
   for (int ch = 0; ch < chunks; ++ch) acc += partial[int64_t(ch) * PH + i];
   sums[i] += acc;
 }
+template <bool kExactDiff>
 static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
                         int64_t head_stride, int64_t total, int H, const int* d_layers, int n,
                         double* sums, double* partial, int64_t partial_cap) {
@@ -590,9 +599,9 @@ static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
   const int chunks = int((total + kFoldChunk - 1) / kFoldChunk);
   if (int64_t(chunks) * P * H > partial_cap) fail(KRUL_E_CUDA, "fold partial buffer too small");
   const size_t smem = size_t(n) * kFoldChunk * sizeof(float);
-  KB_CUDA(cudaFuncSetAttribute(k_fold_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
-  k_fold_stage1<<<dim3(unsigned(chunks), unsigned(H)), 256, smem, s>>>(
+  KB_CUDA(cudaFuncSetAttribute(k_fold_stage1<kExactDiff>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k_fold_stage1<kExactDiff><<<dim3(unsigned(chunks), unsigned(H)), 256, smem, s>>>(
       rows, layer_stride, head_stride, total, H, d_layers, n, partial);
   KB_LAUNCH();
   k_fold_stage2<<<unsigned((P * H + 255) / 256), 256, 0, s>>>(partial, chunks, P * H, sums);
@@ -600,7 +609,7 @@ static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
 }
 void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, const int* d_layers,
                         int n, double* sums, double* partial, int64_t partial_cap) {
-  fold_common(s, rows, int64_t(H) * W, W, W, H, d_layers, n, sums, partial, partial_cap);
+  fold_common<false>(s, rows, int64_t(H) * W, W, W, H, d_layers, n, sums, partial, partial_cap);
 }
 // Prefill fold over the full [rows x W] rectangle per (pair, head): the
 // direct sum of squared differences in double; the reference's expanded
@@ -608,8 +617,8 @@ void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, con
 void launch_fold_prefill(cudaStream_t s, const float* probs, int64_t rows, int64_t W, int H,
                          const int* d_layers, int n, double* sums, double* partial,
                          int64_t partial_cap) {
-  fold_common(s, probs, int64_t(H) * rows * W, rows * W, rows * W, H, d_layers, n, sums, partial,
-              partial_cap);
+  fold_common<true>(s, probs, int64_t(H) * rows * W, rows * W, rows * W, H, d_layers, n, sums,
+                    partial, partial_cap);
 }
 
 // analysis.cpp:153-179 — D(i,j) = mean over heads of sqrt(sums).
