@@ -149,12 +149,18 @@ def run_b200(args, rank, local, world, dist):
     b_h2d, f_rec = ctx.measure_rates(prev)
     pairs = [(a, b, 0.0) for a, b in spec["pairs"]]
     cost = K.CostModel.for_model(cfg, f_rec, b_h2d)
-    r_c = K.calibrate_rc(cost, cfg.n_layers, L, cfg.d_model, pairs)
+    r_analytic = K.calibrate_rc(cost, cfg.n_layers, L, cfg.d_model, pairs)
+    conv = ctx.conversation(L + n_new + 64)
+    ctx.set_capture(False)
+    # calibrate_rc_measured on the device: coarse grid, then a fine grid
+    # around the coarse argmin of |T_C - T_L| (acceptance.cpp:478-487 style)
+    coarse = [round(0.02 * k, 4) for k in range(0, 21)]
+    r0, _, _ = ctx.calibrate_rc_measured(prev, conv, hist, pairs, coarse)
+    fine = sorted({min(1.0, max(0.0, round(r0 + 0.004 * k, 4))) for k in range(-5, 6)})
+    r_c, tc_f, tl_f = ctx.calibrate_rc_measured(prev, conv, hist, pairs, fine)
     plan = K.build_plan(L, cfg.n_layers, r_c, pairs)
     snap = K.KVSnapshot.compress(ctx, prev, pairs, plan, L, K.MERGE_MEAN)
     full_b, stored_b = snap.storage_report()
-    conv = ctx.conversation(L + n_new + 64)
-    ctx.set_capture(False)
 
     def step():
         return ctx.restore_and_prefill(conv, hist, snap, new)
@@ -175,6 +181,7 @@ def run_b200(args, rank, local, world, dist):
     ctx.sync()
     barrier(dist)
     clk = clocks.stop()
+    tl_c, tl_l, tl_n = ctx.restore_timeline()
     total_ms = float(np.sum(ttfts))
     total_ms = allmax(dist, total_ms, local)
     wall_total = allmax(dist, float(np.sum(walls)), local)
@@ -204,10 +211,14 @@ def run_b200(args, rank, local, world, dist):
                                f"{n_new}-token new-input prefill, 1 conversation/step/GPU",
                    "global_batch": world, "seq_len": L, "parallelism": f"dp{world} (conversation shards, no collective)",
                    "l2": "inputs (16 GB weights, 1 GB KV) larger than L2; no flush",
-                   "r_c": r_c, "plan_head": [int(x) for x in plan[:4]], "pairs": len(pairs),
+                   "r_c": r_c, "r_c_analytic": r_analytic,
+                   "plan_head": [int(x) for x in plan[:4]], "pairs": len(pairs),
                    "h2d_gbs_measured": round(b_h2d / 1e9, 2),
                    "recompute_tflops_measured": round(f_rec / 1e12, 1)},
         "restore": {k: round(v, 4) for k, v in st.items()},
+        "timeline_ms": {"compute_done": [round(x, 3) for x in tl_c],
+                        "load_done": [round(x, 3) for x in tl_l],
+                        "new_prefill_done": [round(x, 3) for x in tl_n]},
         "storage": {"full_bytes": full_b, "stored_bytes": stored_b},
         "roofline": {"bound": "tensor", "kernel": "recompute stream (K6)",
                      "achieved": round(achieved_tf, 2), "peak": peak, "unit": "TFLOP/s",

@@ -110,6 +110,7 @@ typedef struct {
   double h2d_bytes;
   double expand_bytes;    /* algorithmic bytes moved by the expand kernels */
   double recompute_flops;
+  double h2d_ms;          /* copy-engine finish of the last blob */
 } krul_restore_stats;
 
 int krul_abi_version(void);
@@ -247,6 +248,23 @@ int krul_restore_and_prefill(krul_ctx* ctx, krul_conv* conv,
                              int64_t L, const int32_t* new_tokens, int64_t n_new,
                              float* logits, krul_restore_stats* stats,
                              double* ttft_ms);
+
+/* Per-layer timeline of the last restore (ms from launch, CUDA events):
+ * compute[l] = recompute of layer l done, load[l] = layer l expanded,
+ * new_prefill[l] = new-input prefill of layer l done (0 without one). */
+int krul_restore_timeline(krul_ctx* ctx, double* compute, double* load,
+                          double* new_prefill);
+
+/* calibrate_rc_measured (scheduler.cpp:402-443) with the real device
+ * restore: per grid ratio, compress `prev` (full KV of the L-token history)
+ * under build_plan(ratio) and time the two-stream restore into `scratch`;
+ * returns argmin |T_C - T_L|. tc/tl ([n_grid], optional) get the measured
+ * stream times in sorted-grid order. */
+int krul_calibrate_rc_measured(krul_ctx* ctx, krul_conv* prev,
+                               krul_conv* scratch, const int32_t* history,
+                               int64_t L, const krul_pair* pairs, int n_pairs,
+                               const double* grid, int n_grid, int mode,
+                               double* r_c, double* tc, double* tl);
 
 /* ---- measured stream rates (calibrate_rc_measured, scheduler.cpp:402) - */
 /* Times pinned H2D bandwidth (bytes/s) and recompute throughput (flop/s)

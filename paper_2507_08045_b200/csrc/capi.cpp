@@ -721,6 +721,55 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps, doubl
   });
 }
 
+// calibrate_rc_measured (scheduler.cpp:402-443) on the device: for each grid
+// ratio, build the plan, compress the previous turn's KV (conv `prev`, full
+// span [0, L)) into a snapshot and run the real two-stream restore into
+// `scratch`; pick argmin |T_C - T_L| of the measured stream finish times
+// (strict <, ties to the smaller ratio). tc/tl (optional, [ng]) receive the
+// measured times in sorted-grid order.
+int krul_calibrate_rc_measured(krul_ctx* ctx, krul_conv* prev, krul_conv* scratch,
+                               const int32_t* hist, int64_t L, const krul_pair* pairs, int np,
+                               const double* grid, int ng, int mode, double* r_out, double* tc,
+                               double* tl) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(prev, "prev");
+    need(scratch, "scratch");
+    if (ng <= 0) fail(KRUL_E_CONFIG, "calibration grid is empty");
+    Ctx& c = *ctx->c;
+    std::vector<double> g(grid, grid + ng);
+    std::sort(g.begin(), g.end());
+    double best = g.front(), gap = 1e300;
+    for (int k = 0; k < ng; ++k) {
+      const std::vector<int64_t> p = build_plan(L, c.cfg.N, g[size_t(k)], pairs, np);
+      std::unique_ptr<Snapshot> s(snapshot_compress(c, *prev->v, pairs, np, p.data(), L, mode));
+      krul_restore_stats st{};
+      restore(c, *scratch->v, *s, hist, L, &st, nullptr, 0, nullptr, nullptr);  // warm
+      restore(c, *scratch->v, *s, hist, L, &st, nullptr, 0, nullptr, nullptr);
+      if (tc) tc[k] = st.compute_ms;
+      if (tl) tl[k] = st.load_ms;
+      const double d = std::abs(st.compute_ms - st.load_ms);
+      if (d < gap) {
+        gap = d;
+        best = g[size_t(k)];
+      }
+    }
+    *r_out = best;
+  });
+}
+
+int krul_restore_timeline(krul_ctx* ctx, double* comp, double* load, double* newp) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    if (c.tl_compute.empty()) fail(KRUL_E_STATE_CORRUPTION, "no restore has run on this context");
+    const size_t n = c.tl_compute.size();
+    if (comp) std::copy(c.tl_compute.begin(), c.tl_compute.end(), comp);
+    if (load) std::copy(c.tl_load.begin(), c.tl_load.end(), load);
+    if (newp) std::copy(c.tl_new.begin(), c.tl_new.begin() + n, newp);
+  });
+}
+
 int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A,
                     const float* B, const float* bias, int epi, float* Cout) {
   return guard([&] {

@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  // M-tile fastest: co-resident CTAs share one B (weight) tile, so each
+  // weight tile streams from HBM once while the small A panel stays in L2
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int num_k = (K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
@@ -318,7 +320,7 @@ void launch_tc(cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A, i
     KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  dim3 grid(unsigned((N + BN - 1) / BN), unsigned((M + 127) / 128));
+  dim3 grid(unsigned((M + 127) / 128), unsigned((N + BN - 1) / BN));
   kern<<<grid, 192, smem, s>>>(ta, tb, int(M), int(N), int(K), e);
   KB_LAUNCH();
 }
@@ -339,7 +341,14 @@ void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const v
                      ldb % 8 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(B) & 15) == 0 && K >= 1;
   if (tc_ok) {
-    if (N >= 2048 && M >= 256)
+    // wave efficiency of each tile width on this device; prefer the wider
+    // (higher arithmetic intensity) tile unless it strands SMs
+    const int64_t mt = (M + 127) / 128, sms = c.sm_count > 0 ? c.sm_count : 148;
+    auto eff = [&](int64_t bn) {
+      const int64_t t = mt * ((N + bn - 1) / bn);
+      return double(t) / double(((t + sms - 1) / sms) * sms);
+    };
+    if (N >= 256 && eff(256) >= 0.8 * eff(128))
       launch_tc<256, 4>(s, M, N, K, A, lda, B, ldb, e);
     else
       launch_tc<128, 6>(s, M, N, K, A, lda, B, ldb, e);

@@ -23,7 +23,8 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
 void check_tokens(const Ctx& c, const int32_t* t, int64_t n);
 int32_t* upload_tokens(Ctx& c, cudaStream_t s, const int32_t* t, int64_t n, DevBuf& buf);
 void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_tok, int64_t n,
-                  int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits);
+                  int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits,
+                  cudaEvent_t* layer_done = nullptr);
 void prefill(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, float* logits);
 void prefill_new(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, float* logits);
 void decode_step(Ctx& c, Conv& conv, int32_t tok, float* logits);

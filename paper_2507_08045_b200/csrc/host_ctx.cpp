@@ -98,7 +98,7 @@ Ctx::~Ctx() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
   for (auto e : ev_pool) cudaEventDestroy(e);
-  for (auto s : {s_comp, s_load, s_new, s_est})
+  for (auto s : {s_comp, s_load, s_new, s_est, s_exp})
     if (s) cudaStreamDestroy(s);
 }
 

@@ -27,6 +27,7 @@ Ctx* ctx_create(int device, const krul_model_desc& desc) {
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_load, cudaStreamNonBlocking));
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_new, cudaStreamNonBlocking));
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_est, cudaStreamNonBlocking));
+    KB_CUDA(cudaStreamCreateWithFlags(&c->s_exp, cudaStreamNonBlocking));
     KB_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     // RoPE table: angles in double, cast to float (engine.cpp:131-136).
     const int half = cfg.hd / 2;
@@ -330,7 +331,8 @@ static AttnArgs capture_for_layer(const Ctx& c, const AttnArgs& base, int l) {
 // cache (fresh prefill when pos0 == 0; new-input prefill otherwise).
 // Per-layer waits (restore events) are honoured when given.
 void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_tok, int64_t n,
-                  int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits) {
+                  int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits,
+                  cudaEvent_t* layer_done) {
   const Cfg& g = c.cfg;
   WS w = ws_get(c, set, n);
   AttnArgs cap{};
@@ -345,6 +347,7 @@ void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_
     }
     AttnArgs a = capture_for_layer(c, cap, l);
     layer_forward(c, s, w, conv, l, hin, n, pos0, n, hout, &a);
+    if (layer_done) KB_CUDA(cudaEventRecord(layer_done[l], s));
     std::swap(hin, hout);
   }
   launch_logits(c, s, hin + (n - 1) * g.d, d_logits);

@@ -175,9 +175,11 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
 
   c.reset_events();
   cudaEvent_t ev0 = c.event(), ev_c_end = c.event(), ev_l_end = c.event(), ev_end = c.event();
-  std::vector<cudaEvent_t> computed(size_t(g.N)), loaded(size_t(g.N));
+  cudaEvent_t ev_h2d_end = c.event();
+  std::vector<cudaEvent_t> computed(size_t(g.N)), loaded(size_t(g.N)), newp(size_t(g.N));
   for (auto& e : computed) e = c.event();
   for (auto& e : loaded) e = c.event();
+  for (auto& e : newp) e = c.event();
 
   cudaStream_t sc = c.s_comp, sl = c.s_load;
   char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(snap.total, 256)));
@@ -188,22 +190,34 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
 
   KB_CUDA(cudaEventRecord(ev0, sc));
   KB_CUDA(cudaStreamWaitEvent(sl, ev0, 0));
-  // ---- load stream: K4 (H2D) + K5 (expand) per blob in service order
+  KB_CUDA(cudaStreamWaitEvent(c.s_exp, ev0, 0));
+  // ---- load stream: K4 H2D copies back to back on the copy engine; K5
+  // expand kernels on their own stream behind each blob's copy event, so
+  // the PCIe link never idles while a scatter runs.
   double h2d = 0, expand_bytes = 0;
-  for (const auto& b : snap.blobs) {
+  std::vector<cudaEvent_t> copied(snap.blobs.size());
+  for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
+    const auto& b = snap.blobs[bi];
+    copied[bi] = c.event();
     if (b.bytes) {
       KB_CUDA(cudaMemcpyAsync(stg + b.off, static_cast<char*>(snap.host.p) + b.off, b.bytes,
                               cudaMemcpyHostToDevice, sl));
       h2d += double(b.bytes);
     }
+    KB_CUDA(cudaEventRecord(copied[bi], sl));
+  }
+  KB_CUDA(cudaEventRecord(ev_h2d_end, sl));
+  for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
+    const auto& b = snap.blobs[bi];
+    KB_CUDA(cudaStreamWaitEvent(c.s_exp, copied[bi], 0));
     for (int o : b.owners) {
       if (o < 0) continue;
-      launch_expand(c, sl, stg + b.off, b.start, L, conv, o, p[size_t(o)]);
+      launch_expand(c, c.s_exp, stg + b.off, b.start, L, conv, o, p[size_t(o)]);
       expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;
-      KB_CUDA(cudaEventRecord(loaded[size_t(o)], sl));
+      KB_CUDA(cudaEventRecord(loaded[size_t(o)], c.s_exp));
     }
   }
-  KB_CUDA(cudaEventRecord(ev_l_end, sl));
+  KB_CUDA(cudaEventRecord(ev_l_end, c.s_exp));
   // ---- compute stream: K6 pyramid recompute
   if (p[0] > 0) {
     enqueue_partial(c, sc, conv, d_tok, p, false, computed.data());
@@ -220,7 +234,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     waits.insert(waits.end(), computed.begin(), computed.end());
     waits.insert(waits.end(), loaded.begin(), loaded.end());
     conv.len = L;
-    forward_rows(c, sn, 1, conv, d_new, n_new, L, d_logits, &waits);
+    forward_rows(c, sn, 1, conv, d_new, n_new, L, d_logits, &waits, newp.data());
     KB_CUDA(cudaEventRecord(ev_end, sn));
     KB_CUDA(cudaStreamWaitEvent(sc, ev_end, 0));
     KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end, 0));
@@ -234,12 +248,31 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     KB_CUDA(cudaMemcpyAsync(logits, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sc));
   KB_CUDA(cudaStreamSynchronize(sc));
   KB_CUDA(cudaStreamSynchronize(sl));
+  KB_CUDA(cudaStreamSynchronize(c.s_exp));
 
-  float tc = 0, tl = 0, te = 0;
+  float tc = 0, tl = 0, te = 0, th = 0;
   KB_CUDA(cudaEventElapsedTime(&tc, ev0, ev_c_end));
   KB_CUDA(cudaEventElapsedTime(&tl, ev0, ev_l_end));
   KB_CUDA(cudaEventElapsedTime(&te, ev0, ev_end));
+  KB_CUDA(cudaEventElapsedTime(&th, ev0, ev_h2d_end));
   if (ttft_ms) *ttft_ms = te;
+  // measured per-layer timeline (ms from restore launch), the device
+  // counterpart of PipelineTrace (scheduler.hpp:71-97)
+  c.tl_compute.assign(size_t(g.N), 0.0);
+  c.tl_load.assign(size_t(g.N), 0.0);
+  c.tl_new.assign(size_t(g.N), 0.0);
+  for (int l = 0; l < g.N; ++l) {
+    float a = 0, b = 0, e = 0;
+    KB_CUDA(cudaEventElapsedTime(&a, ev0, computed[size_t(l)]));
+    KB_CUDA(cudaEventElapsedTime(&b, ev0, loaded[size_t(l)]));
+    c.tl_compute[size_t(l)] = a;
+    c.tl_load[size_t(l)] = b;
+    if (new_tok) {
+      KB_CUDA(cudaEventElapsedTime(&e, ev0, newp[size_t(l)]));
+      c.tl_new[size_t(l)] = e;
+    }
+  }
+  c.tl_h2d_ms = th;
   if (st) {
     Cost cm;
     cm.kv_dim = g.kvd();
@@ -258,6 +291,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     st->h2d_bytes = h2d;
     st->expand_bytes = expand_bytes;
     st->recompute_flops = fl;
+    st->h2d_ms = th;
   }
 }
 

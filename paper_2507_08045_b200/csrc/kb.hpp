@@ -120,6 +120,7 @@ struct Ctx {
   Cfg cfg;
   size_t esz = 4;  // compute element size
   cudaStream_t s_comp = nullptr, s_load = nullptr, s_new = nullptr, s_est = nullptr;
+  cudaStream_t s_exp = nullptr;  // expand (K5) behind the H2D copies
   int sm_count = 0;
 
   // weights
@@ -158,8 +159,10 @@ struct Ctx {
   int64_t dec_width = 0;
   bool dec_valid = false;
 
-  // restore staging
+  // restore staging + last measured timeline (ms from launch)
   DevBuf staging;
+  std::vector<double> tl_compute, tl_load, tl_new;
+  double tl_h2d_ms = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
 

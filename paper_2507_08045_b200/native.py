@@ -100,7 +100,7 @@ class RestoreStats(C.Structure):
     _fields_ = [("restore_ms", C.c_double), ("compute_ms", C.c_double), ("load_ms", C.c_double),
                 ("bubble_compute", C.c_double), ("bubble_load", C.c_double),
                 ("h2d_bytes", C.c_double), ("expand_bytes", C.c_double),
-                ("recompute_flops", C.c_double)]
+                ("recompute_flops", C.c_double), ("h2d_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -271,6 +271,25 @@ class Context:
         _check(lib().krul_classify(self.h, C.c_double(gamma), C.c_double(initial_frac),
                                    C.c_double(recent_frac), _p(avg), _p(ir)))
         return avg, [l for l in range(N) if ir[l]], [l for l in range(N) if not ir[l]]
+
+    def restore_timeline(self):
+        """Per-layer ms from restore launch: (compute[l], load[l], new_prefill[l])."""
+        N = self.cfg.n_layers
+        a, b, c = (np.zeros(N, np.float64) for _ in range(3))
+        _check(lib().krul_restore_timeline(self.h, _p(a), _p(b), _p(c)))
+        return a, b, c
+
+    def calibrate_rc_measured(self, prev, scratch, history, pairs, grid, mode=1):
+        """scheduler.cpp:402-443 on the device -> (r_c, tc[ms], tl[ms]) over the sorted grid."""
+        t = np.ascontiguousarray(history, np.int32)
+        arr, n = _pairs(pairs)
+        g = np.ascontiguousarray(sorted(grid), np.float64)
+        tc, tl = np.zeros(len(g)), np.zeros(len(g))
+        r = C.c_double()
+        _check(lib().krul_calibrate_rc_measured(self.h, prev.h, scratch.h, _p(t), C.c_int64(t.size),
+                                                arr, n, _p(g), len(g), mode, C.byref(r), _p(tc),
+                                                _p(tl)))
+        return r.value, tc, tl
 
     def measure_rates(self, scratch):
         b, f = C.c_double(), C.c_double()
