@@ -276,6 +276,9 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps,
 /* C[M,N] = A[M,K] B[N,K]^T through the engine GEMM (inputs rounded to the
  * ctx dtype; tcgen05 path for bf16). epi: 0 = f32 store, 2 = resid (C +=),
  * 3 = tanh(acc + bias), 4 = swiglu over column pairs (C is [M, N/2]). */
+/* Kernel-tuning aid: times `iters` device-resident bf16 GEMMs (not a product entry). */
+int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
+                          int splits, int iters, float* ms_per_iter);
 int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K,
                     const float* A, const float* B, const float* bias, int epi,
                     float* C);

@@ -813,4 +813,60 @@ int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float*
   });
 }
 
+
+// Device-resident GEMM timing for kernel tuning (not on the product path):
+// random bf16 A[M,K], B[N,K], `iters` back-to-back launches timed with CUDA
+// events on the compute stream. force: 0 planner, 1 1-SM BN256, 2 1-SM
+// BN128, 3 pair, 4 pair BK128; splits: 0 planner.
+int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
+                          int splits, int iters, float* ms_per_iter) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    if (c.cfg.dtype != KRUL_BF16) fail(KRUL_E_CONFIG, "gemm bench needs a bf16 context");
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t s = c.s_comp;
+    DevBuf a, b, out, res, out2, bias;
+    void* da = a.ensure(size_t(M * K) * 2);
+    void* db = b.ensure(size_t(N * K) * 2);
+    launch_init_uniform(c, s, da, M * K, 1, 1, 1.0f);
+    launch_init_uniform(c, s, db, N * K, 1, 2, 0.02f);
+    Epi e;
+    e.kind = epi;
+    e.out = out.ensure(size_t(M * N) * 4 + 16);
+    e.ldo = epi == Epi::SWIGLU ? N / 2 : N;
+    if (epi == Epi::RESID) {
+      e.resid = static_cast<float*>(res.ensure(size_t(M * N) * 4));
+      KB_CUDA(cudaMemsetAsync(const_cast<float*>(e.resid), 0, size_t(M * N) * 4, s));
+      e.ldr = N;
+      e.out2 = out2.ensure(size_t(M * N) * 2);
+      e.ldo2 = N;
+    }
+    if (epi == Epi::TANH) {
+      e.bias = static_cast<float*>(bias.ensure(size_t(N) * 4));
+      KB_CUDA(cudaMemsetAsync(const_cast<float*>(e.bias), 0, size_t(N) * 4, s));
+    }
+    g_gemm_force = force;
+    g_gemm_splits = splits;
+    try {
+      for (int i = 0; i < 2; ++i) gemm(c, s, M, N, K, da, K, db, K, e);
+      cudaEvent_t e0 = c.event(), e1 = c.event();
+      KB_CUDA(cudaEventRecord(e0, s));
+      for (int i = 0; i < iters; ++i) gemm(c, s, M, N, K, da, K, db, K, e);
+      KB_CUDA(cudaEventRecord(e1, s));
+      KB_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      KB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      *ms_per_iter = ms / float(iters);
+    } catch (...) {
+      g_gemm_force = 0;
+      g_gemm_splits = 0;
+      throw;
+    }
+    g_gemm_force = 0;
+    g_gemm_splits = 0;
+    c.reset_events();
+  });
+}
+
 }  // extern "C"

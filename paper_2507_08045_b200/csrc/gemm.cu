@@ -9,6 +9,7 @@
 //    shapes TMA cannot describe, e.g. rows not 16-byte aligned).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -16,6 +17,9 @@
 #include "kb.hpp"
 
 namespace kb {
+
+int g_gemm_force = 0;   // debug: 0 auto, 1 1-SM BN256, 2 1-SM BN128, 3 pair, 4 pair BK128
+int g_gemm_splits = 0;  // debug: force the split-K count (0 = planner)
 
 // ---------------------------------------------------------------- epilogue
 template <class T>
@@ -176,10 +180,282 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 }  // namespace tc
 
-template <int BN, int STAGES>
+// Element-wise epilogue on one accumulator value (row, col) — used by the
+// coalesced (smem-transposed) tcgen05 epilogue and by the split-K reduce.
+template <class T>
+__device__ __forceinline__ void epi_elem(const Epi& e, int64_t r, int64_t c, float v) {
+  switch (e.kind) {
+    case Epi::F32:
+      static_cast<float*>(e.out)[r * e.ldo + c] = v;
+      break;
+    case Epi::CDT:
+      static_cast<T*>(e.out)[r * e.ldo + c] = fromf<T>(v);
+      break;
+    case Epi::RESID: {  // engine.cpp:190 / :192
+      const float y = e.bias ? v + e.bias[c] : v;
+      const float h = e.resid[r * e.ldr + c] + y;
+      static_cast<float*>(e.out)[r * e.ldo + c] = h;
+      if (e.out2) static_cast<T*>(e.out2)[r * e.ldo2 + c] = fromf<T>(h);
+      break;
+    }
+    case Epi::TANH:  // engine.cpp:191
+      static_cast<T*>(e.out)[r * e.ldo + c] = fromf<T>(tanhf(v + e.bias[c]));
+      break;
+  }
+}
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
+
+// One 32x32 accumulator block of an epilogue warp: TMEM lanes row0..row0+31
+// (this warp's quadrant), columns col0..col0+31. tcgen05.ld gives thread =
+// row; the block is transposed through padded smem (`my`, 32x33 floats) so
+// every global access below is a 128-byte row-coalesced warp access. The
+// residual operand (RESID) is prefetched before the TMEM load so its latency
+// overlaps it. P != nullptr stores an fp32 split-K partial instead.
+__device__ __forceinline__ void epi_block(const Epi& e, float* my, uint32_t taddr, int64_t row0,
+                                          int64_t col0, int64_t M, int64_t N, float* P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t col = col0 + lane;
+  const bool cok = col < N;
+  float rv[32];
+  const bool resid = !P && e.kind == Epi::RESID;
+  if (resid) {
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t r = row0 + rr;
+      rv[rr] = (r < M && cok) ? e.resid[r * e.ldr + col] : 0.f;
+    }
+  }
+  float v[32];
+  tc::tmem_ld32(taddr, v);
+  if (!P && e.kind == Epi::NONE) return;
+  if (!P && e.kind == Epi::F32_DIRECT) {  // debug: row-per-thread 16-byte stores, no transpose
+    const int64_t r = row0 + lane;
+    if (r < M) {
+      float4* o = reinterpret_cast<float4*>(static_cast<float*>(e.out) + r * e.ldo + col0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) my[lane * 33 + j] = v[j];
+  __syncwarp();
+  if (!P && e.kind == Epi::STAGE_ONLY) {  // debug: transpose through smem, no global access
+    float acc = 0.f;
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) acc += my[rr * 33 + lane];
+    if (acc == 12345.678f) static_cast<float*>(e.out)[lane] = acc;
+    __syncwarp();
+    return;
+  }
+  if (P) {
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t r = row0 + rr;
+      if (r < M && cok) P[r * N + col] = my[rr * 33 + lane];
+    }
+  } else if (e.kind == Epi::SWIGLU) {  // gate/up adjacent columns: even lane writes silu(g)*u
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t r = row0 + rr;
+      const float g = my[rr * 33 + lane];
+      const float up = __shfl_down_sync(0xffffffffu, g, 1);
+      if (r < M && col + 1 < N && !(lane & 1))
+        static_cast<bf16*>(e.out)[r * e.ldo + col / 2] = fromf<bf16>(silu_mul(g, up));
+    }
+  } else if (resid) {
+    const float b = (e.bias && cok) ? e.bias[col] : 0.f;
+    float* o = static_cast<float*>(e.out);
+    bf16* o2 = static_cast<bf16*>(e.out2);
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t r = row0 + rr;
+      if (r < M && cok) {
+        const float h = rv[rr] + (my[rr * 33 + lane] + b);
+        o[r * e.ldo + col] = h;
+        if (o2) o2[r * e.ldo2 + col] = fromf<bf16>(h);
+      }
+    }
+  } else {
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t r = row0 + rr;
+      if (r < M && cok) epi_elem<bf16>(e, r, col, my[rr * 33 + lane]);
+    }
+  }
+  __syncwarp();
+}
+
+// Epilogue kinds resolved at compile time (EK_GENERIC = runtime e.kind via
+// epi_block, used when the output cannot be described by a TMA map).
+enum : int { EK_F32 = 0, EK_CDT = 1, EK_RESID = 2, EK_TANH = 3, EK_SWIGLU = 4, EK_NONE = 5,
+             EK_PARTIAL = 8, EK_GENERIC = 9 };
+
+namespace tc {
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y,
+                                             int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+}  // namespace tc
+
+// One accumulator tile row-block of an epilogue warp through TMA stores.
+// The warp owns TMEM lanes [32q, 32q+32) = output rows row0..row0+31; thread
+// = row. Outputs are packed into a 32-row x 128-byte staging tile in the
+// TMA SWIZZLE_128B layout (16-byte piece j of row r at piece j ^ (r & 7):
+// conflict-free st.shared.v4), then one lane issues the bulk tensor store
+// (rows >= M and columns >= N are clipped by the TMA unit). Two staging
+// tiles per warp alternate; a tile is rewritten only after its previous
+// store has finished reading shared memory.
+//   F32 / RESID / PARTIAL : 32 accumulator columns per staging tile (f32)
+//   CDT / TANH            : 64 columns (bf16)
+//   SWIGLU                : 128 accumulator columns -> 64 bf16 outputs
+// RESID reads its residual rows directly (16-byte loads issued before the
+// TMEM load) and writes the optional bf16 copy with direct 16-byte stores.
+template <int KIND, int BN>
+__device__ __forceinline__ void epi_unit(const Epi& e, const CUtensorMap* tmC, unsigned char* stage,
+                                         int& sbuf, uint32_t tbase, int64_t row0, int64_t col0,
+                                         int64_t M, int64_t N, int ks) {
+  constexpr int ACC = (KIND == EK_SWIGLU) ? 128 : (KIND == EK_CDT || KIND == EK_TANH) ? 64 : 32;
+  constexpr int PIECES = 128 / (ACC / 32) / 16;  // 16-byte pieces per 32-column chunk
+  const int lane = threadIdx.x & 31;
+  const int64_t r = row0 + lane;
+  const bool rok = r < M;
+#pragma unroll 1
+  for (int t = 0; t < BN; t += ACC) {
+    if (col0 + t >= N) break;
+    unsigned char* tile = stage + sbuf * 4096;
+    if (lane == 0) tc::bulk_wait_read1();
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < ACC; c += 32) {
+      const int64_t cc = col0 + t + c;  // first accumulator column of this chunk
+      float rv[32];
+      if constexpr (KIND == EK_RESID) {
+        if (rok && cc + 32 <= N && ((e.ldr & 3) == 0)) {
+          const float4* src = reinterpret_cast<const float4*>(e.resid + r * e.ldr + cc);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 x = __ldg(src + j);
+            rv[4 * j] = x.x;
+            rv[4 * j + 1] = x.y;
+            rv[4 * j + 2] = x.z;
+            rv[4 * j + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rv[j] = (rok && cc + j < N) ? e.resid[r * e.ldr + cc + j] : 0.f;
+        }
+      }
+      float v[32];
+      tc::tmem_ld32(tbase + uint32_t(t + c), v);
+      uint32_t w[32];  // packed output words of this chunk for this row
+      if constexpr (KIND == EK_F32 || KIND == EK_PARTIAL || KIND == EK_NONE) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
+      } else if constexpr (KIND == EK_RESID) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float b = e.bias && cc + j < N ? __ldg(e.bias + cc + j) : 0.f;
+          w[j] = __float_as_uint(rv[j] + (v[j] + b));
+        }
+        if (e.out2 && rok) {
+          bf16* o2 = static_cast<bf16*>(e.out2) + r * e.ldo2 + cc;
+          if (cc + 32 <= N && ((e.ldo2 & 7) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 pk;
+              pk.x = tc::pack_bf16(__uint_as_float(w[8 * j]), __uint_as_float(w[8 * j + 1]));
+              pk.y = tc::pack_bf16(__uint_as_float(w[8 * j + 2]), __uint_as_float(w[8 * j + 3]));
+              pk.z = tc::pack_bf16(__uint_as_float(w[8 * j + 4]), __uint_as_float(w[8 * j + 5]));
+              pk.w = tc::pack_bf16(__uint_as_float(w[8 * j + 6]), __uint_as_float(w[8 * j + 7]));
+              reinterpret_cast<uint4*>(o2)[j] = pk;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (cc + j < N) o2[j] = __float2bfloat16_rn(__uint_as_float(w[j]));
+          }
+        }
+      } else if constexpr (KIND == EK_CDT) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j] = tc::pack_bf16(v[2 * j], v[2 * j + 1]);
+      } else if constexpr (KIND == EK_TANH) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float b0 = cc + 2 * j < N ? __ldg(e.bias + cc + 2 * j) : 0.f;
+          const float b1 = cc + 2 * j + 1 < N ? __ldg(e.bias + cc + 2 * j + 1) : 0.f;
+          w[j] = tc::pack_bf16(tanhf(v[2 * j] + b0), tanhf(v[2 * j + 1] + b1));
+        }
+      } else if constexpr (KIND == EK_SWIGLU) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          w[j] = tc::pack_bf16(silu_mul(v[4 * j], v[4 * j + 1]), silu_mul(v[4 * j + 2], v[4 * j + 3]));
+      }
+      if constexpr (KIND != EK_NONE) {
+        const int p0 = (c / 32) * PIECES;
+#pragma unroll
+        for (int j = 0; j < PIECES; ++j) {
+          const int piece = (p0 + j) ^ (lane & 7);
+          *reinterpret_cast<uint4*>(tile + lane * 128 + piece * 16) =
+              make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+        }
+      }
+    }
+    if constexpr (KIND != EK_NONE) {
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int x = int(KIND == EK_SWIGLU ? (col0 + t) / 2 : col0 + t);
+        if constexpr (KIND == EK_PARTIAL)
+          tc::tma_store_3d(tmC, tile, x, int(row0), ks);
+        else
+          tc::tma_store_2d(tmC, tile, x, int(row0));
+        tc::bulk_commit();
+      }
+      sbuf ^= 1;
+    }
+  }
+}
+
+// Persistent warp-specialised tcgen05 GEMM, C[M,N] = A[M,K] B[N,K]^T.
+//   warp 0      : TMA producer (A 128x64 + B BNx64 bf16 tiles, SW128) into an
+//                 STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1      : TMEM owner + single-thread tcgen05.mma issuer; two TMEM
+//                 accumulators (2 x BN fp32 columns) so the epilogue of unit
+//                 i overlaps the mainloop of unit i+1 (tmem_full/tmem_empty)
+//   warps 2..5  : epilogue; warp w reads TMEM lanes 32*(w%4).. via
+//                 tcgen05.ld.32x32b, transposes each 32x32 block through
+//                 padded smem so global stores/loads are row-coalesced, then
+//                 applies the fused epilogue (or stores an fp32 split-K
+//                 partial).
+// Work units = (m_tile, n_tile, k_split), m fastest: co-resident CTAs share
+// the weight (B) tile so each weight tile streams from HBM about once.
+template <int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              int M, int N, int K, Epi e) {
+              const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int mt, int nt, int splits, int kb_per, Epi e,
+              float* __restrict__ partial) {
   constexpr int BM = 128, BK = 64;
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   extern __shared__ unsigned char smem_raw[];
@@ -187,23 +463,26 @@ __global__ void __launch_bounds__(192, 1)
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = base;
   unsigned char* sB = base + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  float* stg = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // 4 warps x 2 x 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + 4 * 2 * 1024);
   uint64_t* empty = full + STAGES;
-  uint64_t* accum = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // M-tile fastest: co-resident CTAs share one B (weight) tile, so each
-  // weight tile streams from HBM once while the small A panel stays in L2
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int num_k = (K + BK - 1) / BK;
+  const int units = mt * nt * splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(accum, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -211,7 +490,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      tc::smem_u32(tmem_slot)),
-                 "r"(uint32_t(BN)));
+                 "r"(uint32_t(2 * BN)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc::fence_before();
@@ -221,57 +500,352 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        tc::mbar_wait(&empty[s], ph ^ 1);
-        tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
-        tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int m = u % mt, rest = u / mt, n = rest % nt, ks = rest / nt;
+        const int k0 = ks * kb_per, k1 = min(num_k, k0 + kb_per);
+        for (int kb = k0; kb < k1; ++kb) {
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+          tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m * BM);
+          tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n * BN);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
                                  (uint32_t(BM >> 4) << 24);
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        tc::mbar_wait(&full[s], ph);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int ks = u / mt / nt;
+        const int k0 = ks * kb_per, k1 = min(num_k, k0 + kb_per);
+        tc::mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
         tc::fence_after();
+        const uint32_t d = tmem + uint32_t(acc * BN);
+        for (int kb = k0; kb < k1; ++kb) {
+          tc::mbar_wait(&full[s], ph);
+          tc::fence_after();
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t da = tc::sw128_desc(sA + s * A_BYTES + k * 32);
-          const uint64_t db = tc::sw128_desc(sB + s * B_BYTES + k * 32);
-          tc::mma_bf16(tmem, da, db, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = tc::sw128_desc(sA + s * A_BYTES + k * 32);
+            const uint64_t db = tc::sw128_desc(sB + s * B_BYTES + k * 32);
+            tc::mma_bf16(d, da, db, idesc, (kb > k0 || k > 0) ? 1u : 0u);
+          }
+          tc::mma_commit(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
-        tc::mma_commit(&empty[s]);
+        tc::mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
       }
-      tc::mma_commit(accum);
     }
-  } else {  // epilogue warps 2..5 -> TMEM lanes 32*(warp%4)
-    tc::mbar_wait(accum, 0);
-    tc::fence_after();
-    const int lane_base = 32 * (warp & 3);
-    const int64_t r = int64_t(m0) + lane_base + lane;
-    float v[32];
+  } else {  // epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    float* my = stg + q * 32 * 33;
+    unsigned char* stage = reinterpret_cast<unsigned char*>(stg) + q * 8192;
+    int sbuf = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int m = u % mt, rest = u / mt, n = rest % nt, ks = rest / nt;
+      tc::mbar_wait(&tfull[acc], aph);
+      tc::fence_after();
+      const int64_t row0 = int64_t(m) * BM + 32 * q;
+      float* P = partial ? partial + int64_t(ks) * M * N : nullptr;
+      if constexpr (KIND == EK_GENERIC) {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      tc::tmem_ld32(tmem + (uint32_t(lane_base) << 16) + uint32_t(c), v);
-      const int64_t col = int64_t(n0) + c;
-      if (r < M && col < N) {
-        const int nv = int(N - col < 32 ? N - col : 32);
-        epi_apply<bf16>(e, r, col, v, nv);
+        for (int c = 0; c < BN; c += 32) {
+          if (int64_t(n) * BN + c >= N) break;
+          epi_block(e, my, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + c), row0,
+                    int64_t(n) * BN + c, M, N, P);
+        }
+      } else {
+        epi_unit<KIND, BN>(e, &tmC, stage, sbuf, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN),
+                           row0, int64_t(n) * BN, M, N, ks);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&tempty[acc])) : "memory");
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
       }
     }
   }
-  __syncwarp();
+  if (warp >= 2 && lane == 0) tc::bulk_wait_all();
   tc::fence_before();
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(uint32_t(BN)));
+                 "r"(uint32_t(2 * BN)));
+  }
+}
+
+// ---------------------------------------------------------------- 2-SM pair
+namespace tc {
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of CTA rank 0
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion bytes land on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerMask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+}  // namespace tc
+
+// CTA-pair (cta_group::2) variant for M > 128: the pair computes a 256x256
+// tile; each CTA stages its own 128-row half of A and its own 128-row half
+// of B (32 KB per k-block instead of 48 KB for a 1-SM 128x256 tile, so the
+// L2->SM feed per MAC drops by a third), the leader's single thread issues
+// M=256 x N=256 MMAs that read both CTAs' shared memory, and each CTA's
+// TMEM receives its 128 accumulator rows. Same double-buffered TMEM and
+// epilogue as k_gemm_tc; the leader's tmem_empty barrier collects the
+// epilogue warps of both CTAs.
+template <int STAGES, int KSUB, int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int mt, int nt, int splits, int kb_per, Epi e,
+               float* __restrict__ partial) {
+  constexpr int BK = 64 * KSUB, BN = 256;  // KSUB 64-wide SW128 sub-tiles per stage
+  constexpr uint32_t SUB = 128 * 64 * 2;
+  constexpr uint32_t A_BYTES = SUB * KSUB, B_BYTES = SUB * KSUB;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = base;
+  unsigned char* sB = base + STAGES * A_BYTES;
+  float* stg = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // 4 warps x 2 x 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + 4 * 2 * 1024);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2] (leader: 8 arrivals = 4 warps x 2 CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cta_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int num_k = (K + BK - 1) / BK;
+  const int units = mt * nt * splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc::fence_before();
+  tc::cluster_sync();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs): own A half + own B half
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int m = u % mt, rest = u / mt, n = rest % nt, ks = rest / nt;
+        const int k0 = ks * kb_per, k1 = min(num_k, k0 + kb_per);
+        for (int kb = k0; kb < k1; ++kb) {
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) tc::mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+#pragma unroll
+          for (int j = 0; j < KSUB; ++j) {
+            tc::tma_load_2d_pair(sA + s * A_BYTES + j * SUB, &tmA, &full[s], kb * BK + 64 * j,
+                                 m * 256 + int(rank) * 128);
+            tc::tma_load_2d_pair(sB + s * B_BYTES + j * SUB, &tmB, &full[s], kb * BK + 64 * j,
+                                 n * 256 + int(rank) * 128);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // MMA issuer (pair leader)
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(256 >> 3) << 17) |
+                                 (uint32_t(256 >> 4) << 24);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int u = cid; u < units; u += ncl) {
+        const int ks = u / mt / nt;
+        const int k0 = ks * kb_per, k1 = min(num_k, k0 + kb_per);
+        tc::mbar_wait(&tempty[acc], aph ^ 1);
+        tc::fence_after();
+        const uint32_t d = tmem + uint32_t(acc * BN);
+        for (int kb = k0; kb < k1; ++kb) {
+          tc::mbar_wait(&full[s], ph);
+          tc::fence_after();
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t off = (k >> 2) * SUB + (k & 3) * 32;
+            const uint64_t da = tc::sw128_desc(sA + s * A_BYTES + off);
+            const uint64_t db = tc::sw128_desc(sB + s * B_BYTES + off);
+            tc::mma_bf16_pair(d, da, db, idesc, (kb > k0 || k > 0) ? 1u : 0u);
+          }
+          tc::mma_commit_pair(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tc::mma_commit_pair(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else {  // epilogue warps 2..5 of both CTAs
+    const int q = warp & 3;
+    float* my = stg + q * 32 * 33;
+    unsigned char* stage = reinterpret_cast<unsigned char*>(stg) + q * 8192;
+    int sbuf = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int u = cid; u < units; u += ncl) {
+      const int m = u % mt, rest = u / mt, n = rest % nt, ks = rest / nt;
+      tc::mbar_wait(&tfull[acc], aph);
+      tc::fence_after();
+      const int64_t row0 = int64_t(m) * 256 + int64_t(rank) * 128 + 32 * q;
+      float* P = partial ? partial + int64_t(ks) * M * N : nullptr;
+      if constexpr (KIND == EK_GENERIC) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (int64_t(n) * BN + c >= N) break;
+          epi_block(e, my, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + c), row0,
+                    int64_t(n) * BN + c, M, N, P);
+        }
+      } else {
+        epi_unit<KIND, BN>(e, &tmC, stage, sbuf, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN),
+                           row0, int64_t(n) * BN, M, N, ks);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::arrive_leader(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  if (warp >= 2 && lane == 0) tc::bulk_wait_all();
+  tc::fence_before();
+  tc::cluster_sync();
+  if (warp == 1) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+  }
+}
+
+// Deterministic split-K reduction (fixed split order) + fused epilogue; four
+// consecutive columns per thread (128-bit partial loads) when N % 4 == 0.
+template <class T>
+__global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t M, int64_t N,
+                                Epi e) {
+  const int64_t MN = M * N;
+  if ((N & 3) == 0) {
+    const int64_t q = N >> 2, total = M * q;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+      const int64_t r = i / q, c = (i % q) * 4;
+      float4 a = *reinterpret_cast<const float4*>(P + r * N + c);
+      for (int s = 1; s < splits; ++s) {
+        const float4 b = *reinterpret_cast<const float4*>(P + int64_t(s) * MN + r * N + c);
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      if (e.kind == Epi::SWIGLU) {
+        T* o = static_cast<T*>(e.out) + r * e.ldo + c / 2;
+        o[0] = fromf<T>(silu_mul(a.x, a.y));
+        o[1] = fromf<T>(silu_mul(a.z, a.w));
+      } else {
+        epi_elem<T>(e, r, c, a.x);
+        epi_elem<T>(e, r, c + 1, a.y);
+        epi_elem<T>(e, r, c + 2, a.z);
+        epi_elem<T>(e, r, c + 3, a.w);
+      }
+    }
+    return;
+  }
+  const bool sw = e.kind == Epi::SWIGLU;
+  const int64_t cols = sw ? N / 2 : N;
+  const int64_t total = M * cols;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    if (sw) {
+      float g = 0.f, u = 0.f;
+      for (int s = 0; s < splits; ++s) {
+        const float* p = P + int64_t(s) * MN + r * N + 2 * c;
+        g += p[0];
+        u += p[1];
+      }
+      static_cast<T*>(e.out)[r * e.ldo + c] = fromf<T>(silu_mul(g, u));
+    } else {
+      float a = 0.f;
+      for (int s = 0; s < splits; ++s) a += P[int64_t(s) * MN + r * N + c];
+      epi_elem<T>(e, r, c, a);
+    }
   }
 }
 
@@ -308,21 +882,166 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
   return m;
 }
 
-template <int BN, int STAGES>
-void launch_tc(cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
-               const void* B, int64_t ldb, const Epi& e) {
-  const CUtensorMap ta = make_map(A, M, K, lda, 128);
-  const CUtensorMap tb = make_map(B, N, K, ldb, BN);
-  const size_t smem = 1024 + size_t(STAGES) * (128 * 64 * 2 + BN * 64 * 2) + 8 * (2 * STAGES + 1) + 16;
-  auto kern = k_gemm_tc<BN, STAGES>;
+struct GemmPlan {
+  int bn = 256, splits = 1, kb_per = 1, grid = 1;
+  bool pair = false;  // cta_group::2, 256x256 tiles
+};
+
+// Pick the kernel (1-SM 128xBN or 2-SM 256x256), tile width and split-K
+// count with a small cost model (ns). Per k-block time = max(MMA issue time,
+// weight bytes streamed from HBM by this SM (shared by the co-resident
+// m-tiles), operand bytes through L2 -> SM at the measured ~75 B/ns/SM);
+// times the k-blocks on the busiest SM, plus the split-K partial round trip.
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms) {
+  const int64_t num_k = (K + 63) / 64;
+  const int force = g_gemm_force;
+  GemmPlan best;
+  double best_t = 1e30;
+  const double l2_bw = 75.0, hbm_bw = 6000.0, clk = 1.85;
+  for (int variant = 0; variant < 3; ++variant) {
+    const bool pair = variant == 0;
+    const int bn = variant == 2 ? 128 : 256;
+    const int bm = pair ? 256 : 128;
+    if (pair && M <= 128 && force != 3 && force != 4) continue;
+    if ((force == 1 && variant != 1) || (force == 2 && variant != 2) ||
+        ((force == 3 || force == 4) && variant != 0))
+      continue;
+    const int64_t mt = (M + bm - 1) / bm, nt = (N + bn - 1) / bn;
+    const int64_t slots = pair ? sms / 2 : sms;
+    for (int s = 1; s <= 16; ++s) {
+      const int64_t kb_per = (num_k + s - 1) / s;
+      const int64_t splits = (num_k + kb_per - 1) / kb_per;
+      if (splits != s) continue;
+      if (g_gemm_splits > 0 && splits != g_gemm_splits) continue;
+      if (splits > 1 && M * N * splits * 4 > (int64_t(256) << 20)) break;
+      const int64_t units = mt * nt * splits;
+      const int64_t active = std::min<int64_t>(units, slots);
+      const int64_t per = (units + slots - 1) / slots;
+      // per-SM quantities (a pair unit is two SMs' worth of work)
+      const double mma_ns = (bn == 256 ? 512.0 : 256.0) / clk;
+      const double b_bytes = (pair ? 128.0 : double(bn)) * 128.0, a_bytes = 128.0 * 128.0;
+      const double share = double(std::min<int64_t>(mt, active));
+      const double sm_active = double(active) * (pair ? 2.0 : 1.0);
+      const double hbm_ns = (b_bytes / share) / (hbm_bw / sm_active);
+      const double l2_ns = (a_bytes + b_bytes) / l2_bw;
+      const double kb_ns = std::max(mma_ns, std::max(hbm_ns, l2_ns));
+      double t = double(per) * double(kb_per) * kb_ns + double(per) * 600.0;
+      if (splits > 1) t += double(M) * double(N) * double(splits) * 8.0 / 3000.0 + 2500.0;
+      if (t < best_t * 0.97) {
+        best_t = t;
+        best.pair = pair;
+        best.bn = bn;
+        best.splits = int(splits);
+        best.kb_per = int(kb_per);
+        best.grid = int(active) * (pair ? 2 : 1);
+      }
+    }
+  }
+  return best;
+}
+
+// Output map for the TMA-store epilogue: 2-D [rows][cols] (or 3-D
+// [splits][rows][cols] for split-K partials), 32-row x 128-byte boxes,
+// SWIZZLE_128B. Returns false when the output cannot be described (address or
+// row stride not 16-byte aligned) -> generic epilogue.
+bool make_out_map(CUtensorMap* m, const Epi& e, int64_t M, int64_t N, int splits, float* partial,
+                  int* kind) {
+  std::memset(m, 0, sizeof *m);
+  int k = partial ? EK_PARTIAL : e.kind;
+  if (k == Epi::NONE) {
+    *kind = EK_NONE;
+    return true;
+  }
+  if (k == Epi::STAGE_ONLY || k == Epi::F32_DIRECT) return false;
+  const bool f32 = k == EK_F32 || k == EK_RESID || k == EK_PARTIAL;
+  void* ptr = partial ? static_cast<void*>(partial) : e.out;
+  const int64_t cols = k == EK_SWIGLU ? N / 2 : N;
+  const int64_t ld = partial ? N : e.ldo;
+  const int64_t esz = f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || cols <= 0) return false;
+  if (k == EK_SWIGLU && (N & 1)) return false;
+  cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(M), cuuint64_t(std::max(splits, 1))};
+  cuuint64_t strides[2] = {cuuint64_t(ld * esz), cuuint64_t(ld * esz * M)};
+  cuuint32_t box[3] = {cuuint32_t(128 / esz), 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const int rank = k == EK_PARTIAL ? 3 : 2;
+  CUresult r = encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           rank, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  *kind = k;
+  return true;
+}
+
+constexpr size_t kEpiSmem = 4 * 2 * 4096;  // staging tiles of the 4 epilogue warps
+
+template <int BN, int STAGES, int KIND>
+void run_tc(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& tb,
+            const CUtensorMap& tcm, int64_t M, int64_t N, int64_t K, const Epi& e, float* partial) {
+  const size_t smem = 1024 + size_t(STAGES) * (128 * 64 * 2 + BN * 64 * 2) + kEpiSmem +
+                      8 * (2 * STAGES + 4) + 16;
+  auto kern = k_gemm_tc<BN, STAGES, KIND>;
   static bool attr = false;
   if (!attr) {
     KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  dim3 grid(unsigned((M + 127) / 128), unsigned((N + BN - 1) / BN));
-  kern<<<grid, 192, smem, s>>>(ta, tb, int(M), int(N), int(K), e);
+  const int mt = int((M + 127) / 128), nt = int((N + BN - 1) / BN);
+  kern<<<gp.grid, 192, smem, s>>>(ta, tb, tcm, int(M), int(N), int(K), mt, nt, gp.splits, gp.kb_per,
+                                  e, partial);
   KB_LAUNCH();
+}
+
+template <int STAGES, int KSUB, int KIND>
+void run_tc2(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& tb,
+             const CUtensorMap& tcm, int64_t M, int64_t N, int64_t K, const Epi& e, float* partial) {
+  const size_t smem = 1024 + size_t(STAGES) * KSUB * (2 * 128 * 64 * 2) + kEpiSmem +
+                      8 * (2 * STAGES + 4) + 16;
+  auto kern = k_gemm_tc2<STAGES, KSUB, KIND>;
+  static bool attr = false;
+  if (!attr) {
+    KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  const int mt = int((M + 255) / 256), nt = int((N + 255) / 256);
+  const int kb_per = (gp.kb_per + KSUB - 1) / KSUB;
+  kern<<<gp.grid, 192, smem, s>>>(ta, tb, tcm, int(M), int(N), int(K), mt, nt, gp.splits, kb_per, e,
+                                  partial);
+  KB_LAUNCH();
+}
+
+#define KB_EPI_DISPATCH(FN, ...)                                   \
+  switch (kind) {                                                  \
+    case EK_F32: FN<__VA_ARGS__, EK_F32>(ARGS); break;             \
+    case EK_CDT: FN<__VA_ARGS__, EK_CDT>(ARGS); break;             \
+    case EK_RESID: FN<__VA_ARGS__, EK_RESID>(ARGS); break;         \
+    case EK_TANH: FN<__VA_ARGS__, EK_TANH>(ARGS); break;           \
+    case EK_SWIGLU: FN<__VA_ARGS__, EK_SWIGLU>(ARGS); break;       \
+    case EK_NONE: FN<__VA_ARGS__, EK_NONE>(ARGS); break;           \
+    case EK_PARTIAL: FN<__VA_ARGS__, EK_PARTIAL>(ARGS); break;     \
+    default: FN<__VA_ARGS__, EK_GENERIC>(ARGS); break;             \
+  }
+
+void launch_gemm_tc(const GemmPlan& gp, cudaStream_t s, int64_t M, int64_t N, int64_t K,
+                    const void* A, int64_t lda, const void* B, int64_t ldb, const Epi& e,
+                    float* partial) {
+  const CUtensorMap ta = make_map(A, M, K, lda, 128);
+  const CUtensorMap tb = make_map(B, N, K, ldb, gp.pair ? 128 : gp.bn);
+  CUtensorMap tcm;
+  int kind = EK_GENERIC;
+  if (!make_out_map(&tcm, e, M, N, gp.splits, partial, &kind)) kind = EK_GENERIC;
+#define ARGS gp, s, ta, tb, tcm, M, N, K, e, partial
+  if (gp.pair && g_gemm_force == 4) {
+    KB_EPI_DISPATCH(run_tc2, 3, 2)
+  } else if (gp.pair) {
+    KB_EPI_DISPATCH(run_tc2, 6, 1)
+  } else if (gp.bn == 256) {
+    KB_EPI_DISPATCH(run_tc, 256, 4)
+  } else {
+    KB_EPI_DISPATCH(run_tc, 128, 6)
+  }
+#undef ARGS
 }
 
 int gemm_mode() {  // 0 auto, 1 force SIMT
@@ -341,17 +1060,19 @@ void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const v
                      ldb % 8 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(B) & 15) == 0 && K >= 1;
   if (tc_ok) {
-    // wave efficiency of each tile width on this device; prefer the wider
-    // (higher arithmetic intensity) tile unless it strands SMs
-    const int64_t mt = (M + 127) / 128, sms = c.sm_count > 0 ? c.sm_count : 148;
-    auto eff = [&](int64_t bn) {
-      const int64_t t = mt * ((N + bn - 1) / bn);
-      return double(t) / double(((t + sms - 1) / sms) * sms);
-    };
-    if (N >= 256 && eff(256) >= 0.8 * eff(128))
-      launch_tc<256, 4>(s, M, N, K, A, lda, B, ldb, e);
-    else
-      launch_tc<128, 6>(s, M, N, K, A, lda, B, ldb, e);
+    const GemmPlan gp = plan_gemm(M, N, K, c.sm_count > 0 ? c.sm_count : 148);
+    float* part = nullptr;
+    if (gp.splits > 1) {
+      DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;
+      part = static_cast<float*>(buf.ensure(size_t(M) * size_t(N) * gp.splits * 4));
+    }
+    launch_gemm_tc(gp, s, M, N, K, A, lda, B, ldb, e, part);
+    if (part) {
+      const int64_t work = (N % 4 == 0) ? M * N / 4 : (e.kind == Epi::SWIGLU ? M * N / 2 : M * N);
+      const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8 * 148));
+      k_splitk_reduce<bf16><<<blocks, 256, 0, s>>>(part, gp.splits, M, N, e);
+      KB_LAUNCH();
+    }
     return;
   }
   dim3 grid(unsigned((N + 63) / 64), unsigned((M + 63) / 64));

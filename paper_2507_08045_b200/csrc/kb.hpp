@@ -144,6 +144,7 @@ struct Ctx {
   DevBuf ws_tok, ws_tok2, ws_logits;
   DevBuf ws_new_h, ws_new_h2;  // new-input prefill stream
   DevBuf ws_part, ws2_part;    // split-KV attention partials per stream
+  mutable DevBuf ws_gpart, ws2_gpart;  // split-K GEMM partials per stream
   // second workspace set for the concurrent new-input prefill stream
   DevBuf ws2_xn, ws2_qkv, ws2_q, ws2_attn, ws2_hmid, ws2_hmidc, ws2_act, ws2_y;
 
@@ -173,7 +174,8 @@ struct Ctx {
 
 // ---- kernels (launch wrappers, .cu) ---------------------------------------
 struct Epi {  // GEMM epilogue
-  enum Kind { F32 = 0, CDT = 1, RESID = 2, TANH = 3, SWIGLU = 4 };
+  enum Kind { F32 = 0, CDT = 1, RESID = 2, TANH = 3, SWIGLU = 4, NONE = 5,
+              STAGE_ONLY = 6, F32_DIRECT = 7 };  // 5..7: benchmark/debug only
   int kind = F32;
   void* out = nullptr;        // F32/RESID: float*, CDT/TANH/SWIGLU: cdt*
   int64_t ldo = 0;
@@ -184,6 +186,7 @@ struct Epi {  // GEMM epilogue
   int64_t ldo2 = 0;
 };
 
+extern int g_gemm_force, g_gemm_splits;  // debug knobs (krul_debug_gemm_bench)
 // C = A[M,K] * B[N,K]^T with epilogue; A,B in compute dtype.
 void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K,
           const void* A, int64_t lda, const void* B, int64_t ldb, const Epi& e);

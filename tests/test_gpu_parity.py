@@ -39,7 +39,11 @@ def rel_fro(a, b):
 # ----------------------------------------------------------------- GEMM unit
 
 @pytest.mark.parametrize("M,N,Kd", [(1, 16, 8), (7, 40, 24), (128, 128, 64), (200, 300, 136),
-                                    (256, 2048, 512), (513, 4096, 1024), (64, 6144, 4096)])
+                                    (256, 2048, 512), (513, 4096, 1024), (64, 6144, 4096),
+                                    # split-K (weight streaming, M <= 128) and multi-wave
+                                    # persistent shapes of the Llama-3-8B recompute
+                                    (128, 4096, 14336), (3, 6144, 4096), (983, 6144, 4096),
+                                    (1500, 1024, 2048)])
 def test_gemm_bf16_tcgen05(K, oracle, M, N, Kd):
     from paper_2507_08045_b200.native import _p, lib
     import ctypes as C
@@ -62,6 +66,37 @@ def test_gemm_bf16_tcgen05(K, oracle, M, N, Kd):
     assert rc == 0
     err = np.abs(out - ref).max() / max(np.abs(ref).max(), 1)
     assert err < 1e-4, err
+
+
+@pytest.mark.parametrize("M,N,Kd", [(128, 1024, 4096), (300, 512, 256)])
+def test_gemm_epilogues_bf16_splitk(K, M, N, Kd):
+    """Fused epilogues through both the single-pass and the split-K reduce
+    paths (M=128, K=4096 plans split-K; M=300, K=256 does not)."""
+    from paper_2507_08045_b200.native import _p, lib
+    import ctypes as C
+    cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
+                        dtype=K.KRUL_BF16, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(M + N)
+    A = (rng.uniform(-.5, .5, (M, Kd)) / np.sqrt(Kd / 64)).astype(np.float32)
+    B = rng.uniform(-.5, .5, (N, Kd)).astype(np.float32)
+    bias = rng.uniform(-.5, .5, N).astype(np.float32)
+    acc = A.astype(np.float64) @ B.astype(np.float64).T
+    tol = 5e-2
+    out = np.zeros((M, N), np.float32)
+    assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                 _p(B), _p(bias), 3, _p(out)) == 0
+    assert np.abs(out - np.tanh(acc + bias)).max() < tol
+    out = np.zeros((M, N // 2), np.float32)
+    assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                 _p(B), None, 4, _p(out)) == 0
+    g, u = acc[:, 0::2], acc[:, 1::2]
+    assert np.abs(out - g / (1 + np.exp(-g)) * u).max() < tol * max(1.0, np.abs(g * u).max())
+    resid = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    out = resid.copy()
+    assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                 _p(B), _p(bias), 2, _p(out)) == 0
+    assert np.abs(out - (resid + acc + bias)).max() < tol
 
 
 def test_gemm_epilogues_f32(K):
