@@ -1,16 +1,9 @@
 // attn_tc.cu — causal prefill attention on tcgen05 / TMEM over the paged KV
 // cache (K6 recompute and K7 new-input prefill; engine.cpp:174-188).
 //
-// One CTA = one head x one 128-row query tile x one key split. Warp roles:
-//   warps 0-3 : softmax + epilogue, thread r owns query row r (= TMEM lane r)
-//   warp 4    : TMA producer (Q once; per 128-key block two K pages and two
-//               V^T pages of the paged cache, 128B-swizzled)
-//   warp 5    : MMA issuer: S(i) = Q K_i^T into a double-buffered TMEM S,
-//               O += P_{i-1} V_{i-1} into TMEM O once softmax published P.
-// P is written by the softmax warps straight into shared memory in the
-// UMMA K-major SW128 layout. Online softmax runs in the log2 domain; the
-// classifier region mass (analysis.cpp:46-54) is accumulated alongside the
-// row sum and rescaled with it. Split-KV partials are merged by
+// See k_attn_fa for the warp roles. Online softmax runs in the log2 domain;
+// the classifier region mass (analysis.cpp:46-54) is accumulated alongside
+// the row sum and rescaled with it. Split-KV partials are merged by
 // k_attn_combine.
 #include <cuda.h>
 
@@ -19,7 +12,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <unistd.h>
 
 #include "dev.cuh"
 #include "kb.hpp"
@@ -106,86 +98,124 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
 }  // namespace tca
+using tca::pack2;
+using tca::ex2_approx;
+using tca::imax64;
+using tca::imin64;
 
 struct AttnTc {
   int H, Hkv, grp;
   int64_t rows, pos0, kv_total;  // keys [0, kv_total) exist; causal limit per row
-  int n_qtiles, n_splits, split_blocks;
+  int n_qtiles, target;          // q tiles of 128 rows; key blocks (64) per work item
   float scale_log2;
   const int* pt;
   int max_pages;
   int k_rows_pp;   // K-view rows per page
   int v_rows_pp;   // V-view rows per page
-  bf16* out;       // [rows][H*HD] (n_splits == 1)
-  float* part;     // [split][rows][H][HD + 3] (o..., m, l, mass)
+  bf16* out;       // [rows][H*HD]
+  float* part;     // [slot][rows][H][HD + 3] (o..., m, l, mass) for split q tiles
   double* mass;    // [H][rows] region mass, may be null
   int64_t il, rs;
-  volatile int* dbg;  // KRUL_ATTN_DEBUG: per-CTA progress in host-mapped memory
 };
-#define DBG(slot, val)                                                                  \
-  do {                                                                                  \
-    if (p.dbg) {                                                                        \
-      const int cta_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;   \
-      p.dbg[cta_ * 8 + (slot)] = (val);                                                 \
-      __threadfence_system();                                                           \
-    }                                                                                   \
-  } while (0)
 
-template <int HD>
-__global__ void __launch_bounds__(192, 1)
-    k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+// number of 64-key blocks q tile qt attends to, and its work-item count
+__host__ __device__ __forceinline__ int attn_nblk(const AttnTc& p, int qt) {
+  const int64_t q_end = min(int64_t(qt) * 128 + 128, p.rows);
+  const int64_t hi = min(p.pos0 + q_end, p.kv_total);
+  return int((hi + 63) / 64);
+}
+__host__ __device__ __forceinline__ int attn_nsplit(const AttnTc& p, int qt) {
+  return (attn_nblk(p, qt) + p.target - 1) / p.target;
+}
+
+// Causal flash attention over the paged KV cache, FA4-style on tcgen05.
+// One CTA = one work item (q tile of 128 rows, key-block range) for a PAIR
+// of query heads. With GQA both heads read the same KV head, so each K/V page
+// is staged once for two heads (SHARED); otherwise both KV heads are staged.
+// Key block = one 64-token page (K [64][hd], V^T [hd][64], TMA SW128).
+//   warps 0-3 (WG A) / 4-7 (WG B): softmax for head A / B, thread = query
+//     row = TMEM lane; S(i) double-buffered in TMEM so QK^T of block i+1
+//     runs on the tensor pipe while block i is exponentiated; the O
+//     correction is lazy (the running max moves only when a row max exceeds
+//     it by > 8 in log2 units, so P <= 2^8 stays exact in bf16 range and
+//     O is rescaled rarely); P goes straight to smem in the UMMA K-major
+//     SW128 layout.
+//   warp 8: TMA producer (Q once, per block K + V^T pages, STAGES ring)
+//   warp 9: MMA issuer: S_A(i), S_B(i), then PV_A(i-1), PV_B(i-1).
+// TMEM (512 cols): S_A[2] 0..127, S_B[2] 128..255, O_A 256.., O_B 384..
+template <int HD, bool SHARED>
+__global__ void __launch_bounds__(320, 1)
+    k_attn_fa(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnTc p) {
-  constexpr int KB = 128;                 // keys per block
-  constexpr int NSUB = HD / 64;           // 64-wide hd sub-tiles
-  constexpr uint32_t Q_BYTES = 128 * HD * 2;
-  constexpr uint32_t K_BYTES = KB * HD * 2;
+  constexpr int KB = 64;
+  constexpr int NSUB = HD / 64;
+  constexpr int STAGES = SHARED ? 3 : 2;
+  constexpr int NKV = SHARED ? 1 : 2;
+  constexpr uint32_t Q_BYTES = 128 * HD * 2;        // per head
+  constexpr uint32_t K_BYTES = KB * HD * 2;         // per KV head
   constexpr uint32_t V_BYTES = HD * KB * 2;
-  constexpr uint32_t P_BYTES = 128 * KB * 2;
-  constexpr int STAGES = 2;
+  constexpr uint32_t STAGE_BYTES = NKV * (K_BYTES + V_BYTES);
+  constexpr uint32_t P_BYTES = 128 * KB * 2;        // per head
   extern __shared__ unsigned char smraw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sQ = base;
-  unsigned char* sK = sQ + Q_BYTES;
-  unsigned char* sV = sK + STAGES * K_BYTES;
-  unsigned char* sP = sV + STAGES * V_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = bars + 3;
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* o_done = bars + 8;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
+  unsigned char* sQ = base;                       // [2][Q_BYTES]
+  unsigned char* sKV = sQ + 2 * Q_BYTES;          // [STAGES][NKV][K | V]
+  unsigned char* sP = sKV + STAGES * STAGE_BYTES; // [2][P_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  uint64_t* q_full = bars;                  // 1
+  uint64_t* kv_full = bars + 1;             // STAGES
+  uint64_t* kv_empty = kv_full + STAGES;    // STAGES
+  uint64_t* s_full = kv_empty + STAGES;     // [2 heads][2 bufs]
+  uint64_t* p_ready = s_full + 4;           // [2 heads]
+  uint64_t* o_done = p_ready + 2;           // [2 heads]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heavy (late) query tiles first: causal work grows with the tile index
-  const int qt = p.n_qtiles - 1 - int(blockIdx.x);
-  const int h = blockIdx.y, split = blockIdx.z;
-  const int g = h / p.grp;
+  // work item -> (q tile, split); heavy (late) q tiles first
+  int qt = p.n_qtiles - 1, split = int(blockIdx.x);
+  for (; qt > 0; --qt) {
+    const int ns = attn_nsplit(p, qt);
+    if (split < ns) break;
+    split -= ns;
+  }
+  const int nsplit = attn_nsplit(p, qt);
+  const int nblk_all = attn_nblk(p, qt);
+  const int b0 = split * p.target;
+  const int b1 = min(nblk_all, b0 + p.target);
+  const int nb = b1 - b0;
+  const int hA = 2 * blockIdx.y, hB = hA + 1;
+  const bool hasB = hB < p.H;
+  const int gA = hA / p.grp, gB = hasB ? hB / p.grp : gA;
   const int64_t q0 = int64_t(qt) * 128;
-  const int64_t q_end = q0 + 128 < p.rows ? q0 + 128 : p.rows;
-  const int64_t last_pos = p.pos0 + q_end - 1;
-  const int64_t kv_hi_all = last_pos + 1 < p.kv_total ? last_pos + 1 : p.kv_total;
-  const int nblk_all = int((kv_hi_all + KB - 1) / KB);
-  const int b0 = split * p.split_blocks;
-  const int b1 = min(nblk_all, b0 + p.split_blocks);
-  const int nb = b1 - b0;  // may be <= 0 for trailing splits
 
-  if (threadIdx.x == 0) DBG(7, 1);
   if (threadIdx.x == 0) {
     tca::bar_init(q_full, 1);
     for (int s = 0; s < STAGES; ++s) {
       tca::bar_init(&kv_full[s], 1);
       tca::bar_init(&kv_empty[s], 1);
-      tca::bar_init(&s_full[s], 1);
     }
-    tca::bar_init(p_ready, 128);
-    tca::bar_init(o_done, 1);
+    for (int i = 0; i < 4; ++i) tca::bar_init(&s_full[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      tca::bar_init(&p_ready[i], 128);
+      tca::bar_init(&o_done[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         tca::su32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -194,239 +224,272 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tca::fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tO = tmem + 256;
-  if (threadIdx.x == 0) DBG(7, 2);
 
-  if (warp == 4) {
-    if (lane == 0 && nb > 0) {  // producer
-      tca::bar_expect(q_full, Q_BYTES);
-      for (int j = 0; j < NSUB; ++j)
-        tca::tma2d(sQ + j * (128 * 128), &tmQ, q_full, h * HD + 64 * j, int(q0));
+  if (warp == 8) {
+    if (lane == 0 && nb > 0) {  // TMA producer
+      tca::bar_expect(q_full, (hasB ? 2 : 1) * Q_BYTES);
+      for (int j = 0; j < NSUB; ++j) {
+        tca::tma2d(sQ + j * (128 * 128), &tmQ, q_full, hA * HD + 64 * j, int(q0));
+        if (hasB) tca::tma2d(sQ + Q_BYTES + j * (128 * 128), &tmQ, q_full, hB * HD + 64 * j, int(q0));
+      }
       for (int i = 0; i < nb; ++i) {
         const int s = i % STAGES;
-        DBG(0, 1000 + i);
         tca::bar_wait(&kv_empty[s], ((i / STAGES) & 1) ^ 1);
-        DBG(0, 2000 + i);
-        tca::bar_expect(&kv_full[s], K_BYTES + V_BYTES);
-        const int kb = b0 + i;
-        const int pa = p.pt[min(2 * kb, p.max_pages - 1)];
-        const int pb = p.pt[min(2 * kb + 1, p.max_pages - 1)];
-        unsigned char* k_dst = sK + s * K_BYTES;
-        for (int j = 0; j < NSUB; ++j) {
-          tca::tma2d(k_dst + j * (KB * 128), &tmK, &kv_full[s], 64 * j, pa * p.k_rows_pp + g * 64);
-          tca::tma2d(k_dst + j * (KB * 128) + 64 * 128, &tmK, &kv_full[s], 64 * j,
-                     pb * p.k_rows_pp + g * 64);
+        const int pg = p.pt[min(b0 + i, p.max_pages - 1)];
+        unsigned char* st = sKV + s * STAGE_BYTES;
+        tca::bar_expect(&kv_full[s], STAGE_BYTES);
+#pragma unroll
+        for (int h = 0; h < NKV; ++h) {
+          const int g = h == 0 ? gA : gB;
+          unsigned char* kd = st + h * (K_BYTES + V_BYTES);
+          for (int j = 0; j < NSUB; ++j)
+            tca::tma2d(kd + j * (KB * 128), &tmK, &kv_full[s], 64 * j, pg * p.k_rows_pp + g * 64);
+          tca::tma2d(kd + K_BYTES, &tmV, &kv_full[s], 0, pg * p.v_rows_pp + p.Hkv * HD + g * HD);
         }
-        unsigned char* v_dst = sV + s * V_BYTES;
-        const int voff = p.Hkv * HD + g * HD;
-        tca::tma2d(v_dst, &tmV, &kv_full[s], 0, pa * p.v_rows_pp + voff);
-        tca::tma2d(v_dst + HD * 128, &tmV, &kv_full[s], 0, pb * p.v_rows_pp + voff);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0 && nb > 0) {  // MMA issuer
       constexpr uint32_t idS = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(KB >> 3) << 17) |
                                (uint32_t(128 >> 4) << 24);
       constexpr uint32_t idO = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(HD >> 3) << 17) |
                                (uint32_t(128 >> 4) << 24);
-      DBG(1, 1);
+      const int nh = hasB ? 2 : 1;
       tca::bar_wait(q_full, 0);
-      DBG(1, 2);
-      for (int i = 0; i <= nb; ++i) {
-        if (i < nb) {
-          const int s = i % STAGES;
-          DBG(1, 1000 + i);
-          tca::bar_wait(&kv_full[s], (i / STAGES) & 1);
-          DBG(1, 2000 + i);
-          tca::fence_after();
-          const uint32_t dS = tS + uint32_t((i & 1) * 128);
+      // S_h(i) = Q_h K_i^T into S buffer i&1 (last read by softmax(i-2),
+      // whose p_ready was observed before PV(i-2) was issued)
+      auto issue_s = [&](int i) {
+        const int s = i % STAGES;
+        tca::bar_wait(&kv_full[s], (i / STAGES) & 1);
+        tca::fence_after();
+        for (int h = 0; h < nh; ++h) {
+          const unsigned char* kt = sKV + s * STAGE_BYTES + (SHARED ? 0 : h) * (K_BYTES + V_BYTES);
+          const uint32_t dS = tmem + uint32_t(h * 128 + (i & 1) * 64);
 #pragma unroll
           for (int j = 0; j < NSUB; ++j)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              tca::mma(dS, tca::desc(sQ + j * (128 * 128) + k * 32),
-                       tca::desc(sK + s * K_BYTES + j * (KB * 128) + k * 32), idS, (j | k) != 0);
-          tca::commit(&s_full[i & 1]);
+              tca::mma(dS, tca::desc(sQ + h * Q_BYTES + j * (128 * 128) + k * 32),
+                       tca::desc(kt + j * (KB * 128) + k * 32), idS, (j | k) != 0);
+          tca::commit(&s_full[h * 2 + (i & 1)]);
         }
-        if (i > 0) {
-          const int ip = i - 1, sp = ip % STAGES;
-          DBG(2, 1000 + ip);
-          tca::bar_wait(p_ready, ip & 1);
-          DBG(2, 2000 + ip);
+      };
+      issue_s(0);
+      for (int i = 0; i < nb; ++i) {
+        // QK^T of the next block runs while block i is exponentiated
+        if (i + 1 < nb) issue_s(i + 1);
+        const int sp = i % STAGES;
+        for (int h = 0; h < nh; ++h) {
+          tca::bar_wait(&p_ready[h], i & 1);
           tca::fence_after();
+          const unsigned char* vt =
+              sKV + sp * STAGE_BYTES + (SHARED ? 0 : h) * (K_BYTES + V_BYTES) + K_BYTES;
+          const uint32_t dO = tmem + 256 + uint32_t(h * 128);
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tca::mma(tO, tca::desc(sP + j * (128 * 128) + k * 32),
-                       tca::desc(sV + sp * V_BYTES + j * (HD * 128) + k * 32), idO,
-                       (ip | j | k) != 0);
-          tca::commit(o_done);
-          tca::commit(&kv_empty[sp]);
+          for (int k = 0; k < 4; ++k)
+            tca::mma(dO, tca::desc(sP + h * P_BYTES + k * 32), tca::desc(vt + k * 32), idO,
+                     (i | k) != 0);
+          tca::commit(&o_done[h]);
         }
+        tca::commit(&kv_empty[sp]);
       }
     }
-  } else {  // softmax warps 0..3: row r = TMEM lane r
-    const int r = warp * 32 + lane;
-    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+  } else {  // softmax warp groups
+    const int wg = warp >> 2;  // 0 = head A, 1 = head B
+    const int h = wg == 0 ? hA : hB;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
     const int64_t qpos = p.pos0 + q0 + r;
+    const uint32_t tS = tmem + uint32_t(wg * 128) + lane_off;
+    const uint32_t tO = tmem + 256 + uint32_t(wg * 128) + lane_off;
+    unsigned char* prow = sP + wg * P_BYTES + r * 128;
     float m = -INFINITY, l = 0.f, mn = 0.f;
-    for (int i = 0; i < nb; ++i) {
-      const int64_t k0 = int64_t(b0 + i) * KB;
-      if (threadIdx.x == 0) DBG(3, 1000 + i);
-      tca::bar_wait(&s_full[i & 1], (i >> 1) & 1);
-      if (threadIdx.x == 0) DBG(3, 2000 + i);
-      tca::fence_after();
-      const uint32_t tsrc = tS + uint32_t((i & 1) * 128) + lane_off;
-      uint32_t v[32];
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tca::ld32(tsrc + uint32_t(c * 32), v);
+    const bool active = wg == 0 || hasB;
+    if (active) {
+      for (int i = 0; i < nb; ++i) {
+        const int64_t k0 = int64_t(b0 + i) * KB;
+        tca::bar_wait(&s_full[wg * 2 + (i & 1)], (i >> 1) & 1);
+        tca::fence_after();
+        uint32_t v[64];
+        tca::ld32(tS + uint32_t((i & 1) * 64), v);
+        tca::ld32(tS + uint32_t((i & 1) * 64 + 32), v + 32);
+        // visible keys of this row in the block: [k0, k0 + nv)
+        const int nv = int(imax64(0, imin64(KB, min(qpos + 1, p.kv_total) - k0)));
+        float x[64];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int64_t kp = k0 + c * 32 + t;
-          const float sv = __uint_as_float(v[t]) * p.scale_log2;
-          if (kp <= qpos && kp < p.kv_total) mx = fmaxf(mx, sv);
+        for (int t = 0; t < 64; ++t) x[t] = __uint_as_float(v[t]) * p.scale_log2;
+        if (nv < KB) {
+#pragma unroll
+          for (int t = 0; t < 64; ++t)
+            if (t >= nv) x[t] = -INFINITY;
         }
+        float mx;
+        {  // tree max
+          float t32[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) t32[t] = fmaxf(x[t], x[t + 32]);
+#pragma unroll
+          for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+            for (int t = 0; t < w; ++t) t32[t] = fmaxf(t32[t], t32[t + w]);
+          mx = t32[0];
+        }
+        // lazy max: move only when the block max exceeds it by > 8 (log2)
+        float m_new = m;
+        if (mx > m + 8.f || m == -INFINITY) m_new = fmaxf(mx, m);
+        const float alpha = (m == -INFINITY || m_new == m) ? 1.f : ex2_approx(m - m_new);
+        const float mb = m_new == -INFINITY ? 0.f : m_new;  // all-masked rows: exp2(-inf) = 0
+        uint32_t pk[32];
+        float e2[64];
+#pragma unroll
+        for (int t = 0; t < 64; ++t) e2[t] = ex2_approx(x[t] - mb);
+#pragma unroll
+        for (int t = 0; t < 32; ++t) pk[t] = pack2(e2[2 * t], e2[2 * t + 1]);
+        float msum = 0.f;
+        if (p.mass) {  // classifier regions [0, il) U [rs, W) relative to this block
+          const int ie = int(imax64(0, imin64(KB, p.il - k0)));
+          const int rb = int(imax64(0, imin64(KB, p.rs - k0)));
+#pragma unroll
+          for (int t = 0; t < 64; ++t)
+            if (t < ie || t >= rb) msum += e2[t];
+        }
+        float sum;
+        {
+          float t32[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) t32[t] = e2[t] + e2[t + 32];
+#pragma unroll
+          for (int w = 16; w >= 1; w >>= 1)
+#pragma unroll
+            for (int t = 0; t < w; ++t) t32[t] += t32[t + w];
+          sum = t32[0];
+        }
+        // PV(i-1) must be done before O is rescaled and P overwritten
+        if (i > 0) {
+          tca::bar_wait(&o_done[wg], (i - 1) & 1);
+          tca::fence_after();
+        }
+        if (i > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          uint32_t o[32];
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            tca::ld32(tO + uint32_t(c * 32), o);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+            tca::st32(tO + uint32_t(c * 32), o);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        l = l * alpha + sum;
+        mn = mn * alpha + msum;
+        m = m_new;
+        tca::fence_before();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tca::bar_arrive(&p_ready[wg]);
       }
-      const float m_new = fmaxf(m, mx);
-      const float alpha = (m == -INFINITY) ? (m_new == -INFINITY ? 1.f : 0.f) : exp2f(m - m_new);
-      // the previous PV must finish before O is rescaled and P overwritten
-      if (threadIdx.x == 0) DBG(3, 3000 + i);
-      if (i > 0) {
-        tca::bar_wait(o_done, (i - 1) & 1);
+      if (nb > 0) {
+        tca::bar_wait(&o_done[wg], (nb - 1) & 1);
         tca::fence_after();
       }
-      if (threadIdx.x == 0) DBG(3, 4000 + i);
-      float sum = 0.f, msum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tca::ld32(tsrc + uint32_t(c * 32), v);
-        uint32_t packed[16];
-#pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          float pr[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int64_t kp = k0 + c * 32 + t + u;
-            const bool ok = kp <= qpos && kp < p.kv_total && m_new != -INFINITY;
-            const float e = ok ? exp2f(__uint_as_float(v[t + u]) * p.scale_log2 - m_new) : 0.f;
-            pr[u] = e;
-            sum += e;
-            if (kp < p.il || kp >= p.rs) msum += e;
-          }
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(pr[0], pr[1]);
-          packed[t / 2] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        // columns [32c, 32c + 32) = four 16-byte chunks of sub-tile c / 2
-        unsigned char* rowp = sP + (c >> 1) * (128 * 128) + r * 128;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = (c & 1) * 4 + q;
-          uint4 val = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
-          *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) = val;
-        }
-      }
-      if (i > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+      const int64_t row = q0 + r;
+      const bool valid = row < p.rows;
+      uint32_t o[32];
+      if (nsplit == 1) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* dst = p.out + (row * p.H + h) * HD;
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
-          tca::ld32(tO + lane_off + uint32_t(c * 32), v);
-#pragma unroll
-          for (int t = 0; t < 32; ++t) v[t] = __float_as_uint(__uint_as_float(v[t]) * alpha);
-          tca::st32(tO + lane_off + uint32_t(c * 32), v);
-        }
-      }
-      l = l * alpha + sum;
-      mn = mn * alpha + msum;
-      m = m_new;
-      tca::fence_before();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tca::bar_arrive(p_ready);
-    }
-    if (threadIdx.x == 0) DBG(3, 5000);
-    if (nb > 0) {
-      tca::bar_wait(o_done, (nb - 1) & 1);
-      tca::fence_after();
-    }
-    if (threadIdx.x == 0) DBG(3, 6000);
-    // tcgen05.ld is warp-collective: every lane loads, only valid rows store
-    const int64_t row = q0 + r;
-    const bool valid = row < p.rows;
-    uint32_t v[32];
-    if (p.n_splits == 1) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      bf16* dst = p.out + (row * p.H + h) * HD;
-#pragma unroll 1
-      for (int c = 0; c < HD / 32; ++c) {
-        tca::ld32(tO + lane_off + uint32_t(c * 32), v);
-        if (!valid) continue;
-#pragma unroll
-        for (int t = 0; t < 32; t += 8) {
-          uint4 o;
-          __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(v[t]) * inv, __uint_as_float(v[t + 1]) * inv);
-          __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(v[t + 2]) * inv, __uint_as_float(v[t + 3]) * inv);
-          __nv_bfloat162 cc = __floats2bfloat162_rn(__uint_as_float(v[t + 4]) * inv, __uint_as_float(v[t + 5]) * inv);
-          __nv_bfloat162 d = __floats2bfloat162_rn(__uint_as_float(v[t + 6]) * inv, __uint_as_float(v[t + 7]) * inv);
-          o.x = *reinterpret_cast<uint32_t*>(&a);
-          o.y = *reinterpret_cast<uint32_t*>(&b);
-          o.z = *reinterpret_cast<uint32_t*>(&cc);
-          o.w = *reinterpret_cast<uint32_t*>(&d);
-          *reinterpret_cast<uint4*>(dst + c * 32 + t) = o;
-        }
-      }
-      if (valid && p.mass) p.mass[int64_t(h) * p.rows + row] = l > 0.f ? double(mn) / double(l) : 0.0;
-    } else {
-      float* dst = p.part + ((int64_t(split) * p.rows + row) * p.H + h) * (HD + 3);
-      if (nb > 0) {
-#pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-          tca::ld32(tO + lane_off + uint32_t(c * 32), v);
+          tca::ld32(tO + uint32_t(c * 32), o);
           if (!valid) continue;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) dst[c * 32 + t] = __uint_as_float(v[t]);
+          for (int t = 0; t < 32; t += 8) {
+            uint4 w;
+            w.x = pack2(__uint_as_float(o[t]) * inv, __uint_as_float(o[t + 1]) * inv);
+            w.y = pack2(__uint_as_float(o[t + 2]) * inv, __uint_as_float(o[t + 3]) * inv);
+            w.z = pack2(__uint_as_float(o[t + 4]) * inv, __uint_as_float(o[t + 5]) * inv);
+            w.w = pack2(__uint_as_float(o[t + 6]) * inv, __uint_as_float(o[t + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c * 32 + t) = w;
+          }
         }
-      } else if (valid) {
-        for (int t = 0; t < HD; ++t) dst[t] = 0.f;
-      }
-      if (valid) {
-        dst[HD] = m;
-        dst[HD + 1] = l;
-        dst[HD + 2] = mn;
+        if (valid && p.mass) p.mass[int64_t(h) * p.rows + row] = l > 0.f ? double(mn) / double(l) : 0.0;
+      } else {
+        // [slot][h][HD + 3][rows]: for each column the warp's 32 rows are
+        // contiguous, so every store below is one coalesced 128-byte access
+        float* dst = p.part + (int64_t(split) * p.H + h) * (HD + 3) * p.rows + row;
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          if (nb > 0) tca::ld32(tO + uint32_t(c * 32), o);
+          if (!valid) continue;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) dst[int64_t(c * 32 + t) * p.rows] = nb > 0 ? __uint_as_float(o[t]) : 0.f;
+        }
+        if (valid) {
+          dst[int64_t(HD) * p.rows] = m;
+          dst[int64_t(HD + 1) * p.rows] = l;
+          dst[int64_t(HD + 2) * p.rows] = mn;
+        }
       }
     }
   }
-  if (lane == 0) DBG(4 + (warp >= 4 ? warp - 3 : 0), 7000);
   __syncwarp();
   tca::fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) DBG(7, 9999);
-  if (warp == 5) {
+  if (warp == 9) {
     tca::fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
-// Split-KV merge: weights 2^(m_s - M) (log2 domain).
+// Split-KV merge for rows of split q tiles: weights 2^(m_s - M) (log2
+// domain); rows whose q tile ran as one item were written by the kernel.
+// Block = (32-row group, head); partials are read column-coalesced and the
+// merged rows leave through a smem transpose as contiguous bf16 rows.
 template <int HD>
-__global__ void k_attn_combine(const float* part, int n_splits, int64_t rows, int H, bf16* out,
-                               double* mass) {
-  const int64_t row = blockIdx.x;
+__global__ void __launch_bounds__(256) k_attn_combine(AttnTc p) {
+  __shared__ float tile[32][HD + 1];
+  __shared__ float wgt[16][32];
+  __shared__ float invL[32];
+  const int64_t r0 = int64_t(blockIdx.x) * 32;
   const int h = blockIdx.y;
-  const int t = threadIdx.x;
-  float M = -INFINITY;
-  for (int s = 0; s < n_splits; ++s)
-    M = fmaxf(M, part[((int64_t(s) * rows + row) * H + h) * (HD + 3) + HD]);
-  float L = 0.f, MN = 0.f, acc = 0.f;
-  for (int s = 0; s < n_splits; ++s) {
-    const float* q = part + ((int64_t(s) * rows + row) * H + h) * (HD + 3);
-    const float w = (q[HD] == -INFINITY) ? 0.f : exp2f(q[HD] - M);
-    L += w * q[HD + 1];
-    MN += w * q[HD + 2];
-    if (t < HD) acc += w * q[t];
+  const int n_splits = attn_nsplit(p, int(r0 / 128));
+  if (n_splits <= 1) return;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;  // 8 warps
+  const int64_t row = r0 + lane;
+  const bool valid = row < p.rows;
+  auto col = [&](int s, int d) {
+    return p.part + ((int64_t(s) * p.H + h) * (HD + 3) + d) * p.rows + row;
+  };
+  if (wp == 0) {
+    float M = -INFINITY;
+    for (int s = 0; s < n_splits; ++s) M = fmaxf(M, valid ? *col(s, HD) : -INFINITY);
+    float L = 0.f, MN = 0.f;
+    for (int s = 0; s < n_splits; ++s) {
+      const float ms = valid ? *col(s, HD) : -INFINITY;
+      const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      wgt[s][lane] = w;
+      if (valid) {
+        L += w * *col(s, HD + 1);
+        MN += w * *col(s, HD + 2);
+      }
+    }
+    invL[lane] = L > 0.f ? 1.f / L : 0.f;
+    if (valid && p.mass) p.mass[int64_t(h) * p.rows + row] = L > 0.f ? double(MN) / double(L) : 0.0;
   }
-  if (t < HD) out[(row * H + h) * HD + t] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
-  if (t == 0 && mass) mass[int64_t(h) * rows + row] = L > 0.f ? double(MN) / double(L) : 0.0;
+  __syncthreads();
+  for (int d = wp; d < HD; d += 8) {
+    float acc = 0.f;
+    if (valid)
+      for (int s = 0; s < n_splits; ++s) acc += wgt[s][lane] * *col(s, d);
+    tile[lane][d] = acc * invL[lane];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * HD; i += blockDim.x) {
+    const int rr = i / HD, d = i % HD;
+    if (r0 + rr < p.rows) p.out[((r0 + rr) * p.H + h) * HD + d] = __float2bfloat16_rn(tile[rr][d]);
+  }
 }
 
 // ---------------------------------------------------------------- host
@@ -466,31 +529,34 @@ bool attention_tc_supported(const Ctx& c, const AttnArgs& a) {
          a.rows >= 1;
 }
 
-// Returns the number of splits used (partials in `scratch`).
+template <int HD, bool SHARED>
+void run_fa(const Ctx& c, cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk,
+            const CUtensorMap& tv, const AttnTc& p) {
+  constexpr int STAGES = SHARED ? 3 : 2, NKV = SHARED ? 1 : 2;
+  const size_t smem = 1024 + 2 * size_t(128) * HD * 2 + size_t(STAGES) * NKV * (2 * 64 * HD * 2) +
+                      2 * 128 * 64 * 2 + 256;
+  auto kern = k_attn_fa<HD, SHARED>;
+  static bool attr = false;
+  if (!attr) {
+    KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  kern<<<grid, 320, smem, s>>>(tq, tk, tv, p);
+  KB_LAUNCH();
+}
+
 void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                          const AttnArgs& a, DevBuf& scratch) {
-  double* mass_f32 = a.mass;
   const Cfg& g = c.cfg;
   const int HD = g.hd;
-  const int64_t kv_total = a.pos0 + a.rows;
-  const int n_qtiles = int((a.rows + 127) / 128);
-  const int nblk = int((kv_total + 127) / 128);
-  int splits = 1;
-  const int base = n_qtiles * g.H;
-  if (base < 2 * c.sm_count) splits = std::max(1, std::min(nblk / 2, (2 * c.sm_count + base - 1) / base));
-  const int split_blocks = (nblk + splits - 1) / splits;
-  splits = (nblk + split_blocks - 1) / split_blocks;
-
   AttnTc p{};
   p.H = g.H;
   p.Hkv = g.Hkv;
   p.grp = g.H / g.Hkv;
   p.rows = a.rows;
   p.pos0 = a.pos0;
-  p.kv_total = kv_total;
-  p.n_qtiles = n_qtiles;
-  p.n_splits = splits;
-  p.split_blocks = split_blocks;
+  p.kv_total = a.pos0 + a.rows;
+  p.n_qtiles = int((a.rows + 127) / 128);
   p.scale_log2 = (1.0f / sqrtf(float(HD))) * 1.4426950408889634f;
   p.pt = conv.d_pt + int64_t(layer) * conv.max_pages;
   p.max_pages = conv.max_pages;
@@ -498,74 +564,44 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   p.k_rows_pp = int(pe / HD);
   p.v_rows_pp = int(pe / 64);
   p.out = static_cast<bf16*>(a.out);
-  p.mass = mass_f32;
-  p.il = a.il;
+  p.mass = a.mass;
+  p.il = a.mass ? a.il : 0;
   p.rs = a.mass ? a.rs : INT64_MAX;
-  if (!a.mass) p.il = 0;
-  if (splits > 1) {
-    p.part = static_cast<float*>(
-        scratch.ensure(size_t(splits) * a.rows * g.H * (HD + 3) * sizeof(float)));
+  // key blocks per work item: about one SM's fair share of all block-pairs,
+  // at least 8 (splitting costs a partial round trip + the merge)
+  const int pairs = (g.H + 1) / 2;
+  int64_t total = 0;
+  p.target = 1 << 30;
+  for (int qt = 0; qt < p.n_qtiles; ++qt) total += attn_nblk(p, qt);
+  const int64_t sms = c.sm_count > 0 ? c.sm_count : 148;
+  p.target = int(std::max<int64_t>(8, (total * pairs + sms - 1) / sms));
+  int items = 0, max_split = 1;
+  for (int qt = 0; qt < p.n_qtiles; ++qt) {
+    items += attn_nsplit(p, qt);
+    max_split = std::max(max_split, attn_nsplit(p, qt));
   }
+  if (max_split > 1)
+    p.part = static_cast<float*>(
+        scratch.ensure(size_t(max_split) * a.rows * g.H * (HD + 3) * sizeof(float)));
   const uint64_t pool_elems = uint64_t(c.pool_pages) * pe;
   const CUtensorMap tq = map2d(a.q, uint64_t(a.rows), uint64_t(g.H) * HD, uint64_t(g.H) * HD, 128);
   const CUtensorMap tk = map2d(c.pool.p, pool_elems / HD, HD, HD, 64);
   const CUtensorMap tv = map2d(c.pool.p, pool_elems / 64, 64, 64, uint32_t(HD));
-  // >= 116 KB so exactly one CTA is resident per SM: the CTA owns all 512
-  // TMEM columns (S double buffer + O)
-  const size_t smem = std::max<size_t>(
-      1024 + size_t(128) * HD * 2 + 2 * size_t(128) * HD * 2 * 2 + 128 * 128 * 2 + 256, 116 * 1024 + 512);
-  dim3 grid(unsigned(n_qtiles), unsigned(g.H), unsigned(splits));
-  static const bool dbg_on = std::getenv("KRUL_ATTN_DEBUG") != nullptr;
-  int* dbg_host = nullptr;
-  const int n_cta = int(grid.x * grid.y * grid.z);
-  if (dbg_on) {
-    KB_CUDA(cudaHostAlloc(&dbg_host, size_t(n_cta) * 8 * 4, cudaHostAllocMapped));
-    std::memset(dbg_host, 0, size_t(n_cta) * 8 * 4);
-    int* dev = nullptr;
-    KB_CUDA(cudaHostGetDevicePointer(&dev, dbg_host, 0));
-    p.dbg = dev;
-    std::fprintf(stderr, "[attn dbg] grid %u x %u x %u rows=%lld pos0=%lld splits=%d sb=%d smem=%zu\n",
-                 grid.x, grid.y, grid.z, (long long)a.rows, (long long)a.pos0, splits, split_blocks, smem);
-  }
+  const dim3 grid{unsigned(items), unsigned(pairs), 1u};
+  const bool shared = p.grp >= 2 && (p.grp % 2) == 0;
   if (HD == 128) {
-    static bool attr = false;
-    if (!attr) {
-      KB_CUDA(cudaFuncSetAttribute(k_attn_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
-    }
-    k_attn_tc<128><<<grid, 192, smem, s>>>(tq, tk, tv, p);
+    if (shared) run_fa<128, true>(c, s, grid, tq, tk, tv, p);
+    else run_fa<128, false>(c, s, grid, tq, tk, tv, p);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      KB_CUDA(cudaFuncSetAttribute(k_attn_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
-    }
-    k_attn_tc<64><<<grid, 192, smem, s>>>(tq, tk, tv, p);
+    if (shared) run_fa<64, true>(c, s, grid, tq, tk, tv, p);
+    else run_fa<64, false>(c, s, grid, tq, tk, tv, p);
   }
-  KB_LAUNCH();
-  if (dbg_on) {
-    for (int t = 0; t < 300; ++t) {
-      if (cudaStreamQuery(s) == cudaSuccess) break;
-      usleep(10000);
-    }
-    if (cudaStreamQuery(s) != cudaSuccess) {
-      std::fprintf(stderr, "[attn dbg] TIMEOUT; per-CTA progress (prod, mma, mma_p, soft, w0..3?, w4, w5, cta):\n");
-      for (int c = 0; c < n_cta && c < 64; ++c) {
-        std::fprintf(stderr, "cta %d:", c);
-        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %d", dbg_host[c * 8 + k]);
-        std::fprintf(stderr, "\n");
-      }
-      std::fflush(stderr);
-      std::abort();
-    }
-    cudaFreeHost(dbg_host);
-  }
-  if (splits > 1) {
-    dim3 g2(unsigned(a.rows), unsigned(g.H));
+  if (max_split > 1) {
+    const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), 1u};
     if (HD == 128)
-      k_attn_combine<128><<<g2, 128, 0, s>>>(p.part, splits, a.rows, g.H, p.out, mass_f32);
+      k_attn_combine<128><<<g2, 256, 0, s>>>(p);
     else
-      k_attn_combine<64><<<g2, 64, 0, s>>>(p.part, splits, a.rows, g.H, p.out, mass_f32);
+      k_attn_combine<64><<<g2, 256, 0, s>>>(p);
     KB_LAUNCH();
   }
 }

@@ -200,14 +200,16 @@ def test_prefill_bf16_close_to_oracle(K, oracle):
         assert rel_fro(k, ok) < 2e-2 and rel_fro(v, ov) < 2e-2
 
 
-@pytest.mark.parametrize("hd,L,n_new", [(64, 300, 0), (128, 700, 0), (128, 1000, 70),
-                                         (64, 2500, 128)])
-def test_tcgen05_attention_matches_simt(K, oracle, hd, L, n_new):
+@pytest.mark.parametrize("hd,L,n_new,H,Hkv", [(64, 300, 0, 4, 2), (128, 700, 0, 4, 2),
+                                                 (128, 1000, 70, 4, 2), (64, 2500, 128, 4, 2),
+                                                 (64, 900, 40, 3, 3), (128, 1500, 128, 8, 2),
+                                                 (128, 3900, 128, 4, 1)])
+def test_tcgen05_attention_matches_simt(K, oracle, hd, L, n_new, H, Hkv):
     """bf16: the tcgen05 flash-attention path (capture off) against the SIMT
     path (capture on) on the same weights; also the new-input prefill with
-    split-KV and the in-kernel classifier mass."""
-    H = 4
-    kw = dict(n_layers=3, n_heads=H, n_kv_heads=2, head_dim=hd, d_model=H * hd, vocab_size=256,
+    split-KV and the in-kernel classifier mass. Covers GQA head pairs sharing
+    a KV head, MHA pairs with two KV heads and an odd head count."""
+    kw = dict(n_layers=3, n_heads=H, n_kv_heads=Hkv, head_dim=hd, d_model=H * hd, vocab_size=256,
               ffn_mult=2.0, seed=3)
     ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, **kw)
     cfg.max_tokens = 4096
