@@ -289,7 +289,7 @@ __device__ __forceinline__ void epi_block(const Epi& e, float* my, uint32_t tadd
 // Epilogue kinds resolved at compile time (EK_GENERIC = runtime e.kind via
 // epi_block, used when the output cannot be described by a TMA map).
 enum : int { EK_F32 = 0, EK_CDT = 1, EK_RESID = 2, EK_TANH = 3, EK_SWIGLU = 4, EK_NONE = 5,
-             EK_PARTIAL = 8, EK_GENERIC = 9 };
+             EK_PARTIAL = 8, EK_GENERIC = 9, EK_QKV = 10 };
 
 namespace tc {
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
@@ -318,6 +318,68 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&t);
 }
 }  // namespace tc
+
+// QKV epilogue (engine.cpp:128-143, :162-170 fused into the projection):
+// thread = token row r (position pos0 + r), 32 consecutive output columns
+// per TMEM chunk. Q columns are rotated and stored bf16 for rows < q_rows;
+// K columns are rotated and stored as one contiguous 64-byte run of the
+// token's K row in its page; V columns go to the transposed V^T page
+// layout, where the warp's 32 consecutive tokens make each store a
+// contiguous 64-byte run. hd % 32 == 0 so a chunk never straddles a head.
+template <int BN>
+__device__ __forceinline__ void epi_qkv(const Epi& e, uint32_t tbase, int64_t row0, int64_t col0,
+                                        int64_t M, int64_t N) {
+  const EpiKV& kv = e.kv;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = row0 + lane;
+  const bool rok = r < M;
+  const int64_t pos = kv.pos0 + r;
+  const int nq = kv.H * kv.hd, nkv = kv.Hkv * kv.hd, half = kv.hd / 2;
+  bf16* page = rok ? reinterpret_cast<bf16*>(kv.pool + int64_t(kv.pt[pos / kPageTokens]) * kv.page_bytes)
+                   : nullptr;
+  const int64_t slot = pos % kPageTokens;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    const int64_t cc = col0 + c;
+    if (cc >= N) break;
+    float v[32];
+    tc::tmem_ld32(tbase + uint32_t(c), v);
+    if (!rok) continue;
+    const bool isq = cc < nq, isk = !isq && cc < nq + nkv;
+    if (isq || isk) {
+      if (isq && r >= kv.q_rows) continue;
+      const int t0 = int((isq ? cc : cc - nq) % kv.hd);
+      const float4* cs4 = reinterpret_cast<const float4*>(kv.cosT + pos * half + t0 / 2);
+      const float4* sn4 = reinterpret_cast<const float4*>(kv.sinT + pos * half + t0 / 2);
+      uint32_t w[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 cq = __ldg(cs4 + j), sq = __ldg(sn4 + j);
+        const float cv[4] = {cq.x, cq.y, cq.z, cq.w}, sv[4] = {sq.x, sq.y, sq.z, sq.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float x0 = v[8 * j + 2 * u], x1 = v[8 * j + 2 * u + 1];
+          w[4 * j + u] = tc::pack_bf16(x0 * cv[u] - x1 * sv[u], x0 * sv[u] + x1 * cv[u]);
+        }
+      }
+      uint4* dst;
+      if (isq) {
+        dst = reinterpret_cast<uint4*>(static_cast<bf16*>(kv.q) + r * nq + cc);
+      } else {
+        const int g = int((cc - nq) / kv.hd);
+        dst = reinterpret_cast<uint4*>(page + (int64_t(g) * kPageTokens + slot) * kv.hd + t0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    } else {
+      const int64_t vc = cc - nq - nkv;
+      const int g = int(vc / kv.hd), t0 = int(vc % kv.hd);
+      bf16* vt = page + int64_t(kv.Hkv) * kPageTokens * kv.hd + (int64_t(g) * kv.hd + t0) * kPageTokens + slot;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) vt[j * kPageTokens] = __float2bfloat16_rn(v[j]);
+    }
+  }
+}
 
 // One accumulator tile row-block of an epilogue warp through TMA stores.
 // The warp owns TMEM lanes [32q, 32q+32) = output rows row0..row0+31; thread
@@ -571,6 +633,8 @@ __global__ void __launch_bounds__(192, 1)
           epi_block(e, my, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + c), row0,
                     int64_t(n) * BN + c, M, N, P);
         }
+      } else if constexpr (KIND == EK_QKV) {
+        epi_qkv<BN>(e, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN), row0, int64_t(n) * BN, M, N);
       } else {
         epi_unit<KIND, BN>(e, &tmC, stage, sbuf, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN),
                            row0, int64_t(n) * BN, M, N, ks);
@@ -773,6 +837,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           epi_block(e, my, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + c), row0,
                     int64_t(n) * BN + c, M, N, P);
         }
+      } else if constexpr (KIND == EK_QKV) {
+        epi_qkv<BN>(e, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN), row0, int64_t(n) * BN, M, N);
       } else {
         epi_unit<KIND, BN>(e, &tmC, stage, sbuf, tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN),
                            row0, int64_t(n) * BN, M, N, ks);
@@ -892,7 +958,7 @@ struct GemmPlan {
 // weight bytes streamed from HBM by this SM (shared by the co-resident
 // m-tiles), operand bytes through L2 -> SM at the measured ~75 B/ns/SM);
 // times the k-blocks on the busiest SM, plus the split-K partial round trip.
-GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms) {
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
   const int64_t num_k = (K + 63) / 64;
   const int force = g_gemm_force;
   GemmPlan best;
@@ -913,6 +979,7 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms) {
       const int64_t splits = (num_k + kb_per - 1) / kb_per;
       if (splits != s) continue;
       if (g_gemm_splits > 0 && splits != g_gemm_splits) continue;
+      if (!allow_split && splits > 1) break;
       if (splits > 1 && M * N * splits * 4 > (int64_t(256) << 20)) break;
       const int64_t units = mt * nt * splits;
       const int64_t active = std::min<int64_t>(units, slots);
@@ -948,6 +1015,10 @@ bool make_out_map(CUtensorMap* m, const Epi& e, int64_t M, int64_t N, int splits
                   int* kind) {
   std::memset(m, 0, sizeof *m);
   int k = partial ? EK_PARTIAL : e.kind;
+  if (k == Epi::QKV) {
+    *kind = EK_QKV;
+    return true;
+  }
   if (k == Epi::NONE) {
     *kind = EK_NONE;
     return true;
@@ -1020,6 +1091,7 @@ void run_tc2(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CU
     case EK_SWIGLU: FN<__VA_ARGS__, EK_SWIGLU>(ARGS); break;       \
     case EK_NONE: FN<__VA_ARGS__, EK_NONE>(ARGS); break;           \
     case EK_PARTIAL: FN<__VA_ARGS__, EK_PARTIAL>(ARGS); break;     \
+    case EK_QKV: FN<__VA_ARGS__, EK_QKV>(ARGS); break;             \
     default: FN<__VA_ARGS__, EK_GENERIC>(ARGS); break;             \
   }
 
@@ -1053,14 +1125,19 @@ int gemm_mode() {  // 0 auto, 1 force SIMT
 }
 }  // namespace
 
+bool gemm_uses_tc(const Ctx& c, const void* A, int64_t lda, const void* B, int64_t ldb) {
+  return c.cfg.dtype == KRUL_BF16 && gemm_mode() == 0 && lda % 8 == 0 && ldb % 8 == 0 &&
+         (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+}
+
 void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A,
           int64_t lda, const void* B, int64_t ldb, const Epi& e) {
   if (M <= 0 || N <= 0) return;
-  const bool tc_ok = c.cfg.dtype == KRUL_BF16 && gemm_mode() == 0 && lda % 8 == 0 &&
-                     ldb % 8 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
-                     (reinterpret_cast<uintptr_t>(B) & 15) == 0 && K >= 1;
+  const bool tc_ok = gemm_uses_tc(c, A, lda, B, ldb) && K >= 1;
+  if (e.kind == Epi::QKV && !tc_ok) fail(KRUL_E_CUDA, "fused QKV epilogue requires the tcgen05 path");
   if (tc_ok) {
-    const GemmPlan gp = plan_gemm(M, N, K, c.sm_count > 0 ? c.sm_count : 148);
+    // the scatter epilogue cannot take split-K partials
+    const GemmPlan gp = plan_gemm(M, N, K, c.sm_count > 0 ? c.sm_count : 148, e.kind != Epi::QKV);
     float* part = nullptr;
     if (gp.splits > 1) {
       DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;

@@ -241,11 +241,28 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
   if (rows <= 0) return;
   launch_rmsnorm(c, s, h_in, rows, w.xn);
   Epi e;
-  e.kind = Epi::F32;
-  e.out = w.qkv;
-  e.ldo = g.nqkv();
-  gemm(c, s, rows, g.nqkv(), g.d, w.xn, g.d, lw.wqkv, g.d, e);
-  launch_rope_scatter(c, s, w.qkv, rows, pos0, out_rows, w.q, conv, l);
+  if (gemm_uses_tc(c, w.xn, g.d, lw.wqkv, g.d) && g.hd % 32 == 0) {
+    // tcgen05 path: RoPE + paged K/V^T scatter + Q fused into the epilogue
+    e.kind = Epi::QKV;
+    e.kv.pt = conv.d_pt + int64_t(l) * conv.max_pages;
+    e.kv.pool = static_cast<char*>(c.pool.p);
+    e.kv.page_bytes = int64_t(c.page_elems() * c.esz);
+    e.kv.H = g.H;
+    e.kv.Hkv = g.Hkv;
+    e.kv.hd = g.hd;
+    e.kv.pos0 = pos0;
+    e.kv.q_rows = out_rows;
+    e.kv.cosT = c.rope_cos;
+    e.kv.sinT = c.rope_sin;
+    e.kv.q = w.q;
+    gemm(c, s, rows, g.nqkv(), g.d, w.xn, g.d, lw.wqkv, g.d, e);
+  } else {
+    e.kind = Epi::F32;
+    e.out = w.qkv;
+    e.ldo = g.nqkv();
+    gemm(c, s, rows, g.nqkv(), g.d, w.xn, g.d, lw.wqkv, g.d, e);
+    launch_rope_scatter(c, s, w.qkv, rows, pos0, out_rows, w.q, conv, l);
+  }
   if (out_rows <= 0) return;
   AttnArgs a = cap ? *cap : AttnArgs{};
   a.part = w.part;

@@ -173,9 +173,20 @@ struct Ctx {
 };
 
 // ---- kernels (launch wrappers, .cu) ---------------------------------------
+struct EpiKV {  // QKV epilogue: RoPE + paged K / V^T scatter + rotated Q
+  const int* pt = nullptr;  // page table of the layer
+  char* pool = nullptr;
+  int64_t page_bytes = 0;
+  int H = 0, Hkv = 0, hd = 0;
+  int64_t pos0 = 0, q_rows = 0;
+  const float* cosT = nullptr;  // [pos][hd/2]
+  const float* sinT = nullptr;
+  void* q = nullptr;  // [q_rows][H*hd] cdt
+};
 struct Epi {  // GEMM epilogue
   enum Kind { F32 = 0, CDT = 1, RESID = 2, TANH = 3, SWIGLU = 4, NONE = 5,
-              STAGE_ONLY = 6, F32_DIRECT = 7 };  // 5..7: benchmark/debug only
+              STAGE_ONLY = 6, F32_DIRECT = 7,  // 5..7: benchmark/debug only
+              QKV = 10 };                      // tcgen05 path only
   int kind = F32;
   void* out = nullptr;        // F32/RESID: float*, CDT/TANH/SWIGLU: cdt*
   int64_t ldo = 0;
@@ -184,9 +195,13 @@ struct Epi {  // GEMM epilogue
   int64_t ldr = 0;
   void* out2 = nullptr;          // RESID: optional cdt copy of out
   int64_t ldo2 = 0;
+  EpiKV kv;                      // QKV
 };
 
 extern int g_gemm_force, g_gemm_splits;  // debug knobs (krul_debug_gemm_bench)
+// True when gemm() will take the tcgen05 path for these operands (fused
+// epilogues such as Epi::QKV exist only there).
+bool gemm_uses_tc(const Ctx& c, const void* A, int64_t lda, const void* B, int64_t ldb);
 // C = A[M,K] * B[N,K]^T with epilogue; A,B in compute dtype.
 void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K,
           const void* A, int64_t lda, const void* B, int64_t ldb, const Epi& e);
