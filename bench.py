@@ -154,10 +154,12 @@ def run_b200(args, rank, local, world, dist):
     ctx.set_capture(False)
     # calibrate_rc_measured on the device: coarse grid, then a fine grid
     # around the coarse argmin of |T_C - T_L| (acceptance.cpp:478-487 style)
+    # objective: measured TTFT of the restore + new-input prefill DAG
     coarse = [round(0.02 * k, 4) for k in range(0, 21)]
-    r0, _, _ = ctx.calibrate_rc_measured(prev, conv, hist, pairs, coarse)
+    r0, _ = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, coarse)
     fine = sorted({min(1.0, max(0.0, round(r0 + 0.004 * k, 4))) for k in range(-5, 6)})
-    r_c, tc_f, tl_f = ctx.calibrate_rc_measured(prev, conv, hist, pairs, fine)
+    r_c, ttft_fine = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, fine)
+    r_bal, _, _ = ctx.calibrate_rc_measured(prev, conv, hist, pairs, fine)
     plan = K.build_plan(L, cfg.n_layers, r_c, pairs)
     snap = K.KVSnapshot.compress(ctx, prev, pairs, plan, L, K.MERGE_MEAN)
     full_b, stored_b = snap.storage_report()
@@ -211,7 +213,7 @@ def run_b200(args, rank, local, world, dist):
                                f"{n_new}-token new-input prefill, 1 conversation/step/GPU",
                    "global_batch": world, "seq_len": L, "parallelism": f"dp{world} (conversation shards, no collective)",
                    "l2": "inputs (16 GB weights, 1 GB KV) larger than L2; no flush",
-                   "r_c": r_c, "r_c_analytic": r_analytic,
+                   "r_c": r_c, "r_c_analytic": r_analytic, "r_c_balanced_restore": r_bal,
                    "plan_head": [int(x) for x in plan[:4]], "pairs": len(pairs),
                    "h2d_gbs_measured": round(b_h2d / 1e9, 2),
                    "recompute_tflops_measured": round(f_rec / 1e12, 1)},

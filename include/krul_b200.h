@@ -266,6 +266,16 @@ int krul_calibrate_rc_measured(krul_ctx* ctx, krul_conv* prev,
                                const double* grid, int n_grid, int mode,
                                double* r_c, double* tc, double* tl);
 
+/* B200 extension of calibrate_rc_measured (scheduler.cpp:402-443): argmin of
+ * the measured TTFT of the full restore + new-input prefill DAG over the
+ * grid (median of `reps` runs per ratio); ttft ([n_grid], optional) gets
+ * the medians in sorted-grid order. */
+int krul_calibrate_rc_ttft(krul_ctx* ctx, krul_conv* prev, krul_conv* scratch,
+                           const int32_t* history, int64_t L, const int32_t* new_tokens,
+                           int64_t n_new, const krul_pair* pairs, int n_pairs,
+                           const double* grid, int n_grid, int mode, int reps,
+                           double* r_c, double* ttft);
+
 /* ---- measured stream rates (calibrate_rc_measured, scheduler.cpp:402) - */
 /* Times pinned H2D bandwidth (bytes/s) and recompute throughput (flop/s)
  * on this device; feeds krul_cost_model. */

@@ -445,50 +445,60 @@ __global__ void __launch_bounds__(320, 1)
 
 // Split-KV merge for rows of split q tiles: weights 2^(m_s - M) (log2
 // domain); rows whose q tile ran as one item were written by the kernel.
-// Block = (32-row group, head); partials are read column-coalesced and the
-// merged rows leave through a smem transpose as contiguous bf16 rows.
+// Block = (32 rows, head, 32-dim slice), 4 warps, lane = row, warp = 8 dims.
+// Partials are [slot][h][HD + 3][rows], so every load is a coalesced
+// 128-byte row segment; all split loads of a thread are issued up front
+// (kMaxSplit unrolled, predicated) for memory-level parallelism. The merged
+// 32x32 block leaves through smem as 64-byte bf16 row runs.
+constexpr int kMaxSplit = 16;
 template <int HD>
-__global__ void __launch_bounds__(256) k_attn_combine(AttnTc p) {
-  __shared__ float tile[32][HD + 1];
-  __shared__ float wgt[16][32];
-  __shared__ float invL[32];
+__global__ void __launch_bounds__(128) k_attn_combine(AttnTc p) {
+  __shared__ float tile[32][33];
   const int64_t r0 = int64_t(blockIdx.x) * 32;
-  const int h = blockIdx.y;
+  const int h = blockIdx.y, d0 = blockIdx.z * 32;
   const int n_splits = attn_nsplit(p, int(r0 / 128));
   if (n_splits <= 1) return;
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;  // 8 warps
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int64_t row = r0 + lane;
   const bool valid = row < p.rows;
-  auto col = [&](int s, int d) {
-    return p.part + ((int64_t(s) * p.H + h) * (HD + 3) + d) * p.rows + row;
-  };
-  if (wp == 0) {
-    float M = -INFINITY;
-    for (int s = 0; s < n_splits; ++s) M = fmaxf(M, valid ? *col(s, HD) : -INFINITY);
-    float L = 0.f, MN = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float ms = valid ? *col(s, HD) : -INFINITY;
-      const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
-      wgt[s][lane] = w;
-      if (valid) {
-        L += w * *col(s, HD + 1);
-        MN += w * *col(s, HD + 2);
-      }
+  const int64_t sstride = int64_t(p.H) * (HD + 3) * p.rows;
+  const float* base = p.part + (int64_t(h) * (HD + 3)) * p.rows + (valid ? row : 0);
+  float ms[kMaxSplit], w[kMaxSplit];
+  float M = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < kMaxSplit; ++s) {
+    ms[s] = (s < n_splits) ? base[s * sstride + int64_t(HD) * p.rows] : -INFINITY;
+    M = fmaxf(M, ms[s]);
+  }
+  float L = 0.f, MN = 0.f;
+  const bool do_mass = p.mass && blockIdx.z == 0 && wp == 0;
+#pragma unroll
+  for (int s = 0; s < kMaxSplit; ++s) {
+    w[s] = (s < n_splits && ms[s] != -INFINITY) ? exp2f(ms[s] - M) : 0.f;
+    if (s < n_splits) {
+      L += w[s] * base[s * sstride + int64_t(HD + 1) * p.rows];
+      if (do_mass) MN += w[s] * base[s * sstride + int64_t(HD + 2) * p.rows];
     }
-    invL[lane] = L > 0.f ? 1.f / L : 0.f;
-    if (valid && p.mass) p.mass[int64_t(h) * p.rows + row] = L > 0.f ? double(MN) / double(L) : 0.0;
   }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  if (do_mass && valid) p.mass[int64_t(h) * p.rows + row] = L > 0.f ? double(MN) / double(L) : 0.0;
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int s = 0; s < kMaxSplit; ++s)
+    if (s < n_splits) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += w[s] * base[s * sstride + int64_t(d0 + wp * 8 + j) * p.rows];
+    }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) tile[lane][wp * 8 + j] = acc[j] * inv;
   __syncthreads();
-  for (int d = wp; d < HD; d += 8) {
-    float acc = 0.f;
-    if (valid)
-      for (int s = 0; s < n_splits; ++s) acc += wgt[s][lane] * *col(s, d);
-    tile[lane][d] = acc * invL[lane];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 32 * HD; i += blockDim.x) {
-    const int rr = i / HD, d = i % HD;
-    if (r0 + rr < p.rows) p.out[((r0 + rr) * p.H + h) * HD + d] = __float2bfloat16_rn(tile[rr][d]);
+  // 32 rows x 16 bf16 pairs
+  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) {
+    const int rr = i >> 4, d = 2 * (i & 15);
+    if (r0 + rr < p.rows)
+      *reinterpret_cast<uint32_t*>(p.out + ((r0 + rr) * p.H + h) * HD + d0 + d) = pack2(tile[rr][d], tile[rr][d + 1]);
   }
 }
 
@@ -575,6 +585,7 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   for (int qt = 0; qt < p.n_qtiles; ++qt) total += attn_nblk(p, qt);
   const int64_t sms = c.sm_count > 0 ? c.sm_count : 148;
   p.target = int(std::max<int64_t>(8, (total * pairs + sms - 1) / sms));
+  p.target = std::max(p.target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
   int items = 0, max_split = 1;
   for (int qt = 0; qt < p.n_qtiles; ++qt) {
     items += attn_nsplit(p, qt);
@@ -597,11 +608,11 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
     else run_fa<64, false>(c, s, grid, tq, tk, tv, p);
   }
   if (max_split > 1) {
-    const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), 1u};
+    const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), unsigned(HD / 32)};
     if (HD == 128)
-      k_attn_combine<128><<<g2, 256, 0, s>>>(p);
+      k_attn_combine<128><<<g2, 128, 0, s>>>(p);
     else
-      k_attn_combine<64><<<g2, 256, 0, s>>>(p);
+      k_attn_combine<64><<<g2, 128, 0, s>>>(p);
     KB_LAUNCH();
   }
 }

@@ -758,6 +758,50 @@ int krul_calibrate_rc_measured(krul_ctx* ctx, krul_conv* prev, krul_conv* scratc
   });
 }
 
+// B200 extension of calibrate_rc_measured: the objective is the measured
+// time to first token of the real restore + new-input prefill DAG (the
+// prefill stream competes with the recompute stream for SMs, so the split
+// that balances the bare restore is not the one that minimises TTFT). For
+// each grid ratio: build the plan, compress `prev` into a snapshot, run
+// `reps` restores (after one warm-up) and keep the median TTFT; returns the
+// argmin (strict <, ties to the smaller ratio). ttft ([n_grid], optional)
+// receives the medians in sorted-grid order.
+int krul_calibrate_rc_ttft(krul_ctx* ctx, krul_conv* prev, krul_conv* scratch,
+                           const int32_t* hist, int64_t L, const int32_t* new_tok, int64_t n_new,
+                           const krul_pair* pairs, int np, const double* grid, int ng, int mode,
+                           int reps, double* r_out, double* ttft) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(prev, "prev");
+    need(scratch, "scratch");
+    if (ng <= 0) fail(KRUL_E_CONFIG, "calibration grid is empty");
+    if (!new_tok || n_new <= 0) fail(KRUL_E_CONFIG, "TTFT calibration needs new input tokens");
+    Ctx& c = *ctx->c;
+    std::vector<double> g(grid, grid + ng);
+    std::sort(g.begin(), g.end());
+    double best = g.front(), best_t = 1e300;
+    std::vector<float> logits(size_t(c.cfg.V));
+    for (int k = 0; k < ng; ++k) {
+      const std::vector<int64_t> p = build_plan(L, c.cfg.N, g[size_t(k)], pairs, np);
+      std::unique_ptr<Snapshot> s(snapshot_compress(c, *prev->v, pairs, np, p.data(), L, mode));
+      std::vector<double> ts;
+      for (int rep = 0; rep <= std::max(1, reps); ++rep) {
+        double t = 0;
+        restore(c, *scratch->v, *s, hist, L, nullptr, new_tok, n_new, logits.data(), &t);
+        if (rep > 0) ts.push_back(t);
+      }
+      std::sort(ts.begin(), ts.end());
+      const double med = ts[ts.size() / 2];
+      if (ttft) ttft[k] = med;
+      if (med < best_t) {
+        best_t = med;
+        best = g[size_t(k)];
+      }
+    }
+    *r_out = best;
+  });
+}
+
 int krul_restore_timeline(krul_ctx* ctx, double* comp, double* load, double* newp) {
   return guard([&] {
     need(ctx, "ctx");

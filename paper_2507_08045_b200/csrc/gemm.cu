@@ -915,6 +915,66 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
   }
 }
 
+// Split-K partner of the fused QKV epilogue (weight-streaming shapes, small
+// M): sums the fp32 partials in fixed split order, then RoPE + Q store + paged
+// K / V^T scatter exactly as epi_qkv. Block = 64 tokens x 32 columns staged
+// in smem so both the token-major (Q, K) and the dimension-major (V^T)
+// stores are contiguous runs.
+__global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P, int splits,
+                                                     int64_t M, int64_t N, EpiKV kv) {
+  __shared__ float t[64][33];
+  const int64_t r0 = int64_t(blockIdx.x) * 64;
+  const int64_t cc = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, token group
+  const int64_t MN = M * N;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t r = r0 + ty + 8 * j;
+    float a = 0.f;
+    if (r < M && cc + tx < N)
+      for (int s = 0; s < splits; ++s) a += P[int64_t(s) * MN + r * N + cc + tx];
+    t[ty + 8 * j][tx] = a;
+  }
+  __syncthreads();
+  const int nq = kv.H * kv.hd, nkv = kv.Hkv * kv.hd, half = kv.hd / 2;
+  const bool isq = cc < nq, isk = !isq && cc < nq + nkv;
+  if (isq || isk) {
+    const int t0 = int((isq ? cc : cc - nq) % kv.hd);
+    const int i = (t0 + tx) >> 1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int rr = ty + 8 * j;
+      const int64_t r = r0 + rr;
+      if (r >= M || (isq && r >= kv.q_rows)) continue;
+      const int64_t pos = kv.pos0 + r;
+      const float x0 = t[rr][tx & ~1], x1 = t[rr][tx | 1];
+      const float cs = kv.cosT[pos * half + i], sn = kv.sinT[pos * half + i];
+      const float y = (tx & 1) ? (x0 * sn + x1 * cs) : (x0 * cs - x1 * sn);
+      if (isq) {
+        static_cast<bf16*>(kv.q)[r * nq + cc + tx] = __float2bfloat16_rn(y);
+      } else {
+        const int g = int((cc - nq) / kv.hd);
+        bf16* page = reinterpret_cast<bf16*>(kv.pool + int64_t(kv.pt[pos / kPageTokens]) * kv.page_bytes);
+        page[(int64_t(g) * kPageTokens + pos % kPageTokens) * kv.hd + t0 + tx] = __float2bfloat16_rn(y);
+      }
+    }
+  } else {
+    const int64_t vc = cc - nq - nkv;
+    const int g = int(vc / kv.hd), t0 = int(vc % kv.hd);
+    // thread -> (dimension d, 8 consecutive tokens)
+    const int d = threadIdx.x >> 3, tg = (threadIdx.x & 7) * 8;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t r = r0 + tg + u;
+      if (r >= M) break;
+      const int64_t pos = kv.pos0 + r;
+      bf16* page = reinterpret_cast<bf16*>(kv.pool + int64_t(kv.pt[pos / kPageTokens]) * kv.page_bytes);
+      page[int64_t(kv.Hkv) * kPageTokens * kv.hd + (int64_t(g) * kv.hd + t0 + d) * kPageTokens +
+           pos % kPageTokens] = __float2bfloat16_rn(t[tg + u][d]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1136,15 +1196,19 @@ void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const v
   const bool tc_ok = gemm_uses_tc(c, A, lda, B, ldb) && K >= 1;
   if (e.kind == Epi::QKV && !tc_ok) fail(KRUL_E_CUDA, "fused QKV epilogue requires the tcgen05 path");
   if (tc_ok) {
-    // the scatter epilogue cannot take split-K partials
-    const GemmPlan gp = plan_gemm(M, N, K, c.sm_count > 0 ? c.sm_count : 148, e.kind != Epi::QKV);
+    const GemmPlan gp = plan_gemm(M, N, K, c.sm_count > 0 ? c.sm_count : 148, true);
     float* part = nullptr;
     if (gp.splits > 1) {
       DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;
       part = static_cast<float*>(buf.ensure(size_t(M) * size_t(N) * gp.splits * 4));
     }
     launch_gemm_tc(gp, s, M, N, K, A, lda, B, ldb, e, part);
-    if (part) {
+    if (part && e.kind == Epi::QKV) {
+      if (c.cfg.hd % 32) fail(KRUL_E_CUDA, "fused QKV epilogue needs head_dim % 32 == 0");
+      const dim3 g2{unsigned((M + 63) / 64), unsigned((N + 31) / 32), 1u};
+      k_qkv_reduce<<<g2, 256, 0, s>>>(part, gp.splits, M, N, e.kv);
+      KB_LAUNCH();
+    } else if (part) {
       const int64_t work = (N % 4 == 0) ? M * N / 4 : (e.kind == Epi::SWIGLU ? M * N / 2 : M * N);
       const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8 * 148));
       k_splitk_reduce<bf16><<<blocks, 256, 0, s>>>(part, gp.splits, M, N, e);

@@ -444,7 +444,6 @@ __global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView 
   const T* vb = blob + (int64_t(Hkv + g) * rows_blob) * hd;
   T* page = reinterpret_cast<T*>(pv.page(lo));
   const int n = int(hi - lo);
-  const int ldt = hd + 8;
   // K: straight row copy (contiguous [rows][hd] on both sides)
   const int64_t krow0 = lo - blob_start;
   T* kdst = page + pv.k_off(g, lo, 0);
@@ -457,18 +456,44 @@ __global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView 
   } else {
     for (int i = threadIdx.x; i < elems; i += blockDim.x) kdst[i] = kb[krow0 * hd + i];
   }
-  // V: stage [n][hd] then write V^T [hd][pos%P]
-  for (int i = threadIdx.x; i < elems; i += blockDim.x) {
-    const int r = i / hd, t = i % hd;
-    tile[r * ldt + t] = vb[(krow0 + r) * hd + t];
+  // V: stage [n][hd] (16-byte loads; row pitch hd + 2 elements keeps the
+  // column reads below spread over the banks), then write V^T [hd][pos%P]
+  // as 16-byte runs of 8 consecutive tokens when the span is page-aligned
+  const int ldt = hd + 2;
+  if (sizeof(T) == 2 && hd % 8 == 0) {
+    const int vpr = hd / 8;
+    for (int i = threadIdx.x; i < n * vpr; i += blockDim.x) {
+      const int r = i / vpr, t8 = (i % vpr) * 8;
+      const int4 x = *reinterpret_cast<const int4*>(vb + (krow0 + r) * hd + t8);
+      const uint32_t w[4] = {uint32_t(x.x), uint32_t(x.y), uint32_t(x.z), uint32_t(x.w)};
+      uint32_t* d = reinterpret_cast<uint32_t*>(tile + r * ldt + t8);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = w[j];
+    }
+  } else {
+    for (int i = threadIdx.x; i < elems; i += blockDim.x) {
+      const int r = i / hd, t = i % hd;
+      tile[r * ldt + t] = vb[(krow0 + r) * hd + t];
+    }
   }
   __syncthreads();
-  const int off = int(lo % kPageTokens);
-  for (int i = threadIdx.x; i < hd * n; i += blockDim.x) {
-    const int t = i / n, r = i % n;
-    page[pv.v_off(g, lo + r, t) - 0] = tile[r * ldt + t];
+  if (sizeof(T) == 2 && n == kPageTokens) {
+    T* vt = page + pv.v_off(g, lo, 0);  // lo is page-aligned: [hd][64] contiguous
+    for (int i = threadIdx.x; i < hd * 8; i += blockDim.x) {
+      const int t = i >> 3, c = (i & 7) * 8;
+      uint16_t u[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u[j] = reinterpret_cast<const uint16_t*>(tile)[(c + j) * ldt + t];
+      *reinterpret_cast<uint4*>(vt + t * kPageTokens + c) =
+          make_uint4(u[0] | (uint32_t(u[1]) << 16), u[2] | (uint32_t(u[3]) << 16),
+                     u[4] | (uint32_t(u[5]) << 16), u[6] | (uint32_t(u[7]) << 16));
+    }
+  } else {
+    for (int i = threadIdx.x; i < hd * n; i += blockDim.x) {
+      const int t = i / n, r = i % n;
+      page[pv.v_off(g, lo + r, t)] = tile[r * ldt + t];
+    }
   }
-  (void)off;
 }
 void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,
                    const Conv& conv, int layer, int64_t from) {
@@ -476,7 +501,7 @@ void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_
   PageView pv = page_view(c, conv, layer);
   const int64_t tiles = (L - 1) / kPageTokens - from / kPageTokens + 1;
   dim3 grid(unsigned(tiles), unsigned(c.cfg.Hkv));
-  const size_t smem = size_t(kPageTokens) * (c.cfg.hd + 8) * c.esz;
+  const size_t smem = size_t(kPageTokens) * (c.cfg.hd + 2) * c.esz + 16;
   if (c.cfg.dtype == KRUL_BF16) {
     KB_CUDA(cudaFuncSetAttribute(k_expand<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));

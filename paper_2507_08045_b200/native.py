@@ -291,6 +291,20 @@ class Context:
                                                 _p(tl)))
         return r.value, tc, tl
 
+    def calibrate_rc_ttft(self, prev, scratch, history, new_tokens, pairs, grid, mode=1, reps=3):
+        """calibrate_rc_measured with the measured TTFT of restore + new-input
+        prefill as the objective -> (r_c, ttft[ms]) over the sorted grid."""
+        t = np.ascontiguousarray(history, np.int32)
+        nt = np.ascontiguousarray(new_tokens, np.int32)
+        arr, n = _pairs(pairs)
+        g = np.ascontiguousarray(sorted(grid), np.float64)
+        tt = np.zeros(len(g))
+        r = C.c_double()
+        _check(lib().krul_calibrate_rc_ttft(self.h, prev.h, scratch.h, _p(t), C.c_int64(t.size),
+                                            _p(nt), C.c_int64(nt.size), arr, n, _p(g), len(g),
+                                            mode, reps, C.byref(r), _p(tt)))
+        return r.value, tt
+
     def measure_rates(self, scratch):
         b, f = C.c_double(), C.c_double()
         _check(lib().krul_measure_rates(self.h, scratch.h, C.byref(b), C.byref(f)))
