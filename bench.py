@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 PEAKS = {"hbm_gbs": 6547.2, "bf16_tflops": 1676.4, "bf16_tflops_sustained": 1397.8}
 try:
     PEAKS.update(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))))
+    PEAKS["MEASURED_PEAKS_FILE"] = True
 except Exception:
     pass
 
@@ -174,6 +175,7 @@ def run_b200(args, rank, local, world, dist):
     clocks = ClockSampler(local)
     clocks.start()
     ttfts, stats, walls = [], [], []
+    launches0 = K.launch_count()
     for _ in range(args.steps):
         w0 = time.perf_counter()
         logits, st, ttft = step()
@@ -181,9 +183,23 @@ def run_b200(args, rank, local, world, dist):
         ttfts.append(ttft)
         stats.append(st)
     ctx.sync()
+    launches = K.launch_count() - launches0
     barrier(dist)
     clk = clocks.stop()
     tl_c, tl_l, tl_n = ctx.restore_timeline()
+    # Instrumented pass (same workload, right after the timed steps): CUDA
+    # events around every GEMM / attention / expand launch on the stream it
+    # runs on. Kept out of the headline steps because an event between two
+    # kernels costs their launch overlap (~+35% on the step, measured).
+    ctx.ktime_enable(True)
+    tags = (("gemm", 0), ("attention", 1), ("expand", 2))
+    kt = {name: [0, 0.0, 0.0, 0.0] for name, _ in tags}
+    for i in range(args.warmup + args.steps):
+        step()
+        if i >= args.warmup:
+            for name, tag in tags:
+                kt[name] = [a + b for a, b in zip(kt[name], ctx.ktime_read(tag))]
+    ctx.ktime_enable(False)
     total_ms = float(np.sum(ttfts))
     total_ms = allmax(dist, total_ms, local)
     wall_total = allmax(dist, float(np.sum(walls)), local)
@@ -191,10 +207,17 @@ def run_b200(args, rank, local, world, dist):
     conv_s = world * args.steps / (total_ms / 1e3)
     e2e_conv_s = world * args.steps / (wall_total / 1e3)
     st = {k: float(np.median([s[k] for s in stats])) for k in stats[0]}
-    # dominant-kernel roofline: the recompute stream (tcgen05 GEMMs + attention)
-    flops = st["recompute_flops"]
-    achieved_tf = flops / (st["compute_ms"] * 1e-3) / 1e12 if st["compute_ms"] > 0 else 0.0
+    # dominant kernel (by device time): the tcgen05 GEMM, timed per launch
+    # with CUDA events on its own stream (instrumented pass above)
     peak = PEAKS.get("bf16_tflops_sustained", 1397.8)
+    peak_src = ("MEASURED_PEAKS.json bf16_tflops_sustained" if "MEASURED_PEAKS_FILE" in PEAKS
+                else "fallback (B200_PROFILING.md: sustained bf16 ~1.4 PFLOP/s; MEASURED_PEAKS.json absent)")
+    hbm = PEAKS.get("hbm_gbs", 6547.2)
+    g_n, g_ms, g_fl, _ = kt["gemm"]
+    a_n, a_ms, a_fl, _ = kt["attention"]
+    e_n, e_ms, _, e_by = kt["expand"]
+    achieved_tf = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    est = estimator_leg(K, ctx, conv, cfg, spec) if rank == 0 else None
     out = {
         "metric": METRIC,
         "value": round(conv_s, 4),
@@ -222,21 +245,89 @@ def run_b200(args, rank, local, world, dist):
                         "load_done": [round(x, 3) for x in tl_l],
                         "new_prefill_done": [round(x, 3) for x in tl_n]},
         "storage": {"full_bytes": full_b, "stored_bytes": stored_b},
-        "roofline": {"bound": "tensor", "kernel": "recompute stream (K6)",
+        "roofline": {"bound": "tensor", "kernel": "k_gemm_tc / k_gemm_tc2 (tcgen05 GEMM, K6/K7)",
                      "achieved": round(achieved_tf, 2), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved_tf / peak, 4), "traffic": None,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"},
+                     "launches": g_n, "avg_launch_us": round(1e3 * g_ms / max(g_n, 1), 2),
+                     "measured": "CUDA events around each launch, instrumented pass of the same "
+                                 "steps (warm-up + steps) right after the timed region",
+                     "algorithmic": "2*M*N*K per GEMM launch, summed over the timed steps",
+                     "peak_source": peak_src,
+                     "traffic_note": "dram bytes per launch: see profiles/ (ncu --set full)"},
+        "rooflines": {
+            "attention": {"bound": "tensor", "kernel": "k_attn_fa (+ split-KV merge)",
+                          "achieved": round(a_fl / (a_ms * 1e-3) / 1e12, 2) if a_ms else None,
+                          "unit": "TFLOP/s", "peak": peak,
+                          "frac": round(a_fl / (a_ms * 1e-3) / 1e12 / peak, 4) if a_ms else None,
+                          "launches": a_n},
+            "expand": {"bound": "hbm", "kernel": "k_expand (K5)",
+                       "achieved": round(e_by / (e_ms * 1e-3) / 1e9, 1) if e_ms else None,
+                       "unit": "GB/s", "peak": hbm,
+                       "frac": round(e_by / (e_ms * 1e-3) / 1e9 / hbm, 4) if e_ms else None,
+                       "launches": e_n},
+            "h2d_load": {"bound": "pcie", "kernel": "cudaMemcpyAsync pinned->device (K4)",
+                         "achieved": round(st["h2d_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9, 2),
+                         "unit": "GB/s", "peak": round(b_h2d / 1e9, 2),
+                         "peak_source": "measured 256 MiB pinned H2D copy on this box"},
+            "recompute_stream": {"bound": "tensor", "achieved": round(
+                st["recompute_flops"] / (st["compute_ms"] * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+                "note": "algorithmic pyramid flops / recompute-stream makespan (shares SMs with the "
+                        "new-input prefill and expand streams)"},
+            **({"estimator_decode_fold": est["fold"], "selector": est["select"]} if est else {}),
+        },
         "e2e": {"value": round(e2e_conv_s, 4), "unit": "conversations/s",
                 "ttft_p50_ms": round(float(np.median(walls)), 4),
                 "h2d_bytes_per_step": int(st["h2d_bytes"] + 4 * (L + n_new)),
                 "d2h_bytes_per_step": 4 * cfg.vocab_size},
-        "gpu_launches": None,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": round(launches / args.steps, 1),
         "clocks": clk,
         "setup_s": {"history_prefill": round(t_prefill, 2)},
     }
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(args, spec, plan, pairs, budget_s=args.cpu_budget)
     return out
+
+
+def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
+    """The estimator on the restored conversation, as the reference's turn
+    loop runs it (harness.cpp:180-188): teacher-forced decode steps whose
+    per-layer attention rows feed the decode fold (K1), then finalize and
+    the device selector (K3). All N layers are tracked (P = N(N-1)/2 pairs)
+    so the fold reads every layer's row; decode fold HBM GB/s from CUDA
+    events around each fold launch (algorithmic bytes: N*H*W*4 + P*H*16)."""
+    est = K.StreamingEstimator(ctx, list(range(cfg.n_layers)))
+    ctx.ktime_enable(True)
+    rng = np.random.default_rng(7)
+    for _ in range(steps):
+        ctx.decode_step(conv, int(rng.integers(0, cfg.vocab_size)))
+        est.fold_decode()
+    n, ms, _, by = ctx.ktime_read(3)
+    ctx.ktime_enable(False)
+    hbm = PEAKS.get("hbm_gbs", 6547.2)
+    gbs = by / (ms * 1e-3) / 1e9 if ms else None
+    # finalize + selector (one CTA bitonic sort + greedy matching), timed on the host
+    sums = est.sums()
+    D = np.zeros((cfg.n_layers, cfg.n_layers))
+    P = 0
+    for i in range(cfg.n_layers):
+        for j in range(i + 1, cfg.n_layers):
+            D[i, j] = D[j, i] = float(np.mean(np.sqrt(np.maximum(sums[P], 0.0))))
+            P += 1
+    layers = list(range(cfg.n_layers))
+    t0 = time.perf_counter()
+    reps = 20
+    for _ in range(reps):
+        strat = K.select_strategy(ctx, D, layers, layers, 0.5, cfg.n_layers)
+    sel_us = (time.perf_counter() - t0) / reps * 1e6
+    return {"fold": {"bound": "hbm", "kernel": "k_fold_stage1<false> + k_fold_stage2 (K1)",
+                     "achieved": round(gbs, 1) if gbs else None, "unit": "GB/s", "peak": hbm,
+                     "frac": round(gbs / hbm, 4) if gbs else None, "launches": n,
+                     "avg_launch_us": round(1e3 * ms / max(n, 1), 2),
+                     "width": int(len(conv)), "tracked_layers": cfg.n_layers},
+            "select": {"bound": "latency", "kernel": "k_select (K3) incl. D upload + result read",
+                       "us_per_call": round(sel_us, 1), "pairs_selected": len(strat.pairs),
+                       "candidates": cfg.n_layers * (cfg.n_layers - 1) // 2}}
 
 
 # ---------------------------------------------------------------- CPU legs

@@ -286,6 +286,16 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps,
 /* C[M,N] = A[M,K] B[N,K]^T through the engine GEMM (inputs rounded to the
  * ctx dtype; tcgen05 path for bf16). epi: 0 = f32 store, 2 = resid (C +=),
  * 3 = tanh(acc + bias), 4 = swiglu over column pairs (C is [M, N/2]). */
+/* ---- measurement support (not on the reference's interface) ----------
+ * krul_launch_count: number of kernels this library has launched (process
+ * wide). krul_ktime_*: per-launch CUDA-event timing of instrumented kernel
+ * classes (tag: 0 GEMM, 1 attention, 2 expand, 3 decode fold, 4 prefill
+ * fold, 5 selector, 6 compress) with their algorithmic flops / bytes. */
+int krul_launch_count(uint64_t* n);
+int krul_ktime_enable(krul_ctx* ctx, int on);
+int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, double* flops,
+                    double* bytes);
+
 /* Kernel-tuning aid: times `iters` device-resident bf16 GEMMs (not a product entry). */
 int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
                           int splits, int iters, float* ms_per_iter);

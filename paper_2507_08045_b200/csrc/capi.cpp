@@ -346,8 +346,11 @@ static void fold_prefill_dev(Est& e, const float* probs, int64_t rows, int64_t W
   if (!e.layers.empty() && e.layers.back() >= N) fail(KRUL_E_CONFIG, "record does not cover all tracked layers");
   Ctx& c = *e.ctx;
   ensure_partial(e, (rows * W + 511) / 512);
+  cudaEvent_t kt0 = kt_begin(c, c.s_est);
   launch_fold_prefill(c.s_est, probs, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
                       e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);
+  kt_end(c, c.s_est, kt0, KT_FOLD_PREFILL, 0.0,
+         double(e.layers.size()) * e.H * double(rows) * double(W) * 4.0 + double(e.P()) * e.H * 16.0);
   KB_CUDA(cudaStreamSynchronize(c.s_est));
   e.prefill_done = true;
   e.prefill_rows = rows;
@@ -357,8 +360,12 @@ static void fold_decode_dev(Est& e, const float* rows, int64_t W, int N) {
     fail(KRUL_E_STATE_CORRUPTION, "decode rows do not cover all tracked layers");
   Ctx& c = *e.ctx;
   ensure_partial(e, (W + 511) / 512);
+  cudaEvent_t kt0 = kt_begin(c, c.s_est);
   launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
                      e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);
+  // algorithmic bytes: tracked rows read once + f64 accumulator RMW
+  kt_end(c, c.s_est, kt0, KT_FOLD_DECODE, 0.0,
+         double(e.layers.size()) * e.H * double(W) * 4.0 + double(e.P()) * e.H * 16.0);
   KB_CUDA(cudaStreamSynchronize(c.s_est));
   ++e.decode_steps;
 }
@@ -622,6 +629,7 @@ int krul_snapshot_set_plan(krul_snapshot* s, const int64_t* p) {
   return guard([&] {
     need(s, "snapshot");
     std::copy(p, p + s->s->N, s->s->p.begin());
+    s->s->serial = next_serial();
   });
 }
 int krul_expand(krul_snapshot* s, int layer, float* k, float* v, int64_t* start, int64_t* end) {
@@ -910,6 +918,51 @@ int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int ep
     g_gemm_force = 0;
     g_gemm_splits = 0;
     c.reset_events();
+  });
+}
+
+
+// ---- measurement support (bench evidence) -----------------------------------
+int krul_launch_count(uint64_t* n) {
+  return guard([&] {
+    need(n, "n");
+    *n = g_launches.load();
+  });
+}
+int krul_ktime_enable(krul_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaDeviceSynchronize());
+    c.drop_graph();  // captured event nodes belong to the previous timing window
+    c.kt.on = on != 0;
+    c.kt.recs.clear();
+    c.kt.next = 0;
+  });
+}
+int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, double* flops,
+                    double* bytes) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaDeviceSynchronize());
+    int64_t n = 0;
+    double t = 0, f = 0, b = 0;
+    for (const auto& r : c.kt.recs) {
+      if (r.tag != tag) continue;
+      float x = 0;
+      KB_CUDA(cudaEventElapsedTime(&x, r.a, r.b));
+      ++n;
+      t += x;
+      f += r.flops;
+      b += r.bytes;
+    }
+    if (launches) *launches = n;
+    if (ms) *ms = t;
+    if (flops) *flops = f;
+    if (bytes) *bytes = b;
   });
 }
 

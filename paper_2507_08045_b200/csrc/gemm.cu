@@ -1190,9 +1190,19 @@ bool gemm_uses_tc(const Ctx& c, const void* A, int64_t lda, const void* B, int64
          (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
 }
 
+void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A,
+               int64_t lda, const void* B, int64_t ldb, const Epi& e);
+
 void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A,
           int64_t lda, const void* B, int64_t ldb, const Epi& e) {
   if (M <= 0 || N <= 0) return;
+  cudaEvent_t kt0 = kt_begin(c, s);
+  gemm_impl(c, s, M, N, K, A, lda, B, ldb, e);
+  kt_end(c, s, kt0, KT_GEMM, 2.0 * double(M) * double(N) * double(K), 0.0);
+}
+
+void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A,
+               int64_t lda, const void* B, int64_t ldb, const Epi& e) {
   const bool tc_ok = gemm_uses_tc(c, A, lda, B, ldb) && K >= 1;
   if (e.kind == Epi::QKV && !tc_ok) fail(KRUL_E_CUDA, "fused QKV epilogue requires the tcgen05 path");
   if (tc_ok) {

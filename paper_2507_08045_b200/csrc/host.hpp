@@ -24,12 +24,12 @@ void check_tokens(const Ctx& c, const int32_t* t, int64_t n);
 int32_t* upload_tokens(Ctx& c, cudaStream_t s, const int32_t* t, int64_t n, DevBuf& buf);
 void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_tok, int64_t n,
                   int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits,
-                  cudaEvent_t* layer_done = nullptr);
+                  const Mark* layer_done = nullptr);
 void prefill(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, float* logits);
 void prefill_new(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, float* logits);
 void decode_step(Ctx& c, Conv& conv, int32_t tok, float* logits);
 void enqueue_partial(Ctx& c, cudaStream_t s, Conv& conv, const int32_t* d_tok,
-                     const std::vector<int64_t>& p, bool full_last, cudaEvent_t* ev);
+                     const std::vector<int64_t>& p, bool full_last, const Mark* ev);
 void check_plan_shape(const Ctx& c, int64_t n, const int64_t* p, int np);
 void partial_recompute(Ctx& c, Conv& conv, const int32_t* tok, int64_t n, const int64_t* p,
                        int np);
@@ -72,7 +72,9 @@ struct Snapshot {
   std::vector<Blob> blobs;
   PinnedBuf host;  // all blobs, compute dtype, [K: Hkv][rows][hd][V: ...]
   size_t total = 0;
+  uint64_t serial = 0;  // changes whenever blobs or plan change (graph cache key)
 };
+uint64_t next_serial();
 int validate_plan_snapshot(const std::vector<int64_t>& p, int64_t L, const Snapshot& s);
 void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
              krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,

@@ -10,6 +10,45 @@ namespace kb {
 
 void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
+std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_buf_gen{0};
+
+cudaEvent_t KTime::ev() {
+  if (next == pool.size()) {
+    cudaEvent_t e;
+    KB_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[next++];
+}
+KTime::~KTime() {
+  for (auto e : pool) cudaEventDestroy(e);
+}
+cudaError_t record_timing(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t r = cudaStreamIsCapturing(s, &cs);
+  if (r != cudaSuccess) return r;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, s);
+}
+void record_mark(const Mark& m, cudaStream_t s) {
+  // timing node first: a join on `dep` then also covers it under capture
+  if (m.tim) KB_CUDA(record_timing(m.tim, s));
+  if (m.dep) KB_CUDA(cudaEventRecord(m.dep, s));
+}
+cudaEvent_t kt_begin(const Ctx& c, cudaStream_t s) {
+  if (!c.kt.on) return nullptr;
+  cudaEvent_t a = c.kt.ev();
+  KB_CUDA(record_timing(a, s));
+  return a;
+}
+void kt_end(const Ctx& c, cudaStream_t s, cudaEvent_t a, int tag, double flops, double bytes) {
+  if (!a) return;
+  cudaEvent_t b = c.kt.ev();
+  KB_CUDA(record_timing(b, s));
+  c.kt.recs.push_back({tag, flops, bytes, a, b});
+}
+
 DevBuf::~DevBuf() {
   if (p) cudaFree(p);
 }
@@ -20,6 +59,7 @@ void* DevBuf::ensure(size_t n) {
     bytes = 0;
     KB_CUDA(cudaMalloc(&p, n));
     bytes = n;
+    g_buf_gen.fetch_add(1);
   }
   return p;
 }
@@ -33,6 +73,7 @@ void* PinnedBuf::ensure(size_t n) {
     bytes = 0;
     KB_CUDA(cudaMallocHost(&p, n));
     bytes = n;
+    g_buf_gen.fetch_add(1);
   }
   return p;
 }
@@ -94,9 +135,19 @@ uint64_t config_hash(const Cfg& c) {
   return h;
 }
 
+void Ctx::drop_graph() {
+  if (rg.exec) cudaGraphExecDestroy(rg.exec);
+  for (auto& m : rg.ev) {
+    if (m.dep) cudaEventDestroy(m.dep);
+    if (m.tim) cudaEventDestroy(m.tim);
+  }
+  rg = RestoreGraph{};
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
+  drop_graph();
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto s : {s_comp, s_load, s_new, s_est, s_exp})
     if (s) cudaStreamDestroy(s);

@@ -25,7 +25,20 @@ Ctx* ctx_create(int device, const krul_model_desc& desc) {
   try {
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_load, cudaStreamNonBlocking));
-    KB_CUDA(cudaStreamCreateWithFlags(&c->s_new, cudaStreamNonBlocking));
+    {
+      // stream priorities (lower number = higher priority): the new-input
+      // prefill and the recompute are both on the TTFT critical path
+      int lo = 0, hi = 0;
+      KB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const char* pv = std::getenv("KRUL_NEW_PRIO");
+      const int prio = pv && pv[0] == 'h' ? hi : lo;
+      KB_CUDA(cudaStreamCreateWithPriority(&c->s_new, cudaStreamNonBlocking, prio));
+      const char* cv = std::getenv("KRUL_COMP_PRIO");
+      if (cv && cv[0] == 'h') {
+        KB_CUDA(cudaStreamDestroy(c->s_comp));
+        KB_CUDA(cudaStreamCreateWithPriority(&c->s_comp, cudaStreamNonBlocking, hi));
+      }
+    }
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_est, cudaStreamNonBlocking));
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_exp, cudaStreamNonBlocking));
     KB_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -349,7 +362,7 @@ static AttnArgs capture_for_layer(const Ctx& c, const AttnArgs& base, int l) {
 // Per-layer waits (restore events) are honoured when given.
 void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_tok, int64_t n,
                   int64_t pos0, float* d_logits, const std::vector<cudaEvent_t>* waits,
-                  cudaEvent_t* layer_done) {
+                  const Mark* layer_done) {
   const Cfg& g = c.cfg;
   WS w = ws_get(c, set, n);
   AttnArgs cap{};
@@ -364,7 +377,7 @@ void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_
     }
     AttnArgs a = capture_for_layer(c, cap, l);
     layer_forward(c, s, w, conv, l, hin, n, pos0, n, hout, &a);
-    if (layer_done) KB_CUDA(cudaEventRecord(layer_done[l], s));
+    if (layer_done) record_mark(layer_done[l], s);
     std::swap(hin, hout);
   }
   launch_logits(c, s, hin + (n - 1) * g.d, d_logits);
@@ -433,7 +446,7 @@ void decode_step(Ctx& c, Conv& conv, int32_t tok, float* logits) {
 
 // engine.cpp:448-489, enqueued on `s`; records ev[l] after layer l's K/V.
 void enqueue_partial(Ctx& c, cudaStream_t s, Conv& conv, const int32_t* d_tok,
-                     const std::vector<int64_t>& p, bool full_last, cudaEvent_t* ev) {
+                     const std::vector<int64_t>& p, bool full_last, const Mark* ev) {
   const Cfg& g = c.cfg;
   WS w = ws_get(c, 0, p[0]);
   launch_embed(c, s, d_tok, p[0], w.h);
@@ -446,7 +459,7 @@ void enqueue_partial(Ctx& c, cudaStream_t s, Conv& conv, const int32_t* d_tok,
       layer_forward(c, s, w, conv, l, hin, pre, 0, out, hout, nullptr);
       std::swap(hin, hout);
     }
-    if (ev) KB_CUDA(cudaEventRecord(ev[l], s));
+    if (ev) record_mark(ev[l], s);
   }
 }
 

@@ -15,6 +15,8 @@
 //                    on computed[l] and loaded[l] only (K7), so it overlaps the
 //                    remaining restore instead of trailing it.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include "host.hpp"
@@ -67,6 +69,7 @@ static Snapshot* new_snapshot(Ctx& c, const krul_pair* pairs, int np, const int6
   s->mode = mode;
   s->pairs.assign(pairs, pairs + np);
   s->p.assign(p, p + c.cfg.N);
+  s->serial = next_serial();
   return s;
 }
 
@@ -150,7 +153,103 @@ void snapshot_expand(const Snapshot& s, int layer, float* k, float* v, int64_t* 
   snapshot_blob_f32(s, found, ws - bl.start, we - ws, k, v);
 }
 
-// scheduler.cpp:320-336 checks, then the DAG.
+uint64_t next_serial() {
+  static std::atomic<uint64_t> s{1};
+  return s.fetch_add(1);
+}
+
+// The restore DAG on the ctx streams (all asynchronous, joined back into
+// s_comp). Events: ev[0] launch, ev[1] compute end, ev[2] load end, ev[3]
+// end, ev[4] H2D end, ev[5..5+N) computed[l], then loaded[l], then newp[l].
+static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const int32_t* tp_hist,
+                            const int32_t* tp_new, int64_t n_new, float* lp, double* h2d_out,
+                            double* expand_out) {
+  const Cfg& g = c.cfg;
+  const std::vector<int64_t>& p = snap.p;
+  auto& E = c.rg.ev;
+  const Mark &ev0 = E[0], &ev_c_end = E[1], &ev_l_end = E[2], &ev_end = E[3], &ev_h2d_end = E[4];
+  const Mark* computed = E.data() + 5;
+  const Mark* loaded = computed + g.N;
+  const Mark* newp = loaded + g.N;
+  cudaStream_t sc = c.s_comp, sl = c.s_load;
+  char* stg = static_cast<char*>(c.staging.p);
+  float* d_logits = static_cast<float*>(c.ws_logits.p);
+
+  // token uploads first: a small H2D queued behind the blob copies on the
+  // copy engine would hold the recompute back for the whole load (~14 ms)
+  record_mark(ev0, sc);
+  int32_t* d_tok = upload_tokens(c, sc, tp_hist, std::max<int64_t>(p[0], 0), c.ws_tok);
+  int32_t* d_new = tp_new ? upload_tokens(c, sc, tp_new, n_new, c.ws_tok2) : nullptr;
+  cudaEvent_t tok_ready = c.event();
+  KB_CUDA(cudaEventRecord(tok_ready, sc));
+  KB_CUDA(cudaStreamWaitEvent(sl, tok_ready, 0));
+  KB_CUDA(cudaStreamWaitEvent(c.s_exp, ev0.dep, 0));
+  // ---- load stream: K4 H2D copies back to back on the copy engine; K5
+  // expand kernels on their own stream behind each blob's copy, so the PCIe
+  // link never idles while a scatter runs.
+  double h2d = 0, expand_bytes = 0;
+  std::vector<cudaEvent_t> copied(snap.blobs.size());
+  for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
+    const auto& b = snap.blobs[bi];
+    copied[bi] = c.event();
+    if (b.bytes) {
+      KB_CUDA(cudaMemcpyAsync(stg + b.off, static_cast<char*>(snap.host.p) + b.off, b.bytes,
+                              cudaMemcpyHostToDevice, sl));
+      h2d += double(b.bytes);
+    }
+    KB_CUDA(cudaEventRecord(copied[bi], sl));
+  }
+  record_mark(ev_h2d_end, sl);
+  for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
+    const auto& b = snap.blobs[bi];
+    KB_CUDA(cudaStreamWaitEvent(c.s_exp, copied[bi], 0));
+    for (int o : b.owners) {
+      if (o < 0) continue;
+      launch_expand(c, c.s_exp, stg + b.off, b.start, L, conv, o, p[size_t(o)]);
+      expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;
+      record_mark(loaded[o], c.s_exp);
+    }
+  }
+  record_mark(ev_l_end, c.s_exp);
+  // ---- compute stream: K6 pyramid recompute
+  if (p[0] > 0) {
+    enqueue_partial(c, sc, conv, d_tok, p, false, computed);
+  } else {
+    for (int l = 0; l < g.N; ++l) record_mark(computed[l], sc);
+  }
+  record_mark(ev_c_end, sc);
+  // ---- new-input prefill (K7) on its own stream, layer l behind
+  // computed[l] and loaded[l], so it tracks the load events while the
+  // recompute runs (KRUL_TWO_STREAM=0: same stream, after the recompute).
+  static const bool two_stream = [] {
+    const char* v = std::getenv("KRUL_TWO_STREAM");
+    return !(v && v[0] == '0');
+  }();
+  if (tp_new) {
+    cudaStream_t sn = two_stream ? c.s_new : sc;
+    if (two_stream) KB_CUDA(cudaStreamWaitEvent(sn, tok_ready, 0));
+    std::vector<cudaEvent_t> waits;
+    for (int l = 0; l < g.N; ++l) waits.push_back(computed[l].dep);
+    for (int l = 0; l < g.N; ++l) waits.push_back(loaded[l].dep);
+    conv.len = L;
+    forward_rows(c, sn, 1, conv, d_new, n_new, L, d_logits, &waits, newp);
+    record_mark(ev_end, sn);
+    if (two_stream) KB_CUDA(cudaStreamWaitEvent(sc, ev_end.dep, 0));
+  } else {
+    record_mark(ev_end, sc);
+  }
+  // join every forked stream back into s_comp
+  KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end.dep, 0));
+  KB_CUDA(cudaStreamWaitEvent(sc, ev_h2d_end.dep, 0));
+  if (lp) KB_CUDA(cudaMemcpyAsync(lp, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sc));
+  *h2d_out = h2d;
+  *expand_out = expand_bytes;
+}
+
+// scheduler.cpp:320-336 checks, then the DAG. The DAG of a repeated
+// (snapshot, conversation, shape) is captured once into a CUDA graph and
+// replayed: one host launch instead of ~600, so the streams start
+// back-to-back on the device.
 void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
              krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
              double* ttft_ms) {
@@ -172,89 +271,93 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   }
   if (L + std::max<int64_t>(n_new, 0) > conv.capacity) fail(KRUL_E_CONFIG, "history exceeds the conversation capacity");
   KB_CUDA(cudaSetDevice(c.device));
+  const int64_t nh = std::max<int64_t>(p[0], 0), nn = new_tok ? n_new : 0;
 
-  c.reset_events();
-  cudaEvent_t ev0 = c.event(), ev_c_end = c.event(), ev_l_end = c.event(), ev_end = c.event();
-  cudaEvent_t ev_h2d_end = c.event();
-  std::vector<cudaEvent_t> computed(size_t(g.N)), loaded(size_t(g.N)), newp(size_t(g.N));
-  for (auto& e : computed) e = c.event();
-  for (auto& e : loaded) e = c.event();
-  for (auto& e : newp) e = c.event();
+  // pinned token / logits staging (the previous restore has completed)
+  int32_t* tp = static_cast<int32_t*>(c.tok_pin.ensure(size_t(nh + nn + 1) * 4));
+  if (nh) std::memcpy(tp, hist, size_t(nh) * 4);
+  if (nn) std::memcpy(tp + nh, new_tok, size_t(nn) * 4);
+  float* lp = (logits && new_tok) ? static_cast<float*>(c.logits_pin.ensure(size_t(g.V) * 4)) : nullptr;
+  c.staging.ensure(std::max<size_t>(snap.total, 256));
+  c.ws_logits.ensure(size_t(g.V) * 4);
 
-  cudaStream_t sc = c.s_comp, sl = c.s_load;
-  char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(snap.total, 256)));
-  // tokens of the recomputed prefix (pinned bounce keeps the copy async)
-  int32_t* d_tok = upload_tokens(c, sc, hist, std::max<int64_t>(p[0], 0), c.ws_tok);
-  float* d_logits = static_cast<float*>(c.ws_logits.ensure(size_t(g.V) * 4));
-  int32_t* d_new = nullptr;
-
-  KB_CUDA(cudaEventRecord(ev0, sc));
-  KB_CUDA(cudaStreamWaitEvent(sl, ev0, 0));
-  KB_CUDA(cudaStreamWaitEvent(c.s_exp, ev0, 0));
-  // ---- load stream: K4 H2D copies back to back on the copy engine; K5
-  // expand kernels on their own stream behind each blob's copy event, so
-  // the PCIe link never idles while a scatter runs.
-  double h2d = 0, expand_bytes = 0;
-  std::vector<cudaEvent_t> copied(snap.blobs.size());
-  for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
-    const auto& b = snap.blobs[bi];
-    copied[bi] = c.event();
-    if (b.bytes) {
-      KB_CUDA(cudaMemcpyAsync(stg + b.off, static_cast<char*>(snap.host.p) + b.off, b.bytes,
-                              cudaMemcpyHostToDevice, sl));
-      h2d += double(b.bytes);
+  auto& G = c.rg;
+  const bool same = G.snap_serial == snap.serial && G.conv == &conv && G.L == L && G.n_new == nn &&
+                    G.kt_on == c.kt.on && G.logits == (lp != nullptr) &&
+                    G.capture_probs == c.capture_probs && G.buf_gen == g_buf_gen.load();
+  if (!same) {
+    c.drop_graph();
+    G.snap_serial = snap.serial;
+    G.conv = &conv;
+    G.L = L;
+    G.n_new = nn;
+    G.kt_on = c.kt.on;
+    G.logits = lp != nullptr;
+    G.capture_probs = c.capture_probs;
+    G.ev.resize(size_t(5 + 3 * g.N));
+    for (auto& m : G.ev) {
+      KB_CUDA(cudaEventCreateWithFlags(&m.dep, cudaEventDisableTiming));
+      KB_CUDA(cudaEventCreate(&m.tim));
     }
-    KB_CUDA(cudaEventRecord(copied[bi], sl));
+    G.buf_gen = g_buf_gen.load();
   }
-  KB_CUDA(cudaEventRecord(ev_h2d_end, sl));
-  for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
-    const auto& b = snap.blobs[bi];
-    KB_CUDA(cudaStreamWaitEvent(c.s_exp, copied[bi], 0));
-    for (int o : b.owners) {
-      if (o < 0) continue;
-      launch_expand(c, c.s_exp, stg + b.off, b.start, L, conv, o, p[size_t(o)]);
-      expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;
-      KB_CUDA(cudaEventRecord(loaded[size_t(o)], c.s_exp));
+  static const bool graphs_env = [] {
+    const char* v = std::getenv("KRUL_GRAPHS");
+    return !(v && v[0] == '0');
+  }();
+  const bool graphs = c.use_graphs && graphs_env;
+  const int32_t* tp_new = new_tok ? tp + nh : nullptr;
+  if (graphs && G.exec) {
+    KB_CUDA(cudaGraphLaunch(G.exec, c.s_comp));
+    g_launches.fetch_add(G.launches);
+    conv.len = L + nn;
+  } else {
+    if (!G.exec) {
+      c.kt.recs.clear();
+      c.kt.next = 0;
     }
+    c.reset_events();
+    if (graphs && G.seen >= 1) {
+      const uint64_t l0 = g_launches.load();
+      KB_CUDA(cudaStreamBeginCapture(c.s_comp, cudaStreamCaptureModeRelaxed));
+      try {
+        enqueue_restore(c, conv, snap, L, tp, tp_new, nn, lp, &G.h2d, &G.expand_bytes);
+      } catch (...) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(c.s_comp, &junk);
+        if (junk) cudaGraphDestroy(junk);
+        c.use_graphs = false;
+        throw;
+      }
+      cudaGraph_t graph = nullptr;
+      KB_CUDA(cudaStreamEndCapture(c.s_comp, &graph));
+      const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        G.exec = nullptr;
+        c.use_graphs = false;
+        fail(KRUL_E_CUDA, std::string("restore graph instantiation failed: ") + cudaGetErrorString(ie));
+      }
+      G.launches = g_launches.load() - l0;
+      G.buf_gen = g_buf_gen.load();
+      KB_CUDA(cudaGraphLaunch(G.exec, c.s_comp));
+    } else {
+      enqueue_restore(c, conv, snap, L, tp, tp_new, nn, lp, &G.h2d, &G.expand_bytes);
+      ++G.seen;
+      G.buf_gen = g_buf_gen.load();  // workspaces sized by this run
+    }
+    conv.len = L + nn;
   }
-  KB_CUDA(cudaEventRecord(ev_l_end, c.s_exp));
-  // ---- compute stream: K6 pyramid recompute
-  if (p[0] > 0) {
-    enqueue_partial(c, sc, conv, d_tok, p, false, computed.data());
-  } else {
-    for (auto& e : computed) KB_CUDA(cudaEventRecord(e, sc));
-  }
-  KB_CUDA(cudaEventRecord(ev_c_end, sc));
-  // ---- new-input prefill (K7) layer-wise behind both streams
-  if (new_tok) {
-    cudaStream_t sn = c.s_new;
-    KB_CUDA(cudaStreamWaitEvent(sn, ev0, 0));
-    d_new = upload_tokens(c, sn, new_tok, n_new, c.ws_tok2);
-    std::vector<cudaEvent_t> waits;
-    waits.insert(waits.end(), computed.begin(), computed.end());
-    waits.insert(waits.end(), loaded.begin(), loaded.end());
-    conv.len = L;
-    forward_rows(c, sn, 1, conv, d_new, n_new, L, d_logits, &waits, newp.data());
-    KB_CUDA(cudaEventRecord(ev_end, sn));
-    KB_CUDA(cudaStreamWaitEvent(sc, ev_end, 0));
-    KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end, 0));
-    conv.len = L + n_new;
-  } else {
-    KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end, 0));
-    KB_CUDA(cudaEventRecord(ev_end, sc));
-    conv.len = L;
-  }
-  if (logits && new_tok)
-    KB_CUDA(cudaMemcpyAsync(logits, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sc));
-  KB_CUDA(cudaStreamSynchronize(sc));
-  KB_CUDA(cudaStreamSynchronize(sl));
-  KB_CUDA(cudaStreamSynchronize(c.s_exp));
+  KB_CUDA(cudaStreamSynchronize(c.s_comp));
+  if (lp) std::memcpy(logits, lp, size_t(g.V) * 4);
 
+  std::vector<cudaEvent_t> E;
+  for (const auto& mk : G.ev) E.push_back(mk.tim);
   float tc = 0, tl = 0, te = 0, th = 0;
-  KB_CUDA(cudaEventElapsedTime(&tc, ev0, ev_c_end));
-  KB_CUDA(cudaEventElapsedTime(&tl, ev0, ev_l_end));
-  KB_CUDA(cudaEventElapsedTime(&te, ev0, ev_end));
-  KB_CUDA(cudaEventElapsedTime(&th, ev0, ev_h2d_end));
+  KB_CUDA(cudaEventElapsedTime(&tc, E[0], E[1]));
+  KB_CUDA(cudaEventElapsedTime(&tl, E[0], E[2]));
+  KB_CUDA(cudaEventElapsedTime(&te, E[0], E[3]));
+  KB_CUDA(cudaEventElapsedTime(&th, E[0], E[4]));
   if (ttft_ms) *ttft_ms = te;
   // measured per-layer timeline (ms from restore launch), the device
   // counterpart of PipelineTrace (scheduler.hpp:71-97)
@@ -263,12 +366,12 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   c.tl_new.assign(size_t(g.N), 0.0);
   for (int l = 0; l < g.N; ++l) {
     float a = 0, b = 0, e = 0;
-    KB_CUDA(cudaEventElapsedTime(&a, ev0, computed[size_t(l)]));
-    KB_CUDA(cudaEventElapsedTime(&b, ev0, loaded[size_t(l)]));
+    KB_CUDA(cudaEventElapsedTime(&a, E[0], E[5 + l]));
+    KB_CUDA(cudaEventElapsedTime(&b, E[0], E[5 + g.N + l]));
     c.tl_compute[size_t(l)] = a;
     c.tl_load[size_t(l)] = b;
     if (new_tok) {
-      KB_CUDA(cudaEventElapsedTime(&e, ev0, newp[size_t(l)]));
+      KB_CUDA(cudaEventElapsedTime(&e, E[0], E[5 + 2 * g.N + l]));
       c.tl_new[size_t(l)] = e;
     }
   }
@@ -287,9 +390,9 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     st->load_ms = tl;
     st->restore_ms = mk;
     st->bubble_compute = mk > 0 && p[0] > 0 ? (mk - tc) / mk : 0.0;
-    st->bubble_load = mk > 0 && h2d > 0 ? (mk - tl) / mk : 0.0;
-    st->h2d_bytes = h2d;
-    st->expand_bytes = expand_bytes;
+    st->bubble_load = mk > 0 && G.h2d > 0 ? (mk - tl) / mk : 0.0;
+    st->h2d_bytes = G.h2d;
+    st->expand_bytes = G.expand_bytes;
     st->recompute_flops = fl;
     st->h2d_ms = th;
   }

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -26,7 +27,17 @@ struct Error : std::runtime_error {
     if (e_ != cudaSuccess)                                                   \
       ::kb::fail(KRUL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
-#define KB_LAUNCH() KB_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by KB_LAUNCH(), which also
+// counts it (krul_launch_count: the bench's gpu_launches evidence).
+extern std::atomic<uint64_t> g_launches;
+// bumped whenever a DevBuf / PinnedBuf (re)allocates: a captured CUDA graph
+// that baked in workspace addresses is stale once this moves
+extern std::atomic<uint64_t> g_buf_gen;
+#define KB_LAUNCH()                                   \
+  do {                                                \
+    ::kb::g_launches.fetch_add(1, std::memory_order_relaxed); \
+    KB_CUDA(cudaGetLastError());                      \
+  } while (0)
 
 // Blocking copies/memsets that are ordered against the library's
 // non-blocking streams: plain cudaMemcpy/cudaMemset run on the legacy stream,
@@ -115,6 +126,38 @@ struct Conv {
 
 struct Est;
 
+// Per-launch kernel timing (krul_ktime_*): CUDA events bracket each
+// instrumented launch on the stream it runs on; algorithmic flops / bytes
+// are attached so the bench derives achieved TFLOP/s and GB/s per kernel
+// class from the same timed step.
+enum KTag { KT_GEMM = 0, KT_ATTN = 1, KT_EXPAND = 2, KT_FOLD_DECODE = 3, KT_FOLD_PREFILL = 4,
+            KT_SELECT = 5, KT_COMPRESS = 6, KT_NTAGS = 7 };
+struct KTime {
+  bool on = false;
+  struct Rec {
+    int tag;
+    double flops, bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  cudaEvent_t ev();
+  ~KTime();
+};
+// Timing events recorded while a stream is being captured must be external
+// event-record nodes (a plain cudaEventRecord under capture only expresses a
+// dependency and cannot be timed). A Mark is a dependency event (waited on
+// by other streams) plus a timing event.
+cudaError_t record_timing(cudaEvent_t e, cudaStream_t s);
+struct Mark {
+  cudaEvent_t dep = nullptr, tim = nullptr;
+};
+void record_mark(const Mark& m, cudaStream_t s);
+// returns the start event (nullptr when timing is off)
+cudaEvent_t kt_begin(const Ctx& c, cudaStream_t s);
+void kt_end(const Ctx& c, cudaStream_t s, cudaEvent_t a, int tag, double flops, double bytes);
+
 struct Ctx {
   int device = 0;
   Cfg cfg;
@@ -162,13 +205,32 @@ struct Ctx {
 
   // restore staging + last measured timeline (ms from launch)
   DevBuf staging;
+  PinnedBuf tok_pin;     // pinned token staging (history | new input) for async / graph H2D
+  PinnedBuf logits_pin;  // pinned logits landing buffer
+  // CUDA graph of the last restore DAG (replayed when the key repeats)
+  struct RestoreGraph {
+    uint64_t snap_serial = 0;
+    const void* conv = nullptr;
+    int64_t L = -1, n_new = -1;
+    bool kt_on = false, logits = false;
+    int capture_probs = -1;
+    uint64_t buf_gen = 0;
+    int seen = 0;  // eager runs with this key (capture on the second)
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+    std::vector<Mark> ev;  // ev0, c_end, l_end, end, h2d_end, computed[N], loaded[N], newp[N]
+    double h2d = 0, expand_bytes = 0;
+  } rg;
+  bool use_graphs = true;
   std::vector<double> tl_compute, tl_load, tl_new;
   double tl_h2d_ms = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
 
+  mutable KTime kt;
   ~Ctx();
   cudaEvent_t event();  // recycled timing-capable events
+  void drop_graph();
   void reset_events() { ev_next = 0; }
 };
 

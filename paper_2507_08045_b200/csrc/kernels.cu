@@ -196,7 +196,11 @@ void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                       const AttnArgs& a) {
   if (a.rows <= 0) return;
   if (a.part && attention_tc_supported(c, a)) {
+    // algorithmic flops: QK^T + PV over the causally visible keys of each row
+    const double vis = double(a.rows) * double(a.pos0) + 0.5 * double(a.rows) * double(a.rows + 1);
+    cudaEvent_t kt0 = kt_begin(c, s);
     launch_attention_tc(c, s, conv, layer, a, *a.part);
+    kt_end(c, s, kt0, KT_ATTN, 4.0 * c.cfg.hd * double(c.cfg.H) * vis, 0.0);
     return;
   }
   PageView pv = page_view(c, conv, layer);
@@ -430,13 +434,11 @@ void launch_kv_scatter_f32(const Ctx& c, cudaStream_t s, const Conv& conv, int l
 // kv head): K rows copy with 16-byte vectors; V is transposed through shared
 // memory into the page's V^T block so PV reads stay K-major.
 template <class T>
-__global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView pv,
-                         int64_t from) {
-  extern __shared__ unsigned char smraw[];
-  T* tile = reinterpret_cast<T*>(smraw);  // [kPageTokens][hd + pad]
+__device__ __forceinline__ void expand_tile(const T* blob, int64_t blob_start, int64_t L,
+                                            const PageView& pv, int64_t from, int64_t ti, T* tile) {
   const int hd = pv.hd, Hkv = pv.Hkv;
   const int g = blockIdx.y;
-  const int64_t p0 = (from / kPageTokens + blockIdx.x) * kPageTokens;
+  const int64_t p0 = (from / kPageTokens + ti) * kPageTokens;
   const int64_t lo = p0 > from ? p0 : from, hi = p0 + kPageTokens < L ? p0 + kPageTokens : L;
   if (lo >= hi) return;
   const int64_t rows_blob = L - blob_start;
@@ -495,21 +497,48 @@ __global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView 
     }
   }
 }
+// One CTA per (page tile, kv head), or a CTA-capped grid-stride loop over
+// the tiles (KRUL_EXPAND_CTAS) so the scatter leaves SMs to the recompute.
+template <class T>
+__global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView pv, int64_t from,
+                         int64_t tiles) {
+  extern __shared__ unsigned char smraw[];
+  T* tile = reinterpret_cast<T*>(smraw);  // [kPageTokens][hd + pad]
+  for (int64_t ti = blockIdx.x; ti < tiles; ti += gridDim.x) {
+    expand_tile(blob, blob_start, L, pv, from, ti, tile);
+    __syncthreads();
+  }
+}
+
+void launch_expand_impl(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,
+                        const Conv& conv, int layer, int64_t from);
 void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,
                    const Conv& conv, int layer, int64_t from) {
   if (from >= L) return;
+  cudaEvent_t kt0 = kt_begin(c, s);
+  launch_expand_impl(c, s, blob, blob_start, L, conv, layer, from);
+  // bytes: the K and V rows read from the staged blob and written to pages
+  kt_end(c, s, kt0, KT_EXPAND, 0.0, 2.0 * 2.0 * double(L - from) * c.cfg.Hkv * c.cfg.hd * double(c.esz));
+}
+void launch_expand_impl(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,
+                        const Conv& conv, int layer, int64_t from) {
   PageView pv = page_view(c, conv, layer);
   const int64_t tiles = (L - 1) / kPageTokens - from / kPageTokens + 1;
   dim3 grid(unsigned(tiles), unsigned(c.cfg.Hkv));
+  static const int cap = [] {
+    const char* v = std::getenv("KRUL_EXPAND_CTAS");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (cap > 0) grid.x = unsigned(std::min<int64_t>(tiles, std::max(1, cap / int(c.cfg.Hkv))));
   const size_t smem = size_t(kPageTokens) * (c.cfg.hd + 2) * c.esz + 16;
   if (c.cfg.dtype == KRUL_BF16) {
     KB_CUDA(cudaFuncSetAttribute(k_expand<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
-    k_expand<bf16><<<grid, 256, smem, s>>>((const bf16*)blob, blob_start, L, pv, from);
+    k_expand<bf16><<<grid, 256, smem, s>>>((const bf16*)blob, blob_start, L, pv, from, tiles);
   } else {
     KB_CUDA(cudaFuncSetAttribute(k_expand<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
-    k_expand<float><<<grid, 256, smem, s>>>((const float*)blob, blob_start, L, pv, from);
+    k_expand<float><<<grid, 256, smem, s>>>((const float*)blob, blob_start, L, pv, from, tiles);
   }
   KB_LAUNCH();
 }

@@ -305,6 +305,15 @@ class Context:
                                             mode, reps, C.byref(r), _p(tt)))
         return r.value, tt
 
+    def ktime_enable(self, on: bool):
+        _check(lib().krul_ktime_enable(self.h, int(bool(on))))
+
+    def ktime_read(self, tag: int):
+        """(launches, ms, flops, bytes) of the timed launches of a kernel class."""
+        n, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        _check(lib().krul_ktime_read(self.h, tag, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
+        return n.value, ms.value, fl.value, by.value
+
     def measure_rates(self, scratch):
         b, f = C.c_double(), C.c_double()
         _check(lib().krul_measure_rates(self.h, scratch.h, C.byref(b), C.byref(f)))
@@ -429,6 +438,13 @@ class CompressionStrategy:
     @property
     def shared(self):
         return sorted({x for p in self.pairs for x in p[:2]})
+
+
+def launch_count() -> int:
+    """Kernels launched by this library in this process (bench evidence)."""
+    v = C.c_uint64()
+    _check(lib().krul_launch_count(C.byref(v)))
+    return v.value
 
 
 def shared_layer_quota(n_layers, r_l):
