@@ -345,7 +345,7 @@ static void fold_prefill_dev(Est& e, const float* probs, int64_t rows, int64_t W
   if (e.prefill_done) fail(KRUL_E_ACCOUNTING, "prefill attention folded twice");
   if (!e.layers.empty() && e.layers.back() >= N) fail(KRUL_E_CONFIG, "record does not cover all tracked layers");
   Ctx& c = *e.ctx;
-  ensure_partial(e, (rows * W + 511) / 512);
+  ensure_partial(e, (rows * W + kFoldChunk - 1) / kFoldChunk);
   cudaEvent_t kt0 = kt_begin(c, c.s_est);
   launch_fold_prefill(c.s_est, probs, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
                       e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);
@@ -359,7 +359,7 @@ static void fold_decode_dev(Est& e, const float* rows, int64_t W, int N) {
   if (!e.layers.empty() && e.layers.back() >= N)
     fail(KRUL_E_STATE_CORRUPTION, "decode rows do not cover all tracked layers");
   Ctx& c = *e.ctx;
-  ensure_partial(e, (W + 511) / 512);
+  ensure_partial(e, (W + kFoldChunk - 1) / kFoldChunk);
   cudaEvent_t kt0 = kt_begin(c, c.s_est);
   launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
                      e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);

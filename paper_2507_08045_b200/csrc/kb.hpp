@@ -59,6 +59,7 @@ inline cudaError_t kb_memset_sync(void* d, int v, size_t n) {
 }
 
 constexpr int kPageTokens = 64;  // tokens per KV page
+constexpr int kFoldChunk = 256;  // estimator fold: columns per stage-1 CTA
 
 // Model configuration (engine.hpp:17-29 + extensions).
 struct Cfg {

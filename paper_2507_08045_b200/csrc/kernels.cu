@@ -594,55 +594,64 @@ void launch_compress(const Ctx& c, cudaStream_t s, const Conv& conv, int deep, i
 // 128-bit loads) and one warp per pair reduces sum((f32 a - f32 b)^2) in
 // double (analysis.cpp:146-147) with warp shuffles. Stage 2 adds the chunk
 // partials in a fixed order (deterministic, no fp atomics).
-constexpr int kFoldChunk = 512;
+constexpr int kFoldPad = kFoldChunk + 1;  // row pitch: lanes of different layers hit different banks
+constexpr int kFoldThreads = 512;
+// Stage 1, one CTA per (column chunk, head): every tracked layer's chunk is
+// staged in shared memory once (the only HBM read of the step buffer), then
+// each THREAD owns a pair (a, b) and walks the chunk with four independent
+// f64 accumulators -- no shuffles, no per-pair reductions. Partials are
+// written [chunk][head][pair] (coalesced over pairs).
 template <bool kExactDiff>
-__global__ void k_fold_stage1(const float* rows, int64_t layer_stride, int64_t head_stride,
-                              int64_t total, int H, const int* layers, int n, double* partial) {
-  extern __shared__ float fs[];  // [n][kFoldChunk]
+__global__ void __launch_bounds__(kFoldThreads) k_fold_stage1(
+    const float* __restrict__ rows, int64_t layer_stride, int64_t head_stride, int64_t total, int H,
+    const int* layers, int n, double* __restrict__ partial) {
+  extern __shared__ float fs[];  // [n][kFoldPad]
   const int h = blockIdx.y;
   const int64_t c0 = int64_t(blockIdx.x) * kFoldChunk;
   const int cw = int(total - c0 < kFoldChunk ? total - c0 : kFoldChunk);
   for (int a = 0; a < n; ++a) {
     const float* src = rows + int64_t(layers[a]) * layer_stride + int64_t(h) * head_stride + c0;
-    float* dst = fs + a * kFoldChunk;
-    if ((cw & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-      for (int i = threadIdx.x; i < cw / 4; i += blockDim.x)
-        reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
-    } else {
-      for (int i = threadIdx.x; i < cw; i += blockDim.x) dst[i] = src[i];
-    }
+    for (int i = threadIdx.x; i < cw; i += blockDim.x) fs[a * kFoldPad + i] = __ldg(src + i);
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int P = n * (n - 1) / 2;
-  for (int p = warp; p < P; p += nw) {
-    // decode p -> (a, b), a < b
-    int a = 0, rem = p;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    int a = 0, rem = p;  // p -> (a, b), a < b, analysis.cpp:84-93 order
     while (rem >= n - 1 - a) {
       rem -= n - 1 - a;
       ++a;
     }
     const int b = a + 1 + rem;
-    const float* x = fs + a * kFoldChunk;
-    const float* y = fs + b * kFoldChunk;
-    double acc = 0.0;
-    for (int i = lane; i < cw; i += 32) {
-      // decode rows: f32 difference (analysis.cpp:146-147); prefill: the
-      // reference's expanded double form is exact in the operands, so the
-      // difference is taken in double.
-      const double d = kExactDiff ? double(x[i]) - double(y[i]) : double(x[i] - y[i]);
-      acc += d * d;
+    const float* x = fs + a * kFoldPad;
+    const float* y = fs + b * kFoldPad;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int i = 0;
+    for (; i + 4 <= cw; i += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        // decode rows: f32 difference (analysis.cpp:146-147); prefill: the
+        // reference's expanded double form is exact in the operands, so the
+        // difference is taken in double.
+        const double d = kExactDiff ? double(x[i + u]) - double(y[i + u]) : double(x[i + u] - y[i + u]);
+        acc[u] = fma(d, d, acc[u]);
+      }
     }
-    acc = warp_sum_d(acc);
-    if (lane == 0) partial[(int64_t(blockIdx.x) * P + p) * H + h] = acc;
+    for (; i < cw; ++i) {
+      const double d = kExactDiff ? double(x[i]) - double(y[i]) : double(x[i] - y[i]);
+      acc[0] = fma(d, d, acc[0]);
+    }
+    partial[(int64_t(blockIdx.x) * H + h) * P + p] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
 }
-__global__ void k_fold_stage2(const double* partial, int chunks, int PH, double* sums) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= PH) return;
+// Stage 2: fixed-order sum over chunks (deterministic, no fp atomics) into
+// the [pair][head] accumulator of the reference (analysis.hpp:90).
+__global__ void k_fold_stage2(const double* partial, int chunks, int P, int H, double* sums) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // = h * P + p
+  if (i >= P * H) return;
+  const int h = i / P, p = i % P;
   double acc = 0.0;
-  for (int ch = 0; ch < chunks; ++ch) acc += partial[int64_t(ch) * PH + i];
-  sums[i] += acc;
+  for (int ch = 0; ch < chunks; ++ch) acc += partial[(int64_t(ch) * H + h) * P + p];
+  sums[int64_t(p) * H + h] += acc;
 }
 template <bool kExactDiff>
 static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
@@ -652,13 +661,13 @@ static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
   const int P = n * (n - 1) / 2;
   const int chunks = int((total + kFoldChunk - 1) / kFoldChunk);
   if (int64_t(chunks) * P * H > partial_cap) fail(KRUL_E_CUDA, "fold partial buffer too small");
-  const size_t smem = size_t(n) * kFoldChunk * sizeof(float);
+  const size_t smem = size_t(n) * kFoldPad * sizeof(float);
   KB_CUDA(cudaFuncSetAttribute(k_fold_stage1<kExactDiff>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k_fold_stage1<kExactDiff><<<dim3(unsigned(chunks), unsigned(H)), 256, smem, s>>>(
+  k_fold_stage1<kExactDiff><<<dim3(unsigned(chunks), unsigned(H)), kFoldThreads, smem, s>>>(
       rows, layer_stride, head_stride, total, H, d_layers, n, partial);
   KB_LAUNCH();
-  k_fold_stage2<<<unsigned((P * H + 255) / 256), 256, 0, s>>>(partial, chunks, P * H, sums);
+  k_fold_stage2<<<unsigned((P * H + 255) / 256), 256, 0, s>>>(partial, chunks, P, H, sums);
   KB_LAUNCH();
 }
 void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, const int* d_layers,
