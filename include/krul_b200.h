@@ -290,7 +290,8 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps,
  * krul_launch_count: number of kernels this library has launched (process
  * wide). krul_ktime_*: per-launch CUDA-event timing of instrumented kernel
  * classes (tag: 0 GEMM, 1 attention, 2 expand, 3 decode fold, 4 prefill
- * fold, 5 selector, 6 compress) with their algorithmic flops / bytes. */
+ * fold, 5 selector, 6 compress, 7 weight-streaming GEMM with M <= 128) with
+ * their algorithmic flops / bytes. */
 int krul_launch_count(uint64_t* n);
 int krul_ktime_enable(krul_ctx* ctx, int on);
 int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, double* flops,

@@ -1198,7 +1198,10 @@ void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const v
   if (M <= 0 || N <= 0) return;
   cudaEvent_t kt0 = kt_begin(c, s);
   gemm_impl(c, s, M, N, K, A, lda, B, ldb, e);
-  kt_end(c, s, kt0, KT_GEMM, 2.0 * double(M) * double(N) * double(K), 0.0);
+  // M <= 128: a weight-streaming GEMM (HBM-bound: algorithmic bytes = weights
+  // + activations in + out); larger M: tensor-bound (2MNK flops)
+  const double bytes = double(N) * K * c.esz + double(M) * K * c.esz + double(M) * N * 4.0;
+  kt_end(c, s, kt0, M <= 128 ? KT_GEMM_STREAM : KT_GEMM, 2.0 * double(M) * double(N) * double(K), bytes);
 }
 
 void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const void* A,

@@ -132,7 +132,7 @@ struct Est;
 // are attached so the bench derives achieved TFLOP/s and GB/s per kernel
 // class from the same timed step.
 enum KTag { KT_GEMM = 0, KT_ATTN = 1, KT_EXPAND = 2, KT_FOLD_DECODE = 3, KT_FOLD_PREFILL = 4,
-            KT_SELECT = 5, KT_COMPRESS = 6, KT_NTAGS = 7 };
+            KT_SELECT = 5, KT_COMPRESS = 6, KT_GEMM_STREAM = 7, KT_NTAGS = 8 };
 struct KTime {
   bool on = false;
   struct Rec {
