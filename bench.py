@@ -119,8 +119,12 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # KRUL_BENCH_DEVICE pins every rank to one GPU (multi-rank plumbing
+        # test on a 1-GPU box; NCCL refuses shared devices, so gloo then)
+        if os.environ.get("KRUL_BENCH_DEVICE") is not None:
+            local = int(os.environ["KRUL_BENCH_DEVICE"])
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("KRUL_DIST_BACKEND", "nccl"))
         return rank, local, world, dist
     return rank, local, world, None
 
@@ -531,6 +535,11 @@ def main():
     ap.add_argument("--convs", type=int, default=0,
                     help="batch configs: conversations per rank (0 = the whole LPT shard)")
     args = ap.parse_args()
+    # the CPU legs (reference arm, cpu_baseline) use every host thread, also
+    # under torchrun (which exports OMP_NUM_THREADS=1); the oracle's OpenMP
+    # runtime reads this when its library loads
+    if args.impl == "reference" or not args.no_cpu_baseline:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     rank, local, world, dist = dist_setup()
     if args.impl == "reference":
         out = run_reference(args, rank, local, world, dist)
