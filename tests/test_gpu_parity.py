@@ -390,6 +390,47 @@ def test_restore_and_prefill_matches_oracle(K, oracle):
         assert ttft > 0 and len(conv2) == 576
 
 
+def test_restore_graph_replay_is_exact(K, oracle, monkeypatch):
+    """The restore DAG is run eagerly, then captured into a CUDA graph, then
+    replayed: all three produce bit-identical logits and KV, also after an
+    unrelated call grew the workspaces (the graph must be re-captured, not
+    replayed with stale addresses) and after the plan changed."""
+    kw = dict(n_layers=4, n_heads=4, n_kv_heads=2, head_dim=64, d_model=256, vocab_size=256,
+              ffn_mult=3.5, ffn_kind=1, rope_theta=500000.0, seed=9)
+    monkeypatch.setenv("KRUL_KV_POOL_CONVS", "3")
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, **kw)
+    hist = oracle.tokens(700, 21, 256)
+    new = oracle.tokens(48, 22, 256)
+    prev = ctx.conversation(1024)
+    ctx.prefill(prev, hist)
+    pairs = [(1, 2, 0.0)]
+    snap = K.KVSnapshot.compress(ctx, prev, pairs, K.build_plan(700, 4, 0.2, pairs), 700,
+                                 K.MERGE_MEAN)
+    conv = ctx.conversation(1024)
+    runs = [ctx.restore_and_prefill(conv, hist, snap, new)[0] for _ in range(4)]
+    kv0 = [conv.kv(l, 0, 748) for l in range(4)]
+    for r in runs[1:]:
+        assert np.array_equal(r, runs[0])
+    big = ctx.conversation(1024)
+    ctx.prefill(big, oracle.tokens(1000, 23, 256))  # grows the shared workspaces
+    again = ctx.restore_and_prefill(conv, hist, snap, new)[0]
+    again2 = ctx.restore_and_prefill(conv, hist, snap, new)[0]
+    assert np.array_equal(again, runs[0]) and np.array_equal(again2, runs[0])
+    for l in range(4):
+        k, v = conv.kv(l, 0, 748)
+        assert np.array_equal(k, kv0[l][0]) and np.array_equal(v, kv0[l][1])
+    # a new plan on the same snapshot object invalidates the graph: a larger
+    # r_c still covers its load spans (recompute more, load a suffix of each
+    # stored blob), a smaller one does not
+    snap.set_plan(K.build_plan(700, 4, 0.35, pairs))
+    more = [ctx.restore_and_prefill(conv, hist, snap, new)[0] for _ in range(3)]
+    assert np.array_equal(more[1], more[0]) and np.array_equal(more[2], more[0])
+    assert not np.array_equal(more[0], runs[0])  # rows [p_l(0.2), p_l(0.35)) recomputed, not merged
+    snap.set_plan(K.build_plan(700, 4, 0.1, pairs))
+    with pytest.raises(K.RestorationGapError):
+        ctx.restore_and_prefill(conv, hist, snap, new)
+
+
 def test_restore_rejects_mismatch(K, oracle):  # test_scheduler.cpp:402-430
     kw = dict(n_layers=2, n_heads=1, head_dim=4, d_model=4, vocab_size=7)
     ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
