@@ -318,6 +318,24 @@ def test_selector_bit_exact(K, oracle):
 
 # ----------------------------------------------------------------- kvstore + restore
 
+def test_selector_golden_kats(K):
+    """K3 on the device against the reference's hand-built selector KATs
+    (tests/golden/kat.json <- test_strategy.cpp:89-134)."""
+    import json
+    import os
+    kat = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "kat.json")))["kat"]
+    ctx = K.Context(K.ModelConfig(n_layers=6, n_heads=1, head_dim=4, d_model=4, vocab_size=4,
+                                  dtype=K.KRUL_F32, max_tokens=16), 0)
+    h = kat["select_hand"]
+    s = K.select_strategy(ctx, np.array(h["D"], float), h["layers"], h["layers"], h["r_l"],
+                          h["n_layers"])
+    assert [list(p) for p in s.pairs] == h["pairs"] and s.exhausted_before_quota == h["exhausted"]
+    t = kat["select_ties"]
+    D = np.ones((t["n"], t["n"])) - np.eye(t["n"])
+    s = K.select_strategy(ctx, D, list(range(t["n"])), list(range(t["n"])), t["r_l"], t["n"])
+    assert [list(p) for p in s.pairs] == t["pairs"]
+
+
 def test_snapshot_compress_matches_oracle(K, oracle):
     kw = dict(n_layers=4, n_heads=2, head_dim=4, d_model=8, vocab_size=13, seed=21)
     ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
