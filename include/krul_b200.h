@@ -297,6 +297,13 @@ int krul_ktime_enable(krul_ctx* ctx, int on);
 int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, double* flops,
                     double* bytes);
 
+/* Device time of one decode fold (K1) on the last captured decode rows,
+ * `iters` back to back into a scratch accumulator (estimator state untouched). */
+int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* bytes_per_fold);
+
+/* Kernel-tuning aid: times `iters` tcgen05 attention launches over conv's pages. */
+int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0,
+                          int dbg, int target, int iters, float* ms_per_iter);
 /* Kernel-tuning aid: times `iters` device-resident bf16 GEMMs (not a product entry). */
 int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
                           int splits, int iters, float* ms_per_iter);

@@ -33,10 +33,12 @@ __device__ __forceinline__ void bar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  // non-blocking probe loop: the handoffs of this pipeline are short and a
+  // suspended try_wait adds its wake-up latency to every one of them
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra D_%=;\n\t"
       "bra W_%=;\n"
       "D_%=:\n\t}" ::"r"(su32(b)),
@@ -129,7 +131,16 @@ struct AttnTc {
   float* part;     // [slot][rows][H][HD + 3] (o..., m, l, mass) for split q tiles
   double* mass;    // [H][rows] region mass, may be null
   int64_t il, rs;
+  int dbg;  // tuning only (krul_debug_attn_bench): 1 = no softmax math, 2 = also no KV loads
+  unsigned long long* ts;  // tuning only: per-block timestamps of CTA (0, 0)
 };
+__device__ __forceinline__ void attn_ts(const AttnTc& p, int i, int slot) {
+  if (p.ts && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.ts[i * 8 + slot] = t;
+  }
+}
 
 // number of 64-key blocks q tile qt attends to, and its work-item count
 __host__ __device__ __forceinline__ int attn_nblk(const AttnTc& p, int qt) {
@@ -237,6 +248,10 @@ __global__ void __launch_bounds__(320, 1)
         tca::bar_wait(&kv_empty[s], ((i / STAGES) & 1) ^ 1);
         const int pg = p.pt[min(b0 + i, p.max_pages - 1)];
         unsigned char* st = sKV + s * STAGE_BYTES;
+        if (p.dbg == 2 && i >= STAGES) {  // tuning: reuse the staged KV, no loads
+          tca::bar_arrive(&kv_full[s]);
+          continue;
+        }
         tca::bar_expect(&kv_full[s], STAGE_BYTES);
 #pragma unroll
         for (int h = 0; h < NKV; ++h) {
@@ -261,6 +276,7 @@ __global__ void __launch_bounds__(320, 1)
       auto issue_s = [&](int i) {
         const int s = i % STAGES;
         tca::bar_wait(&kv_full[s], (i / STAGES) & 1);
+        attn_ts(p, i, 0);
         tca::fence_after();
         for (int h = 0; h < nh; ++h) {
           const unsigned char* kt = sKV + s * STAGE_BYTES + (SHARED ? 0 : h) * (K_BYTES + V_BYTES);
@@ -273,6 +289,7 @@ __global__ void __launch_bounds__(320, 1)
                        tca::desc(kt + j * (KB * 128) + k * 32), idS, (j | k) != 0);
           tca::commit(&s_full[h * 2 + (i & 1)]);
         }
+        attn_ts(p, i, 1);
       };
       issue_s(0);
       for (int i = 0; i < nb; ++i) {
@@ -281,6 +298,7 @@ __global__ void __launch_bounds__(320, 1)
         const int sp = i % STAGES;
         for (int h = 0; h < nh; ++h) {
           tca::bar_wait(&p_ready[h], i & 1);
+          if (h == 0) attn_ts(p, i, 2);
           tca::fence_after();
           const unsigned char* vt =
               sKV + sp * STAGE_BYTES + (SHARED ? 0 : h) * (K_BYTES + V_BYTES) + K_BYTES;
@@ -290,6 +308,7 @@ __global__ void __launch_bounds__(320, 1)
             tca::mma(dO, tca::desc(sP + h * P_BYTES + k * 32), tca::desc(vt + k * 32), idO,
                      (i | k) != 0);
           tca::commit(&o_done[h]);
+          if (h == 0) attn_ts(p, i, 3);
         }
         tca::commit(&kv_empty[sp]);
       }
@@ -309,10 +328,25 @@ __global__ void __launch_bounds__(320, 1)
       for (int i = 0; i < nb; ++i) {
         const int64_t k0 = int64_t(b0 + i) * KB;
         tca::bar_wait(&s_full[wg * 2 + (i & 1)], (i >> 1) & 1);
+        if (threadIdx.x == 0) attn_ts(p, i, 4);
         tca::fence_after();
         uint32_t v[64];
         tca::ld32(tS + uint32_t((i & 1) * 64), v);
         tca::ld32(tS + uint32_t((i & 1) * 64 + 32), v + 32);
+        if (threadIdx.x == 0) attn_ts(p, i, 5);
+        if (p.dbg) {  // tuning: pipeline without the softmax arithmetic
+          if (i > 0) {
+            tca::bar_wait(&o_done[wg], (i - 1) & 1);
+            tca::fence_after();
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) = make_uint4(v[q], v[q + 8], v[q + 16], v[q + 24]);
+          tca::fence_before();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tca::bar_arrive(&p_ready[wg]);
+          continue;
+        }
         // visible keys of this row in the block: [k0, k0 + nv)
         const int nv = int(imax64(0, imin64(KB, min(qpos + 1, p.kv_total) - k0)));
         float x[64];
@@ -369,6 +403,7 @@ __global__ void __launch_bounds__(320, 1)
           tca::bar_wait(&o_done[wg], (i - 1) & 1);
           tca::fence_after();
         }
+        if (threadIdx.x == 0) attn_ts(p, i, 6);
         if (i > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           uint32_t o[32];
 #pragma unroll 1
@@ -389,6 +424,7 @@ __global__ void __launch_bounds__(320, 1)
         tca::fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tca::bar_arrive(&p_ready[wg]);
+        if (threadIdx.x == 0) attn_ts(p, i, 7);
       }
       if (nb > 0) {
         tca::bar_wait(&o_done[wg], (nb - 1) & 1);
@@ -555,6 +591,9 @@ void run_fa(const Ctx& c, cudaStream_t s, dim3 grid, const CUtensorMap& tq, cons
   KB_LAUNCH();
 }
 
+int g_attn_dbg = 0;     // tuning knob (krul_debug_attn_bench)
+unsigned long long* g_attn_ts = nullptr;  // tuning: device timestamp buffer
+int g_attn_target = 0;  // tuning knob: key blocks per work item (0 = heuristic)
 void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                          const AttnArgs& a, DevBuf& scratch) {
   const Cfg& g = c.cfg;
@@ -586,6 +625,9 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   const int64_t sms = c.sm_count > 0 ? c.sm_count : 148;
   p.target = int(std::max<int64_t>(8, (total * pairs + sms - 1) / sms));
   p.target = std::max(p.target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
+  if (g_attn_target > 0) p.target = std::max(g_attn_target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
+  p.dbg = g_attn_dbg;
+  p.ts = g_attn_ts;
   int items = 0, max_split = 1;
   for (int qt = 0; qt < p.n_qtiles; ++qt) {
     items += attn_nsplit(p, qt);

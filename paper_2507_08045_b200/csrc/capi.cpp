@@ -5,6 +5,7 @@
 // krul_status. The estimator and selector live here because they are thin:
 // their arithmetic is the K1/K2/K3 kernels in kernels.cu.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -75,7 +76,9 @@ void need(const void* p, const char* what) {
   if (!p) fail(KRUL_E_ARG, std::string("null ") + what);
 }
 void ensure_partial(Est& e, int64_t chunks) {
-  const int64_t need_n = std::max<int64_t>(chunks, 1) * std::max(e.P(), 1) * e.H;
+  // per chunk and head: the packed upper-triangle Gram (n(n+1)/2 entries)
+  const int64_t n = int64_t(e.layers.size());
+  const int64_t need_n = (std::max<int64_t>(chunks, 1) + 1) * std::max<int64_t>(n * (n + 1) / 2, 1) * e.H;
   if (need_n > e.partial_cap) {
     e.partial.ensure(size_t(need_n) * 8);
     e.partial_cap = need_n;
@@ -963,6 +966,100 @@ int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, doubl
     if (ms) *ms = t;
     if (flops) *flops = f;
     if (bytes) *bytes = b;
+  });
+}
+
+
+// Attention timing for kernel tuning (not on the product path): fills
+// `conv`'s pages for [0, pos0 + rows) of `layer` with the history's real
+// prefill first (caller's job), then times `iters` launches of the tcgen05
+// attention for `rows` query rows at position pos0 with random Q.
+int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0,
+                          int dbg, int target, int iters, float* ms_per_iter) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    Ctx& c = *ctx->c;
+    if (c.cfg.dtype != KRUL_BF16) fail(KRUL_E_CONFIG, "attention bench needs a bf16 context");
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t s = c.s_comp;
+    DevBuf q, out, part;
+    void* dq = q.ensure(size_t(rows) * c.cfg.qd() * 2);
+    launch_init_uniform(c, s, dq, rows * c.cfg.qd(), 5, 5, 1.0f);
+    AttnArgs a{};
+    a.q = dq;
+    a.rows = rows;
+    a.pos0 = pos0;
+    a.out = out.ensure(size_t(rows) * c.cfg.qd() * 2);
+    a.part = &part;
+    g_attn_dbg = dbg;
+    g_attn_target = target;
+    for (int i = 0; i < 2; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
+    if (std::getenv("KRUL_ATTN_TS")) {  // one launch with per-block timestamps of CTA (0, 0)
+      DevBuf tsb;
+      g_attn_ts = static_cast<unsigned long long*>(tsb.ensure(64 * 8 * 8));
+      KB_CUDA(cudaMemsetAsync(g_attn_ts, 0, 64 * 8 * 8, s));
+      launch_attention_tc(c, s, *conv->v, layer, a, part);
+      std::vector<unsigned long long> h(64 * 8);
+      KB_CUDA(cudaStreamSynchronize(s));
+      KB_CUDA(kb_memcpy_sync(h.data(), g_attn_ts, h.size() * 8, cudaMemcpyDeviceToHost));
+      g_attn_ts = nullptr;
+      const unsigned long long t0 = h[0];
+      for (int i = 0; i < 64 && h[i * 8 + 4]; ++i) {
+        std::fprintf(stderr, "blk %2d:", i);
+        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %7.0f", h[i * 8 + k] ? double(h[i * 8 + k] - t0) : -1.0);
+        std::fprintf(stderr, "\n");
+      }
+    }
+    cudaEvent_t e0 = c.event(), e1 = c.event();
+    KB_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
+    KB_CUDA(cudaEventRecord(e1, s));
+    KB_CUDA(cudaEventSynchronize(e1));
+    g_attn_dbg = 0;
+    g_attn_target = 0;
+    float ms = 0;
+    KB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_iter = ms / float(iters);
+    c.reset_events();
+  });
+}
+
+
+// Device time of the decode fold (K1) on the last captured decode rows:
+// `iters` folds enqueued back to back on the estimator stream between two
+// events (no host gaps), into a scratch accumulator (the estimator's sums
+// are untouched). bytes_per_fold = the algorithmic HBM bytes of one fold.
+int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* bytes_per_fold) {
+  return guard([&] {
+    need(est, "est");
+    Est& e = *est->e;
+    Ctx& c = *e.ctx;
+    if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaDeviceSynchronize());
+    const int64_t W = c.dec_width;
+    ensure_partial(e, (W + kFoldChunk - 1) / kFoldChunk);
+    DevBuf scratch;
+    double* sums = static_cast<double*>(scratch.ensure(size_t(std::max(e.P(), 1)) * e.H * 8));
+    const float* rows = c.dec_rows.as<float>();
+    launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()), sums,
+                       e.partial.as<double>(), e.partial_cap);  // warm
+    cudaEvent_t a, b;
+    KB_CUDA(cudaEventCreate(&a));
+    KB_CUDA(cudaEventCreate(&b));
+    KB_CUDA(cudaEventRecord(a, c.s_est));
+    for (int i = 0; i < iters; ++i)
+      launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()), sums,
+                         e.partial.as<double>(), e.partial_cap);
+    KB_CUDA(cudaEventRecord(b, c.s_est));
+    KB_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    KB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms_per_fold = ms / float(std::max(iters, 1));
+    *bytes_per_fold = double(e.layers.size()) * e.H * double(W) * 4.0 + double(e.P()) * e.H * 16.0;
   });
 }
 

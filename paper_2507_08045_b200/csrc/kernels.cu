@@ -39,12 +39,49 @@ __global__ void k_rmsnorm(const float* h, int d, T* out) {
   const float denom = sqrtf(ss / float(d) + 1e-6f);
   for (int j = threadIdx.x; j < d; j += blockDim.x) out[r * d + j] = fromf<T>(x[j] / denom);
 }
+// bf16 fast path (d in {256, 512, 4096}): one warp per row, the row held
+// in registers (16-byte loads, one HBM pass), shuffle reduction, 8-byte
+// packed bf16 stores; same arithmetic per element as k_rmsnorm.
+template <int V>  // float4 vectors per lane: d = 128 * V
+__global__ void __launch_bounds__(256) k_rmsnorm_warp(const float* __restrict__ h, int64_t rows,
+                                                      int d, bf16* __restrict__ out) {
+  const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const float4* x = reinterpret_cast<const float4*>(h + r * d);
+  float4 v[V];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    v[i] = __ldg(x + lane + 32 * i);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  ss = warp_sum(ss);
+  const float denom = sqrtf(ss / float(d) + 1e-6f);
+  uint2* o = reinterpret_cast<uint2*>(out + r * d);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[i].x / denom, v[i].y / denom);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[i].z / denom, v[i].w / denom);
+    o[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
 void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, void* xn) {
   if (rows <= 0) return;
+  const int d = c.cfg.d;
+  if (c.cfg.dtype == KRUL_BF16 && d % 128 == 0 && d <= 128 * 32) {
+    const unsigned blocks = unsigned((rows + 7) / 8);
+    switch (d / 128) {
+      case 32: k_rmsnorm_warp<32><<<blocks, 256, 0, s>>>(h, rows, d, (bf16*)xn); KB_LAUNCH(); return;
+      case 2: k_rmsnorm_warp<2><<<blocks, 256, 0, s>>>(h, rows, d, (bf16*)xn); KB_LAUNCH(); return;
+      case 4: k_rmsnorm_warp<4><<<blocks, 256, 0, s>>>(h, rows, d, (bf16*)xn); KB_LAUNCH(); return;
+      default: break;
+    }
+  }
   if (c.cfg.dtype == KRUL_BF16)
-    k_rmsnorm<<<unsigned(rows), 256, 0, s>>>(h, c.cfg.d, (bf16*)xn);
+    k_rmsnorm<<<unsigned(rows), 256, 0, s>>>(h, d, (bf16*)xn);
   else
-    k_rmsnorm<<<unsigned(rows), 256, 0, s>>>(h, c.cfg.d, (float*)xn);
+    k_rmsnorm<<<unsigned(rows), 256, 0, s>>>(h, d, (float*)xn);
   KB_LAUNCH();
 }
 
@@ -594,85 +631,200 @@ void launch_compress(const Ctx& c, cudaStream_t s, const Conv& conv, int deep, i
 // 128-bit loads) and one warp per pair reduces sum((f32 a - f32 b)^2) in
 // double (analysis.cpp:146-147) with warp shuffles. Stage 2 adds the chunk
 // partials in a fixed order (deterministic, no fp atomics).
-constexpr int kFoldPad = kFoldChunk + 1;  // row pitch: lanes of different layers hit different banks
-constexpr int kFoldThreads = 512;
-// Stage 1, one CTA per (column chunk, head): every tracked layer's chunk is
-// staged in shared memory once (the only HBM read of the step buffer), then
-// each THREAD owns a pair (a, b) and walks the chunk with four independent
-// f64 accumulators -- no shuffles, no per-pair reductions. Partials are
-// written [chunk][head][pair] (coalesced over pairs).
-template <bool kExactDiff>
-__global__ void __launch_bounds__(kFoldThreads) k_fold_stage1(
+// Estimator fold as a per-head Gram matrix on the FP64 tensor path.
+// For every tracked pair (a, b) and head h the reference accumulates
+// sum_w (A_a - A_b)^2 (decode: analysis.cpp:146-147; prefill: the expanded
+// sum a^2 + sum b^2 - 2 sum ab of analysis.hpp:37-50). Both equal
+// G_aa + G_bb - 2 G_ab with G = R R^T, R = the tracked layers' rows of head
+// h. G is computed with mma.sync.m8n8k4 f64 over 8x8 layer tiles: the f32
+// probabilities are widened once per element (not once per pair), products
+// are exact in f64 and accumulation is f64, so the prefill fold is the
+// reference's expanded form up to summation order and the decode fold
+// differs from the reference's f32-rounded difference by <= 2^-23 relative
+// per term. Stage 1: one CTA per (column chunk, head) stages the chunk of
+// every tracked row in shared memory (the only HBM read), each warp owns a
+// set of upper-triangle 8x8 tiles, and the CTA writes the chunk's packed
+// upper-triangle Gram [n(n+1)/2]. Stage 2 sums the chunks in fixed order
+// (deterministic, no fp atomics) and folds G into the [pair][head] sums.
+constexpr int kGramPitch = kFoldChunk + 4;  // f64 row pitch: fragment loads spread over banks
+constexpr int kGramThreads = 256;
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(kGramThreads) k_fold_gram(
     const float* __restrict__ rows, int64_t layer_stride, int64_t head_stride, int64_t total, int H,
-    const int* layers, int n, double* __restrict__ partial) {
-  extern __shared__ float fs[];  // [n][kFoldPad]
+    const int* layers, int n, int chunks_per_cta, double* __restrict__ partial) {
+  extern __shared__ double R[];  // [n8][kGramPitch] then G [n8][n8]
+  const int n8 = (n + 7) & ~7;
+  double* G = R + n8 * kGramPitch;
   const int h = blockIdx.y;
-  const int64_t c0 = int64_t(blockIdx.x) * kFoldChunk;
-  const int cw = int(total - c0 < kFoldChunk ? total - c0 : kFoldChunk);
-  for (int a = 0; a < n; ++a) {
-    const float* src = rows + int64_t(layers[a]) * layer_stride + int64_t(h) * head_stride + c0;
-    for (int i = threadIdx.x; i < cw; i += blockDim.x) fs[a * kFoldPad + i] = __ldg(src + i);
-  }
-  __syncthreads();
-  const int P = n * (n - 1) / 2;
-  for (int p = threadIdx.x; p < P; p += blockDim.x) {
-    int a = 0, rem = p;  // p -> (a, b), a < b, analysis.cpp:84-93 order
-    while (rem >= n - 1 - a) {
-      rem -= n - 1 - a;
-      ++a;
-    }
-    const int b = a + 1 + rem;
-    const float* x = fs + a * kFoldPad;
-    const float* y = fs + b * kFoldPad;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    int i = 0;
-    for (; i + 4 <= cw; i += 4) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = n8 / 8, ntiles = T * (T + 1) / 2;
+  constexpr int kMaxTilesPerWarp = 7;  // 55 tiles (80 layers) over 8 warps
+  double acc[kMaxTilesPerWarp][2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        // decode rows: f32 difference (analysis.cpp:146-147); prefill: the
-        // reference's expanded double form is exact in the operands, so the
-        // difference is taken in double.
-        const double d = kExactDiff ? double(x[i + u]) - double(y[i + u]) : double(x[i + u] - y[i + u]);
-        acc[u] = fma(d, d, acc[u]);
+  for (int j = 0; j < kMaxTilesPerWarp; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int cc = 0; cc < chunks_per_cta; ++cc) {
+  const int64_t c0 = (int64_t(blockIdx.x) * chunks_per_cta + cc) * kFoldChunk;
+  if (c0 >= total) break;
+  const int cw = int(total - c0 < kFoldChunk ? total - c0 : kFoldChunk);
+  __syncthreads();  // the previous chunk's fragments have been consumed
+  // thread -> 4 consecutive columns of rows q, q + 4, q + 8, ...; batches of
+  // 8 independent 16-byte loads in flight (a store-after-load loop would
+  // serialise one HBM round trip per row)
+  {
+    const int c4 = (threadIdx.x & 63) * 4, q = threadIdx.x >> 6;
+    const bool vec = cw == kFoldChunk && ((reinterpret_cast<uintptr_t>(rows) | layer_stride | head_stride) & 3) == 0;
+    for (int a0 = q; a0 < n8; a0 += 32) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int a = a0 + 4 * u;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a < n) {
+          const float* src = rows + int64_t(layers[a]) * layer_stride + int64_t(h) * head_stride + c0 + c4;
+          if (vec) {
+            v[u] = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            v[u].x = c4 < cw ? __ldg(src) : 0.f;
+            v[u].y = c4 + 1 < cw ? __ldg(src + 1) : 0.f;
+            v[u].z = c4 + 2 < cw ? __ldg(src + 2) : 0.f;
+            v[u].w = c4 + 3 < cw ? __ldg(src + 3) : 0.f;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int a = a0 + 4 * u;
+        if (a < n8) {
+          double* d = R + a * kGramPitch + c4;
+          d[0] = v[u].x;
+          d[1] = v[u].y;
+          d[2] = v[u].z;
+          d[3] = v[u].w;
+        }
       }
     }
-    for (; i < cw; ++i) {
-      const double d = kExactDiff ? double(x[i]) - double(y[i]) : double(x[i] - y[i]);
-      acc[0] = fma(d, d, acc[0]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kMaxTilesPerWarp; ++j) {
+    const int t = warp + j * (kGramThreads / 32);
+    if (t >= ntiles) break;
+    int I = 0, rem = t;  // t -> (I <= J)
+    while (rem >= T - I) {
+      rem -= T - I;
+      ++I;
     }
-    partial[(int64_t(blockIdx.x) * H + h) * P + p] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    const int J = I + rem;
+    const double* ra = R + (I * 8 + (lane >> 2)) * kGramPitch + (lane & 3);
+    const double* rb = R + (J * 8 + (lane >> 2)) * kGramPitch + (lane & 3);
+#pragma unroll 8
+    for (int k = 0; k < kFoldChunk; k += 4) dmma_8x8x4(acc[j][0], acc[j][1], ra[k], rb[k]);
+  }
+  }  // chunk loop
+#pragma unroll
+  for (int j = 0; j < kMaxTilesPerWarp; ++j) {
+    const int t = warp + j * (kGramThreads / 32);
+    if (t >= ntiles) break;
+    int I = 0, rem = t;
+    while (rem >= T - I) {
+      rem -= T - I;
+      ++I;
+    }
+    const int J = I + rem;
+    const int gr = I * 8 + (lane >> 2), gc = J * 8 + (lane & 3) * 2;
+    G[gr * n8 + gc] = acc[j][0];
+    G[gr * n8 + gc + 1] = acc[j][1];
+  }
+  __syncthreads();
+  const int NE = n * (n + 1) / 2;
+  double* out = partial + (int64_t(blockIdx.x) * H + h) * NE;
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    int a = 0, rem = e;  // packed upper triangle incl. diagonal, row-major
+    while (rem >= n - a) {
+      rem -= n - a;
+      ++a;
+    }
+    out[e] = G[a * n8 + a + rem];
   }
 }
-// Stage 2: fixed-order sum over chunks (deterministic, no fp atomics) into
-// the [pair][head] accumulator of the reference (analysis.hpp:90).
-__global__ void k_fold_stage2(const double* partial, int chunks, int P, int H, double* sums) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // = h * P + p
-  if (i >= P * H) return;
-  const int h = i / P, p = i % P;
-  double acc = 0.0;
-  for (int ch = 0; ch < chunks; ++ch) acc += partial[(int64_t(ch) * H + h) * P + p];
-  sums[int64_t(p) * H + h] += acc;
+__device__ __forceinline__ int gram_idx(int n, int a, int b) {  // a <= b
+  return a * n - a * (a - 1) / 2 + (b - a);
 }
-template <bool kExactDiff>
+// Stage 2a: fixed-order sums of the per-chunk Gram entries (one thread per
+// (head, entry), all chunk loads in flight; deterministic, no fp atomics).
+__global__ void k_fold_gsum(const double* __restrict__ partial, int groups, int NE, int H,
+                            double* __restrict__ gsum) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // = h * NE + e
+  if (i >= int64_t(H) * NE) return;
+  const int h = int(i / NE), e = int(i % NE);
+  double acc = 0.0;
+  for (int g0 = 0; g0 < groups; g0 += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      v[u] = g0 + u < groups ? partial[(int64_t(g0 + u) * H + h) * NE + e] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc += v[u];
+  }
+  gsum[i] = acc;
+}
+// Stage 2b: sums[p][h] += max(0, G_aa + G_bb - 2 G_ab) (clamp: analysis.hpp:49).
+__global__ void k_fold_pairs(const double* __restrict__ gsum, int n, int H, double* sums) {
+  const int P = n * (n - 1) / 2, NE = n * (n + 1) / 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // = p * H + h (sums layout)
+  if (i >= P * H) return;
+  const int p = i / H, h = i % H;
+  int a = 0, rem = p;  // p -> (a, b), a < b, analysis.cpp:84-93 order
+  while (rem >= n - 1 - a) {
+    rem -= n - 1 - a;
+    ++a;
+  }
+  const int b = a + 1 + rem;
+  const double* g = gsum + int64_t(h) * NE;
+  const double v = g[gram_idx(n, a, a)] + g[gram_idx(n, b, b)] - 2.0 * g[gram_idx(n, a, b)];
+  sums[i] += v > 0.0 ? v : 0.0;
+}
 static void fold_common(cudaStream_t s, const float* rows, int64_t layer_stride,
                         int64_t head_stride, int64_t total, int H, const int* d_layers, int n,
                         double* sums, double* partial, int64_t partial_cap) {
   if (n < 2 || total <= 0) return;
-  const int P = n * (n - 1) / 2;
+  const int P = n * (n - 1) / 2, NE = n * (n + 1) / 2;
   const int chunks = int((total + kFoldChunk - 1) / kFoldChunk);
-  if (int64_t(chunks) * P * H > partial_cap) fail(KRUL_E_CUDA, "fold partial buffer too small");
-  const size_t smem = size_t(n) * kFoldPad * sizeof(float);
-  KB_CUDA(cudaFuncSetAttribute(k_fold_stage1<kExactDiff>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k_fold_stage1<kExactDiff><<<dim3(unsigned(chunks), unsigned(H)), kFoldThreads, smem, s>>>(
-      rows, layer_stride, head_stride, total, H, d_layers, n, partial);
+  const int n8 = (n + 7) & ~7;
+  if ((n8 / 8) * (n8 / 8 + 1) / 2 > 8 * 7) fail(KRUL_E_CONFIG, "too many tracked layers for the estimator fold");
+  // chunk groups: enough CTAs (groups x heads) for ~2 per SM, each CTA
+  // accumulating its chunks' Gram tiles in registers
+  // chunk groups: ~2 CTAs (groups x heads) per SM, each CTA accumulating its
+  // chunks' Gram tiles in registers (measured: 1 chunk per CTA is 1.8x slower)
+  const int groups = std::max(1, std::min(chunks, (2 * 148 + H - 1) / H));
+  const int per = (chunks + groups - 1) / groups;
+  const int g_used = (chunks + per - 1) / per;
+  if (int64_t(g_used + 1) * NE * H > partial_cap) fail(KRUL_E_CUDA, "fold partial buffer too small");
+  const size_t smem = (size_t(n8) * kGramPitch + size_t(n8) * n8) * sizeof(double);
+  if (smem > 227 * 1024) fail(KRUL_E_CONFIG, "too many tracked layers for the estimator fold");
+  static int smem_set = 0;  // raise the opt-in limit once (host call, not per fold)
+  if (int(smem) > smem_set) {
+    KB_CUDA(cudaFuncSetAttribute(k_fold_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    smem_set = int(smem);
+  }
+  k_fold_gram<<<dim3(unsigned(g_used), unsigned(H)), kGramThreads, smem, s>>>(
+      rows, layer_stride, head_stride, total, H, d_layers, n, per, partial);
   KB_LAUNCH();
-  k_fold_stage2<<<unsigned((P * H + 255) / 256), 256, 0, s>>>(partial, chunks, P, H, sums);
+  // the chunk sums land after the chunk partials in the same scratch
+  double* gsum = partial + int64_t(g_used) * NE * H;
+  k_fold_gsum<<<unsigned((int64_t(H) * NE + 255) / 256), 256, 0, s>>>(partial, g_used, NE, H, gsum);
   KB_LAUNCH();
+  k_fold_pairs<<<unsigned((P * H + 255) / 256), 256, 0, s>>>(gsum, n, H, sums);
+  KB_LAUNCH();
+
 }
 void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, const int* d_layers,
                         int n, double* sums, double* partial, int64_t partial_cap) {
-  fold_common<false>(s, rows, int64_t(H) * W, W, W, H, d_layers, n, sums, partial, partial_cap);
+  fold_common(s, rows, int64_t(H) * W, W, W, H, d_layers, n, sums, partial, partial_cap);
 }
 // Prefill fold over the full [rows x W] rectangle per (pair, head): the
 // direct sum of squared differences in double; the reference's expanded
@@ -680,7 +832,7 @@ void launch_fold_decode(cudaStream_t s, const float* rows, int64_t W, int H, con
 void launch_fold_prefill(cudaStream_t s, const float* probs, int64_t rows, int64_t W, int H,
                          const int* d_layers, int n, double* sums, double* partial,
                          int64_t partial_cap) {
-  fold_common<true>(s, probs, int64_t(H) * rows * W, rows * W, rows * W, H, d_layers, n, sums,
+  fold_common(s, probs, int64_t(H) * rows * W, rows * W, rows * W, H, d_layers, n, sums,
                     partial, partial_cap);
 }
 

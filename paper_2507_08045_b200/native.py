@@ -422,6 +422,13 @@ class StreamingEstimator:
         _check(lib().krul_est_finalize(self.h, _p(D)))
         return D[:n, :n]
 
+    def fold_bench(self, iters=20):
+        """(ms, algorithmic bytes) of one decode fold on the last captured
+        decode rows, device-timed back to back (state untouched)."""
+        ms, by = C.c_float(), C.c_double()
+        _check(lib().krul_est_fold_bench(self.h, iters, C.byref(ms), C.byref(by)))
+        return ms.value, by.value
+
     def counts(self):
         a, b = C.c_int64(), C.c_int64()
         _check(lib().krul_est_counts(self.h, C.byref(a), C.byref(b)))

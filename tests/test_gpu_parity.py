@@ -3,7 +3,8 @@ same seeded inputs.
 
 Tolerances (stated per SURVEY.md §8c):
   * f32 parity mode: K/V and logits max-abs <= 1e-4, probabilities <= 1e-5,
-    estimator sums rel <= 1e-6, D rel <= 1e-6; pairs, plans and blob layouts
+    estimator prefill sums rel <= 1e-12, with decode folds rel <= 1e-6 (the
+    reference rounds decode differences to f32), D rel <= 1e-6; pairs, plans and blob layouts
     bit-exact.
   * bf16 perf mode: per-layer relative Frobenius error <= 2e-2 vs the f32
     oracle on identical weights; the selector bit-exact on identical D.
@@ -246,15 +247,22 @@ def test_estimator_folds_match_oracle(K, oracle):
     acc = oracle.Accumulator(tracked, H)
     est.fold_prefill_rows(pre)
     acc.fold_prefill(pre)
+    # prefill: the reference's expanded f64 form (analysis.hpp:37-50) up to
+    # summation order
+    got, want = est.sums(), acc.sums()
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() < 1e-12, (rel.max(), int(rel.argmax()))
     for t in range(5):
         rows = rng.dirichlet(np.ones(s + t), (N, H)).astype(np.float32)
         est.fold_decode_rows(rows)
         acc.fold_decode(rows)
+    # decode: the reference rounds each difference to f32 before squaring
+    # (analysis.cpp:146-147); the Gram form is exact in f64 -> <= 2^-23 per term
     got, want = est.sums(), acc.sums()
     rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
-    assert rel.max() < 1e-9, (rel.max(), int(rel.argmax()), got[rel.argmax()], want[rel.argmax()])
+    assert rel.max() < 1e-6, (rel.max(), int(rel.argmax()), got[rel.argmax()], want[rel.argmax()])
     D, Do = est.finish(), acc.finalize()
-    assert np.allclose(D, Do, rtol=1e-9, atol=1e-12)
+    assert np.allclose(D, Do, rtol=1e-6, atol=1e-12)
     assert est.counts() == (20, 5)
     with pytest.raises(K.AccountingError):
         est.fold_prefill_rows(pre)
