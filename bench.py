@@ -324,6 +324,8 @@ def run_b200(args, rank, local, world, dist):
     e_n, e_ms, _, e_by = kt["expand"]
     s_n, s_ms, _, s_by = kt["gemm_stream"]
     achieved_tf = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    pol = policies_leg(K, ctx, prev, conv, cfg, hist, new, L, r_c, pairs) if (
+        rank == 0 and not args.no_policies) else None
     est = estimator_leg(K, ctx, conv, cfg, spec) if rank == 0 else None
     out = {
         "metric": METRIC,
@@ -395,9 +397,43 @@ def run_b200(args, rank, local, world, dist):
         "gpu_launches_per_step": round(launches / args.steps, 1),
         "clocks": clk,
         "setup_s": {"history_prefill": round(t_prefill, 2)},
+        **({"policies": pol} if pol else {}),
     }
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(args, spec, plan, pairs, budget_s=args.cpu_budget)
+    return out
+
+
+def policies_leg(K, ctx, prev, conv, cfg, hist, new, L, r_c, pairs, warmup=3, steps=5):
+    """The reference's restore policies (harness.cpp:125-162, 198-220) on the
+    same kernels, device TTFT (restore + new-input prefill, graph replay):
+    full-recompute (uniform plan r=1: everything recomputed, nothing
+    loaded), full-load (r=0, keep-deeper), fixed-partial (uniform r=0.4, the
+    reference's default fixed_ratio, harness.hpp:58), fixed-compression
+    (deeper-half adjacent pairs, r=0, harness.cpp:68-76) and krul (the bench's
+    strategy + pyramid plan at the calibrated r_c)."""
+    N = cfg.n_layers
+    deeper = [(i, i + 1, 0.0) for i in range(N // 2, N - 1, 2)]
+    cases = {
+        "full_recompute": ([], K.uniform_plan(L, N, 1.0), K.MERGE_KEEP_DEEPER),
+        "full_load": ([], K.uniform_plan(L, N, 0.0), K.MERGE_KEEP_DEEPER),
+        "fixed_partial": ([], K.uniform_plan(L, N, 0.4), K.MERGE_KEEP_DEEPER),
+        "fixed_compression": (deeper, K.uniform_plan(L, N, 0.0), K.MERGE_MEAN),
+        "krul": (pairs, K.build_plan(L, N, r_c, pairs), K.MERGE_MEAN),
+    }
+    out = {}
+    for name, (pp, plan, mode) in cases.items():
+        snap = K.KVSnapshot.compress(ctx, prev, pp, plan, L, mode)
+        for _ in range(warmup):
+            ctx.restore_and_prefill(conv, hist, snap, new)
+        t = [ctx.restore_and_prefill(conv, hist, snap, new)[2] for _ in range(steps)]
+        full_b, stored_b = snap.storage_report()
+        out[name] = {"ttft_ms": round(float(np.median(t)), 3), "stored_bytes": int(stored_b),
+                     "pairs": len(pp)}
+        del snap
+    k = out["krul"]["ttft_ms"]
+    for name in out:
+        out[name]["krul_speedup"] = round(out[name]["ttft_ms"] / k, 3)
     return out
 
 
@@ -537,6 +573,8 @@ def main():
     ap.add_argument("--config", default="llama3-8b-8k", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-policies", action="store_true",
+                    help="skip the reference-policy TTFT comparison (full recompute / load / fixed)")
     ap.add_argument("--convs", type=int, default=0,
                     help="batch configs: conversations per rank (0 = the whole LPT shard)")
     args = ap.parse_args()

@@ -873,12 +873,19 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
          i += int64_t(gridDim.x) * blockDim.x) {
       const int64_t r = i / q, c = (i % q) * 4;
       float4 a = *reinterpret_cast<const float4*>(P + r * N + c);
-      for (int s = 1; s < splits; ++s) {
-        const float4 b = *reinterpret_cast<const float4*>(P + int64_t(s) * MN + r * N + c);
-        a.x += b.x;
-        a.y += b.y;
-        a.z += b.z;
-        a.w += b.w;
+      for (int s0 = 1; s0 < splits; s0 += 4) {  // 4 partial loads in flight, fixed order
+        float4 b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          b[u] = s0 + u < splits ? *reinterpret_cast<const float4*>(P + int64_t(s0 + u) * MN + r * N + c)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a.x += b[u].x;
+          a.y += b[u].y;
+          a.z += b[u].z;
+          a.w += b[u].w;
+        }
       }
       if (e.kind == Epi::SWIGLU) {
         T* o = static_cast<T*>(e.out) + r * e.ldo + c / 2;
@@ -927,14 +934,26 @@ __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P,
   const int64_t cc = int64_t(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, token group
   const int64_t MN = M * N;
+  // all partial loads of this thread in flight before the (fixed-order) sums
+  float a[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int64_t r = r0 + ty + 8 * j;
-    float a = 0.f;
-    if (r < M && cc + tx < N)
-      for (int s = 0; s < splits; ++s) a += P[int64_t(s) * MN + r * N + cc + tx];
-    t[ty + 8 * j][tx] = a;
+  for (int j = 0; j < 8; ++j) a[j] = 0.f;
+  for (int s0 = 0; s0 < splits; s0 += 4) {
+    float v[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t r = r0 + ty + 8 * j;
+        v[u][j] = (s0 + u < splits && r < M && cc + tx < N) ? P[int64_t(s0 + u) * MN + r * N + cc + tx] : 0.f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += v[u][j];
   }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t[ty + 8 * j][tx] = a[j];
   __syncthreads();
   const int nq = kv.H * kv.hd, nkv = kv.Hkv * kv.hd, half = kv.hd / 2;
   const bool isq = cc < nq, isk = !isq && cc < nq + nkv;
