@@ -91,6 +91,23 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// issue-only variants: several TMEM transfers in flight, one wait
+__device__ __forceinline__ void ld32_async(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TCA_REGS32(r)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void st32_async(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      TCA_IN32(r)
+      : "memory");
+}
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -119,81 +136,86 @@ using tca::imax64;
 using tca::imin64;
 
 struct AttnTc {
-  int H, Hkv, grp;
+  int H, Hkv, grp, hpc;          // hpc: query heads per CTA (2 = a GQA pair sharing one KV head)
   int64_t rows, pos0, kv_total;  // keys [0, kv_total) exist; causal limit per row
-  int n_qtiles, target;          // q tiles of 128 rows; key blocks (64) per work item
+  int n_qtiles, target;          // q tiles of 128 rows; key blocks (128) per work item
   float scale_log2;
   const int* pt;
   int max_pages;
   int k_rows_pp;   // K-view rows per page
   int v_rows_pp;   // V-view rows per page
   bf16* out;       // [rows][H*HD]
-  float* part;     // [slot][rows][H][HD + 3] (o..., m, l, mass) for split q tiles
+  float* part;     // [slot][h][HD + 3][rows] (o..., m, l, mass) for split q tiles
   double* mass;    // [H][rows] region mass, may be null
   int64_t il, rs;
-  int dbg;  // tuning only (krul_debug_attn_bench): 1 = no softmax math, 2 = also no KV loads
-  unsigned long long* ts;  // tuning only: per-block timestamps of CTA (0, 0)
+  int strict_pv;   // wait for PV(i) before S(i+1) (default; KRUL_ATTN_RELAXED=1 skips it)
 };
-__device__ __forceinline__ void attn_ts(const AttnTc& p, int i, int slot) {
-  if (p.ts && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.ts[i * 8 + slot] = t;
-  }
-}
 
-// number of 64-key blocks q tile qt attends to, and its work-item count
+constexpr int kAttnKB = 128;  // keys per block = two 64-token pages
+
+// number of key blocks q tile qt attends to, and its work-item count
 __host__ __device__ __forceinline__ int attn_nblk(const AttnTc& p, int qt) {
   const int64_t q_end = min(int64_t(qt) * 128 + 128, p.rows);
   const int64_t hi = min(p.pos0 + q_end, p.kv_total);
-  return int((hi + 63) / 64);
+  return int((hi + kAttnKB - 1) / kAttnKB);
 }
 __host__ __device__ __forceinline__ int attn_nsplit(const AttnTc& p, int qt) {
   return (attn_nblk(p, qt) + p.target - 1) / p.target;
 }
 
+namespace tca {
+// A operand from TMEM (P), B from shared memory (V^T): the "TS" form
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+}  // namespace tca
+
 // Causal flash attention over the paged KV cache, FA4-style on tcgen05.
-// One CTA = one work item (q tile of 128 rows, key-block range) for a PAIR
-// of query heads. With GQA both heads read the same KV head, so each K/V page
-// is staged once for two heads (SHARED); otherwise both KV heads are staged.
-// Key block = one 64-token page (K [64][hd], V^T [hd][64], TMA SW128).
-//   warps 0-3 (WG A) / 4-7 (WG B): softmax for head A / B, thread = query
-//     row = TMEM lane; S(i) double-buffered in TMEM so QK^T of block i+1
-//     runs on the tensor pipe while block i is exponentiated; the O
-//     correction is lazy (the running max moves only when a row max exceeds
-//     it by > 8 in log2 units, so P <= 2^8 stays exact in bf16 range and
-//     O is rescaled rarely); P goes straight to smem in the UMMA K-major
-//     SW128 layout.
-//   warp 8: TMA producer (Q once, per block K + V^T pages, STAGES ring)
-//   warp 9: MMA issuer: S_A(i), S_B(i), then PV_A(i-1), PV_B(i-1).
-// TMEM (512 cols): S_A[2] 0..127, S_B[2] 128..255, O_A 256.., O_B 384..
-template <int HD, bool SHARED>
+// One CTA = one work item (q tile of 128 rows, key-block range) for up to
+// two query heads; with GQA the two heads read the same KV head, so every
+// K/V page is staged once for both. Key block = 128 keys = two 64-token
+// pages (K [128][hd], V^T [hd][128], TMA SW128, 2-stage ring).
+//   warps 0-3 / 4-7 : softmax of head A / B; thread = query row = TMEM lane.
+//     S (128 fp32 columns) is read once into registers, the probabilities
+//     are written back as bf16 into the first 64 columns of the same TMEM
+//     region (P never touches shared memory), lazy O rescale (the running
+//     max moves only when a row max exceeds it by > 8 in log2), MUFU ex2.
+//   warp 8 : TMA producer.
+//   warp 9 : MMA issuer, ping-pong over the heads: PV_A(i) (TS-MMA, A = P
+//     from TMEM) then S_A(i+1) while head B is exponentiated, then PV_B(i),
+//     S_B(i+1) while head A is -- the tensor pipe and the softmax warps
+//     overlap across the two heads.
+// TMEM (512 columns): S/P_A [0,128), S/P_B [128,256), O_A [256,..), O_B [384,..).
+template <int HD>
 __global__ void __launch_bounds__(320, 1)
     k_attn_fa(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnTc p) {
-  constexpr int KB = 64;
-  constexpr int NSUB = HD / 64;
-  constexpr int STAGES = SHARED ? 3 : 2;
-  constexpr int NKV = SHARED ? 1 : 2;
-  constexpr uint32_t Q_BYTES = 128 * HD * 2;        // per head
-  constexpr uint32_t K_BYTES = KB * HD * 2;         // per KV head
-  constexpr uint32_t V_BYTES = HD * KB * 2;
-  constexpr uint32_t STAGE_BYTES = NKV * (K_BYTES + V_BYTES);
-  constexpr uint32_t P_BYTES = 128 * KB * 2;        // per head
+  constexpr int KB = kAttnKB;
+  constexpr int NSUB = HD / 64;                 // 64-wide hd sub-tiles
+  constexpr uint32_t Q_BYTES = 128 * HD * 2;    // per head
+  constexpr uint32_t K_BYTES = KB * HD * 2;     // [NSUB][128 keys][128 B]
+  constexpr uint32_t V_BYTES = HD * KB * 2;     // [2 key halves][HD rows][128 B]
+  constexpr int KST = 3, VST = 2;  // separate K and V rings: K frees after S, V after PV
   extern __shared__ unsigned char smraw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sQ = base;                       // [2][Q_BYTES]
-  unsigned char* sKV = sQ + 2 * Q_BYTES;          // [STAGES][NKV][K | V]
-  unsigned char* sP = sKV + STAGES * STAGE_BYTES; // [2][P_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
+  unsigned char* sQ = base;                        // [2][Q_BYTES]
+  unsigned char* sK = sQ + 2 * Q_BYTES;            // [KST][K_BYTES]
+  unsigned char* sV = sK + KST * K_BYTES;          // [VST][V_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * V_BYTES);
   uint64_t* q_full = bars;                  // 1
-  uint64_t* kv_full = bars + 1;             // STAGES
-  uint64_t* kv_empty = kv_full + STAGES;    // STAGES
-  uint64_t* s_full = kv_empty + STAGES;     // [2 heads][2 bufs]
-  uint64_t* p_ready = s_full + 4;           // [2 heads]
-  uint64_t* o_done = p_ready + 2;           // [2 heads]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* k_full = bars + 1;              // KST
+  uint64_t* k_empty = k_full + KST;         // KST
+  uint64_t* v_full = k_empty + KST;         // VST
+  uint64_t* v_empty = v_full + VST;         // VST
+  uint64_t* s_full = v_empty + VST;         // [2 heads]
+  uint64_t* p_ready = s_full + 2;           // [2 heads]
+  uint64_t* pv_done = p_ready + 2;          // [2 heads]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // work item -> (q tile, split); heavy (late) q tiles first
@@ -208,21 +230,25 @@ __global__ void __launch_bounds__(320, 1)
   const int b0 = split * p.target;
   const int b1 = min(nblk_all, b0 + p.target);
   const int nb = b1 - b0;
-  const int hA = 2 * blockIdx.y, hB = hA + 1;
-  const bool hasB = hB < p.H;
-  const int gA = hA / p.grp, gB = hasB ? hB / p.grp : gA;
+  const int hA = p.hpc * blockIdx.y, hB = hA + 1;
+  const bool hasB = p.hpc == 2 && hB < p.H;
+  const int g = hA / p.grp;
   const int64_t q0 = int64_t(qt) * 128;
 
   if (threadIdx.x == 0) {
     tca::bar_init(q_full, 1);
-    for (int s = 0; s < STAGES; ++s) {
-      tca::bar_init(&kv_full[s], 1);
-      tca::bar_init(&kv_empty[s], 1);
+    for (int s = 0; s < KST; ++s) {
+      tca::bar_init(&k_full[s], 1);
+      tca::bar_init(&k_empty[s], 1);
     }
-    for (int i = 0; i < 4; ++i) tca::bar_init(&s_full[i], 1);
+    for (int s = 0; s < VST; ++s) {
+      tca::bar_init(&v_full[s], 1);
+      tca::bar_init(&v_empty[s], 1);
+    }
     for (int i = 0; i < 2; ++i) {
+      tca::bar_init(&s_full[i], 1);
       tca::bar_init(&p_ready[i], 128);
-      tca::bar_init(&o_done[i], 1);
+      tca::bar_init(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -243,24 +269,24 @@ __global__ void __launch_bounds__(320, 1)
         tca::tma2d(sQ + j * (128 * 128), &tmQ, q_full, hA * HD + 64 * j, int(q0));
         if (hasB) tca::tma2d(sQ + Q_BYTES + j * (128 * 128), &tmQ, q_full, hB * HD + 64 * j, int(q0));
       }
+      const int voff = p.Hkv * HD + g * HD;
       for (int i = 0; i < nb; ++i) {
-        const int s = i % STAGES;
-        tca::bar_wait(&kv_empty[s], ((i / STAGES) & 1) ^ 1);
-        const int pg = p.pt[min(b0 + i, p.max_pages - 1)];
-        unsigned char* st = sKV + s * STAGE_BYTES;
-        if (p.dbg == 2 && i >= STAGES) {  // tuning: reuse the staged KV, no loads
-          tca::bar_arrive(&kv_full[s]);
-          continue;
+        const int kb = b0 + i;
+        const int pa = p.pt[min(2 * kb, p.max_pages - 1)];
+        const int pb = p.pt[min(2 * kb + 1, p.max_pages - 1)];
+        const int ks = i % KST, vs = i % VST;
+        tca::bar_wait(&k_empty[ks], ((i / KST) & 1) ^ 1);
+        unsigned char* kd = sK + ks * K_BYTES;
+        tca::bar_expect(&k_full[ks], K_BYTES);
+        for (int j = 0; j < NSUB; ++j) {
+          tca::tma2d(kd + j * (KB * 128), &tmK, &k_full[ks], 64 * j, pa * p.k_rows_pp + g * 64);
+          tca::tma2d(kd + j * (KB * 128) + 64 * 128, &tmK, &k_full[ks], 64 * j, pb * p.k_rows_pp + g * 64);
         }
-        tca::bar_expect(&kv_full[s], STAGE_BYTES);
-#pragma unroll
-        for (int h = 0; h < NKV; ++h) {
-          const int g = h == 0 ? gA : gB;
-          unsigned char* kd = st + h * (K_BYTES + V_BYTES);
-          for (int j = 0; j < NSUB; ++j)
-            tca::tma2d(kd + j * (KB * 128), &tmK, &kv_full[s], 64 * j, pg * p.k_rows_pp + g * 64);
-          tca::tma2d(kd + K_BYTES, &tmV, &kv_full[s], 0, pg * p.v_rows_pp + p.Hkv * HD + g * HD);
-        }
+        tca::bar_wait(&v_empty[vs], ((i / VST) & 1) ^ 1);
+        unsigned char* vd = sV + vs * V_BYTES;
+        tca::bar_expect(&v_full[vs], V_BYTES);
+        tca::tma2d(vd, &tmV, &v_full[vs], 0, pa * p.v_rows_pp + voff);
+        tca::tma2d(vd + HD * 128, &tmV, &v_full[vs], 0, pb * p.v_rows_pp + voff);
       }
     }
   } else if (warp == 9) {
@@ -270,47 +296,52 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idO = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(HD >> 3) << 17) |
                                (uint32_t(128 >> 4) << 24);
       const int nh = hasB ? 2 : 1;
-      tca::bar_wait(q_full, 0);
-      // S_h(i) = Q_h K_i^T into S buffer i&1 (last read by softmax(i-2),
-      // whose p_ready was observed before PV(i-2) was issued)
-      auto issue_s = [&](int i) {
-        const int s = i % STAGES;
-        tca::bar_wait(&kv_full[s], (i / STAGES) & 1);
-        attn_ts(p, i, 0);
-        tca::fence_after();
-        for (int h = 0; h < nh; ++h) {
-          const unsigned char* kt = sKV + s * STAGE_BYTES + (SHARED ? 0 : h) * (K_BYTES + V_BYTES);
-          const uint32_t dS = tmem + uint32_t(h * 128 + (i & 1) * 64);
+      auto issue_s = [&](int h, int i) {  // S_h(i) = Q_h K_i^T -> TMEM [h*128, +128)
+        const unsigned char* kt = sK + (i % KST) * K_BYTES;
+        const uint32_t dS = tmem + uint32_t(h * 128);
 #pragma unroll
-          for (int j = 0; j < NSUB; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tca::mma(dS, tca::desc(sQ + h * Q_BYTES + j * (128 * 128) + k * 32),
-                       tca::desc(kt + j * (KB * 128) + k * 32), idS, (j | k) != 0);
-          tca::commit(&s_full[h * 2 + (i & 1)]);
-        }
-        attn_ts(p, i, 1);
-      };
-      issue_s(0);
-      for (int i = 0; i < nb; ++i) {
-        // QK^T of the next block runs while block i is exponentiated
-        if (i + 1 < nb) issue_s(i + 1);
-        const int sp = i % STAGES;
-        for (int h = 0; h < nh; ++h) {
-          tca::bar_wait(&p_ready[h], i & 1);
-          if (h == 0) attn_ts(p, i, 2);
-          tca::fence_after();
-          const unsigned char* vt =
-              sKV + sp * STAGE_BYTES + (SHARED ? 0 : h) * (K_BYTES + V_BYTES) + K_BYTES;
-          const uint32_t dO = tmem + 256 + uint32_t(h * 128);
+        for (int j = 0; j < NSUB; ++j)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            tca::mma(dO, tca::desc(sP + h * P_BYTES + k * 32), tca::desc(vt + k * 32), idO,
-                     (i | k) != 0);
-          tca::commit(&o_done[h]);
-          if (h == 0) attn_ts(p, i, 3);
+            tca::mma(dS, tca::desc(sQ + h * Q_BYTES + j * (128 * 128) + k * 32),
+                     tca::desc(kt + j * (KB * 128) + k * 32), idS, (j | k) != 0);
+        tca::commit(&s_full[h]);
+      };
+      auto issue_pv = [&](int h, int i) {  // O_h += P_h(i) V_i, P from TMEM
+        const unsigned char* vt = sV + (i % VST) * V_BYTES;
+        const uint32_t dO = tmem + 256 + uint32_t(h * 128);
+        const uint32_t aP = tmem + uint32_t(h * 128);
+#pragma unroll
+        for (int k = 0; k < KB / 16; ++k)
+          tca::mma_ts(dO, aP + uint32_t(k * 8), tca::desc(vt + (k >> 2) * (HD * 128) + (k & 3) * 32),
+                      idO, (i | k) != 0);
+        tca::commit(&pv_done[h]);
+      };
+      tca::bar_wait(q_full, 0);
+      tca::bar_wait(&k_full[0], 0);
+      tca::fence_after();
+      for (int h = 0; h < nh; ++h) issue_s(h, 0);
+      tca::commit(&k_empty[0]);
+      for (int i = 0; i < nb; ++i) {
+        for (int h = 0; h < nh; ++h) {
+          tca::bar_wait(&p_ready[h], i & 1);
+          if (h == 0) tca::bar_wait(&v_full[i % VST], (i / VST) & 1);
+          tca::fence_after();
+          issue_pv(h, i);
+          if (i + 1 < nb) {
+            if (h == 0) tca::bar_wait(&k_full[(i + 1) % KST], ((i + 1) / KST) & 1);
+            // P_h(i) lives in S_h's TMEM columns: S_h(i+1) is issued only
+            // once PV_h(i) has consumed them (KRUL_ATTN_RELAXED=1 relies on
+            // the in-order tensor pipe instead; measured no faster)
+            if (p.strict_pv) {
+              tca::bar_wait(&pv_done[h], i & 1);
+              tca::fence_after();
+            }
+            issue_s(h, i + 1);
+          }
         }
-        tca::commit(&kv_empty[sp]);
+        tca::commit(&v_empty[i % VST]);                      // after PV_A(i), PV_B(i)
+        if (i + 1 < nb) tca::commit(&k_empty[(i + 1) % KST]);  // after S_A(i+1), S_B(i+1)
       }
     }
   } else {  // softmax warp groups
@@ -321,89 +352,40 @@ __global__ void __launch_bounds__(320, 1)
     const int64_t qpos = p.pos0 + q0 + r;
     const uint32_t tS = tmem + uint32_t(wg * 128) + lane_off;
     const uint32_t tO = tmem + 256 + uint32_t(wg * 128) + lane_off;
-    unsigned char* prow = sP + wg * P_BYTES + r * 128;
     float m = -INFINITY, l = 0.f, mn = 0.f;
     const bool active = wg == 0 || hasB;
     if (active) {
       for (int i = 0; i < nb; ++i) {
         const int64_t k0 = int64_t(b0 + i) * KB;
-        tca::bar_wait(&s_full[wg * 2 + (i & 1)], (i >> 1) & 1);
-        if (threadIdx.x == 0) attn_ts(p, i, 4);
+        tca::bar_wait(&s_full[wg], i & 1);
         tca::fence_after();
-        uint32_t v[64];
-        tca::ld32(tS + uint32_t((i & 1) * 64), v);
-        tca::ld32(tS + uint32_t((i & 1) * 64 + 32), v + 32);
-        if (threadIdx.x == 0) attn_ts(p, i, 5);
-        if (p.dbg) {  // tuning: pipeline without the softmax arithmetic
-          if (i > 0) {
-            tca::bar_wait(&o_done[wg], (i - 1) & 1);
-            tca::fence_after();
-          }
+        uint32_t v[128];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) = make_uint4(v[q], v[q + 8], v[q + 16], v[q + 24]);
-          tca::fence_before();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          tca::bar_arrive(&p_ready[wg]);
-          continue;
-        }
+        for (int c = 0; c < 4; ++c) tca::ld32_async(tS + uint32_t(c * 32), v + 32 * c);
+        tca::ld_wait();
         // visible keys of this row in the block: [k0, k0 + nv)
         const int nv = int(imax64(0, imin64(KB, min(qpos + 1, p.kv_total) - k0)));
-        float x[64];
 #pragma unroll
-        for (int t = 0; t < 64; ++t) x[t] = __uint_as_float(v[t]) * p.scale_log2;
-        if (nv < KB) {
-#pragma unroll
-          for (int t = 0; t < 64; ++t)
-            if (t >= nv) x[t] = -INFINITY;
+        for (int t = 0; t < 128; ++t) {
+          const float x = __uint_as_float(v[t]) * p.scale_log2;
+          v[t] = __float_as_uint(t < nv ? x : -INFINITY);
         }
         float mx;
         {  // tree max
-          float t32[32];
+          float t64[64];
 #pragma unroll
-          for (int t = 0; t < 32; ++t) t32[t] = fmaxf(x[t], x[t + 32]);
+          for (int t = 0; t < 64; ++t) t64[t] = fmaxf(__uint_as_float(v[t]), __uint_as_float(v[t + 64]));
 #pragma unroll
-          for (int w = 16; w >= 1; w >>= 1)
+          for (int w = 32; w >= 1; w >>= 1)
 #pragma unroll
-            for (int t = 0; t < w; ++t) t32[t] = fmaxf(t32[t], t32[t + w]);
-          mx = t32[0];
+            for (int t = 0; t < w; ++t) t64[t] = fmaxf(t64[t], t64[t + w]);
+          mx = t64[0];
         }
         // lazy max: move only when the block max exceeds it by > 8 (log2)
         float m_new = m;
         if (mx > m + 8.f || m == -INFINITY) m_new = fmaxf(mx, m);
         const float alpha = (m == -INFINITY || m_new == m) ? 1.f : ex2_approx(m - m_new);
-        const float mb = m_new == -INFINITY ? 0.f : m_new;  // all-masked rows: exp2(-inf) = 0
-        uint32_t pk[32];
-        float e2[64];
-#pragma unroll
-        for (int t = 0; t < 64; ++t) e2[t] = ex2_approx(x[t] - mb);
-#pragma unroll
-        for (int t = 0; t < 32; ++t) pk[t] = pack2(e2[2 * t], e2[2 * t + 1]);
-        float msum = 0.f;
-        if (p.mass) {  // classifier regions [0, il) U [rs, W) relative to this block
-          const int ie = int(imax64(0, imin64(KB, p.il - k0)));
-          const int rb = int(imax64(0, imin64(KB, p.rs - k0)));
-#pragma unroll
-          for (int t = 0; t < 64; ++t)
-            if (t < ie || t >= rb) msum += e2[t];
-        }
-        float sum;
-        {
-          float t32[32];
-#pragma unroll
-          for (int t = 0; t < 32; ++t) t32[t] = e2[t] + e2[t + 32];
-#pragma unroll
-          for (int w = 16; w >= 1; w >>= 1)
-#pragma unroll
-            for (int t = 0; t < w; ++t) t32[t] += t32[t + w];
-          sum = t32[0];
-        }
-        // PV(i-1) must be done before O is rescaled and P overwritten
-        if (i > 0) {
-          tca::bar_wait(&o_done[wg], (i - 1) & 1);
-          tca::fence_after();
-        }
-        if (threadIdx.x == 0) attn_ts(p, i, 6);
+        // O rescale: PV(i-1) has completed (S(i) was issued after it)
         if (i > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           uint32_t o[32];
 #pragma unroll 1
@@ -411,23 +393,38 @@ __global__ void __launch_bounds__(320, 1)
             tca::ld32(tO + uint32_t(c * 32), o);
 #pragma unroll
             for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
-            tca::st32(tO + uint32_t(c * 32), o);
+            tca::st32_async(tO + uint32_t(c * 32), o);
           }
+          tca::st_wait();
         }
+        const float mb = m_new == -INFINITY ? 0.f : m_new;  // all-masked rows: exp2(-inf) = 0
+        const bool do_mass = p.mass != nullptr;
+        const int ie = do_mass ? int(imax64(0, imin64(KB, p.il - k0))) : 0;
+        const int rb = do_mass ? int(imax64(0, imin64(KB, p.rs - k0))) : KB;
+        float sum = 0.f, msum = 0.f;
+        // exponentiate and pack in place: v[j] <- bf16x2(p(2j), p(2j+1))
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        for (int j = 0; j < 64; ++j) {
+          const float e0 = ex2_approx(__uint_as_float(v[2 * j]) - mb);
+          const float e1 = ex2_approx(__uint_as_float(v[2 * j + 1]) - mb);
+          sum += e0 + e1;
+          if (do_mass) {
+            if (2 * j < ie || 2 * j >= rb) msum += e0;
+            if (2 * j + 1 < ie || 2 * j + 1 >= rb) msum += e1;
+          }
+          v[j] = pack2(e0, e1);
+        }
+        tca::st32_async(tS, v);
+        tca::st32_async(tS + 32u, v + 32);
+        tca::st_wait();
         l = l * alpha + sum;
         mn = mn * alpha + msum;
         m = m_new;
         tca::fence_before();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tca::bar_arrive(&p_ready[wg]);
-        if (threadIdx.x == 0) attn_ts(p, i, 7);
       }
       if (nb > 0) {
-        tca::bar_wait(&o_done[wg], (nb - 1) & 1);
+        tca::bar_wait(&pv_done[wg], (nb - 1) & 1);
         tca::fence_after();
       }
       const int64_t row = q0 + r;
@@ -575,13 +572,11 @@ bool attention_tc_supported(const Ctx& c, const AttnArgs& a) {
          a.rows >= 1;
 }
 
-template <int HD, bool SHARED>
-void run_fa(const Ctx& c, cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk,
+template <int HD>
+void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk,
             const CUtensorMap& tv, const AttnTc& p) {
-  constexpr int STAGES = SHARED ? 3 : 2, NKV = SHARED ? 1 : 2;
-  const size_t smem = 1024 + 2 * size_t(128) * HD * 2 + size_t(STAGES) * NKV * (2 * 64 * HD * 2) +
-                      2 * 128 * 64 * 2 + 256;
-  auto kern = k_attn_fa<HD, SHARED>;
+  const size_t smem = 1024 + 2 * size_t(128) * HD * 2 + (3 + 2) * (size_t(kAttnKB) * HD * 2) + 256;
+  auto kern = k_attn_fa<HD>;
   static bool attr = false;
   if (!attr) {
     KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -591,9 +586,7 @@ void run_fa(const Ctx& c, cudaStream_t s, dim3 grid, const CUtensorMap& tq, cons
   KB_LAUNCH();
 }
 
-int g_attn_dbg = 0;     // tuning knob (krul_debug_attn_bench)
-unsigned long long* g_attn_ts = nullptr;  // tuning: device timestamp buffer
-int g_attn_target = 0;  // tuning knob: key blocks per work item (0 = heuristic)
+int g_attn_target = 0;  // tuning knob (krul_debug_attn_bench): key blocks per work item
 void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                          const AttnArgs& a, DevBuf& scratch) {
   const Cfg& g = c.cfg;
@@ -602,6 +595,7 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   p.H = g.H;
   p.Hkv = g.Hkv;
   p.grp = g.H / g.Hkv;
+  p.hpc = (p.grp >= 2 && p.grp % 2 == 0) ? 2 : 1;  // head pairs only when they share a KV head
   p.rows = a.rows;
   p.pos0 = a.pos0;
   p.kv_total = a.pos0 + a.rows;
@@ -616,18 +610,21 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   p.mass = a.mass;
   p.il = a.mass ? a.il : 0;
   p.rs = a.mass ? a.rs : INT64_MAX;
-  // key blocks per work item: about one SM's fair share of all block-pairs,
-  // at least 8 (splitting costs a partial round trip + the merge)
-  const int pairs = (g.H + 1) / 2;
+  static const int strict = [] {
+    const char* v = std::getenv("KRUL_ATTN_RELAXED");
+    return v && v[0] == '1' ? 0 : 1;
+  }();
+  p.strict_pv = strict;
+  // key blocks per work item: about one SM's fair share of all block-units,
+  // at least 4 (splitting costs a partial round trip + the merge)
+  const int units_y = (g.H + p.hpc - 1) / p.hpc;
   int64_t total = 0;
   p.target = 1 << 30;
   for (int qt = 0; qt < p.n_qtiles; ++qt) total += attn_nblk(p, qt);
   const int64_t sms = c.sm_count > 0 ? c.sm_count : 148;
-  p.target = int(std::max<int64_t>(8, (total * pairs + sms - 1) / sms));
+  p.target = int(std::max<int64_t>(4, (total * units_y + sms - 1) / sms));
   p.target = std::max(p.target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
   if (g_attn_target > 0) p.target = std::max(g_attn_target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
-  p.dbg = g_attn_dbg;
-  p.ts = g_attn_ts;
   int items = 0, max_split = 1;
   for (int qt = 0; qt < p.n_qtiles; ++qt) {
     items += attn_nsplit(p, qt);
@@ -640,15 +637,11 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   const CUtensorMap tq = map2d(a.q, uint64_t(a.rows), uint64_t(g.H) * HD, uint64_t(g.H) * HD, 128);
   const CUtensorMap tk = map2d(c.pool.p, pool_elems / HD, HD, HD, 64);
   const CUtensorMap tv = map2d(c.pool.p, pool_elems / 64, 64, 64, uint32_t(HD));
-  const dim3 grid{unsigned(items), unsigned(pairs), 1u};
-  const bool shared = p.grp >= 2 && (p.grp % 2) == 0;
-  if (HD == 128) {
-    if (shared) run_fa<128, true>(c, s, grid, tq, tk, tv, p);
-    else run_fa<128, false>(c, s, grid, tq, tk, tv, p);
-  } else {
-    if (shared) run_fa<64, true>(c, s, grid, tq, tk, tv, p);
-    else run_fa<64, false>(c, s, grid, tq, tk, tv, p);
-  }
+  const dim3 grid{unsigned(items), unsigned(units_y), 1u};
+  if (HD == 128)
+    run_fa<128>(s, grid, tq, tk, tv, p);
+  else
+    run_fa<64>(s, grid, tq, tk, tv, p);
   if (max_split > 1) {
     const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), unsigned(HD / 32)};
     if (HD == 128)

@@ -992,31 +992,14 @@ int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t row
     a.pos0 = pos0;
     a.out = out.ensure(size_t(rows) * c.cfg.qd() * 2);
     a.part = &part;
-    g_attn_dbg = dbg;
+    (void)dbg;
     g_attn_target = target;
     for (int i = 0; i < 2; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
-    if (std::getenv("KRUL_ATTN_TS")) {  // one launch with per-block timestamps of CTA (0, 0)
-      DevBuf tsb;
-      g_attn_ts = static_cast<unsigned long long*>(tsb.ensure(64 * 8 * 8));
-      KB_CUDA(cudaMemsetAsync(g_attn_ts, 0, 64 * 8 * 8, s));
-      launch_attention_tc(c, s, *conv->v, layer, a, part);
-      std::vector<unsigned long long> h(64 * 8);
-      KB_CUDA(cudaStreamSynchronize(s));
-      KB_CUDA(kb_memcpy_sync(h.data(), g_attn_ts, h.size() * 8, cudaMemcpyDeviceToHost));
-      g_attn_ts = nullptr;
-      const unsigned long long t0 = h[0];
-      for (int i = 0; i < 64 && h[i * 8 + 4]; ++i) {
-        std::fprintf(stderr, "blk %2d:", i);
-        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %7.0f", h[i * 8 + k] ? double(h[i * 8 + k] - t0) : -1.0);
-        std::fprintf(stderr, "\n");
-      }
-    }
     cudaEvent_t e0 = c.event(), e1 = c.event();
     KB_CUDA(cudaEventRecord(e0, s));
     for (int i = 0; i < iters; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
     KB_CUDA(cudaEventRecord(e1, s));
     KB_CUDA(cudaEventSynchronize(e1));
-    g_attn_dbg = 0;
     g_attn_target = 0;
     float ms = 0;
     KB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
