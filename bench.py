@@ -123,6 +123,9 @@ def dist_setup():
         # test on a 1-GPU box; NCCL refuses shared devices, so gloo then)
         if os.environ.get("KRUL_BENCH_DEVICE") is not None:
             local = int(os.environ["KRUL_BENCH_DEVICE"])
+        else:
+            from paper_2507_08045_b200 import shard
+            shard.bind_to_gpu_numa(local)  # host snapshots on the GPU's NUMA node
         torch.cuda.set_device(local)
         dist.init_process_group(os.environ.get("KRUL_DIST_BACKEND", "nccl"))
         return rank, local, world, dist

@@ -43,6 +43,15 @@ def test_lpt_partition_properties():
         shard.lpt_assign([1], 0)
 
 
+def test_numa_binding_is_safe_without_a_gpu():
+    # NVML absent / no device: returns None and leaves the affinity alone
+    before = os.sched_getaffinity(0)
+    r = shard.bind_to_gpu_numa(0)
+    assert r is None or (r and set(r) <= set(range(os.cpu_count())))
+    if r is None:
+        assert os.sched_getaffinity(0) == before
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
