@@ -472,3 +472,62 @@ def test_restore_rejects_mismatch(K, oracle):  # test_scheduler.cpp:402-430
         ctx.execute_restore(c2, hist, snap)
     with pytest.raises(K.ConfigError):
         ctx.prefill(c2, np.array([0, 7], np.int32))
+
+
+# ----------------------------------------------------------------- full-size properties
+
+@pytest.mark.parametrize("pairs,mode", [([], 1), ([(1, 2, 0.0)], 0)])
+def test_full_size_restore_properties(K, pairs, mode, monkeypatch):
+    """Llama-3-8B layer shape (d=4096, 32/8 heads, hd=128, SwiGLU 14336,
+    theta 5e5; 4 layers to bound the run) with an 8K history -- size-
+    independent properties instead of an oracle run (the CPU restatement
+    needs minutes per layer at this size):
+      * loaded spans [p_l, L) are bit-identical to the previous turn's KV
+        (keep-deeper, no pairs), or equal to the mean merge 0.5*(a+b) of the
+        pair members (kvstore.cpp:302-307) rounded to bf16;
+      * recomputed spans [0, p_l) match the previous turn's prefill (rel
+        Frobenius <= 1e-2; different GEMM tilings / split-K order);
+      * the restored conversation's next-token logits match a plain prefill
+        of history + new input (rel <= 3e-2), repeated replays bit-stable."""
+    L, n = 8192, 128
+    monkeypatch.setenv("KRUL_KV_POOL_CONVS", "3")
+    cfg = K.ModelConfig(n_layers=4, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096,
+                        vocab_size=32000, ffn_mult=3.5, ffn_kind=1, rope_theta=500000.0, seed=3,
+                        dtype=K.KRUL_BF16, max_tokens=L + n + 64)
+    ctx = K.Context(cfg, 0)
+    ctx.init_weights(3)
+    rng = np.random.default_rng(5)
+    hist = rng.integers(0, cfg.vocab_size, L, dtype=np.int32)
+    new = rng.integers(0, cfg.vocab_size, n, dtype=np.int32)
+    prev = ctx.conversation(L + n + 64)
+    ctx.prefill(prev, hist)
+    ref = [prev.kv(l, 0, L) for l in range(4)]
+    plan = K.build_plan(L, 4, 0.1, pairs)
+    snap = K.KVSnapshot.compress(ctx, prev, pairs, plan, L, mode)
+    conv = ctx.conversation(L + n + 64)
+    outs = [ctx.restore_and_prefill(conv, hist, snap, new)[0] for _ in range(3)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    bf = lambda x: (x.astype(np.float32).view(np.uint32) + 0x7FFF +  # noqa: E731
+                    ((x.astype(np.float32).view(np.uint32) >> 16) & 1)) >> 16 << 16
+    for l in range(4):
+        p = int(plan[l])
+        k, v = conv.kv(l, 0, L)
+        rk, rv = ref[l]
+        owners = [pp for pp in pairs if l in pp[:2]]
+        if owners:  # pair member: the stored blob is the mean over the shallow member's span
+            a, b = owners[0][:2]
+            ka, va = ref[a]
+            kb, vb = ref[b]
+            s = int(plan[a])
+            want_k = bf(0.5 * (ka[:, s:] + kb[:, s:])).astype(np.uint32).view(np.float32)
+            want_v = bf(0.5 * (va[:, s:] + vb[:, s:])).astype(np.uint32).view(np.float32)
+            assert np.array_equal(k[:, max(p, s):], want_k[:, max(p, s) - s:])
+            assert np.array_equal(v[:, max(p, s):], want_v[:, max(p, s) - s:])
+        else:
+            assert np.array_equal(k[:, p:], rk[:, p:]) and np.array_equal(v[:, p:], rv[:, p:])
+        if p:
+            assert rel_fro(k[:, :p], rk[:, :p]) < 1e-2 and rel_fro(v[:, :p], rv[:, :p]) < 1e-2
+    full = ctx.conversation(L + n + 64)
+    want = ctx.prefill(full, np.concatenate([hist, new]))
+    if not pairs:
+        assert rel_fro(outs[0], want) < 3e-2
