@@ -268,7 +268,7 @@ def run_b200(args, rank, local, world, dist):
     coarse = [round(0.02 * k, 4) for k in range(0, 21)]
     r0, _ = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, coarse)
     fine = sorted({min(1.0, max(0.0, round(r0 + 0.004 * k, 4))) for k in range(-5, 6)})
-    r_c, ttft_fine = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, fine)
+    r_c, ttft_fine = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, fine, reps=7)
     r_bal, _, _ = ctx.calibrate_rc_measured(prev, conv, hist, pairs, fine)
     plan = K.build_plan(L, cfg.n_layers, r_c, pairs)
     snap = K.KVSnapshot.compress(ctx, prev, pairs, plan, L, K.MERGE_MEAN)

@@ -324,9 +324,52 @@ __global__ void k_logits(const float* h, const T* wT, int d, int V, float* out) 
   acc = warp_sum(acc);
   if (lane == 0) out[v] = acc;
 }
+// bf16 fast path (d % 256 == 0, d <= 8192): the last hidden row is staged
+// in shared memory once per block; each warp owns one vocabulary row and
+// issues all its 16-byte weight loads before the FMAs, so the unembedding
+// (V x d bf16 -- 1 GB for Llama-3) streams at HBM rate. This GEMV is the
+// last kernel before the first token.
+template <int NV>  // 16-byte vectors per lane: d = 256 * NV
+__global__ void __launch_bounds__(256) k_logits_vec(const float* __restrict__ h,
+                                                    const bf16* __restrict__ wT, int V,
+                                                    float* __restrict__ out) {
+  constexpr int D = 256 * NV;
+  __shared__ float hs[D];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) hs[i] = h[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int v = blockIdx.x * 8 + warp; v < V; v += gridDim.x * 8) {
+    const uint4* w = reinterpret_cast<const uint4*>(wT + int64_t(v) * D);
+    uint4 x[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) x[j] = __ldg(w + lane + 32 * j);
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int k0 = (lane + 32 * j) * 8;
+      const uint32_t u[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[q]));
+        acc += hs[k0 + 2 * q] * f.x + hs[k0 + 2 * q + 1] * f.y;
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) out[v] = acc;
+  }
+}
 void launch_logits(const Ctx& c, cudaStream_t s, const float* h_last, float* logits) {
   const int V = c.cfg.V;
   const unsigned blocks = unsigned((V + 7) / 8);
+  if (c.cfg.dtype == KRUL_BF16 && c.cfg.d % 256 == 0 && (c.cfg.d == 4096 || c.cfg.d == 8192)) {
+    const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count > 0 ? c.sm_count : 148) * 8));
+    if (c.cfg.d == 4096)
+      k_logits_vec<16><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
+    else
+      k_logits_vec<32><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
+    KB_LAUNCH();
+    return;
+  }
   if (c.cfg.dtype == KRUL_BF16)
     k_logits<<<blocks, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, c.cfg.d, V, logits);
   else
