@@ -184,14 +184,14 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
 //     are written back as bf16 into the first 64 columns of the same TMEM
 //     region (P never touches shared memory), lazy O rescale (the running
 //     max moves only when a row max exceeds it by > 8 in log2), MUFU ex2.
-//   warp 8 : TMA producer.
+//   warp 8 : K TMA producer, warp 10 : V TMA producer.
 //   warp 9 : MMA issuer, ping-pong over the heads: PV_A(i) (TS-MMA, A = P
 //     from TMEM) then S_A(i+1) while head B is exponentiated, then PV_B(i),
 //     S_B(i+1) while head A is -- the tensor pipe and the softmax warps
 //     overlap across the two heads.
 // TMEM (512 columns): S/P_A [0,128), S/P_B [128,256), O_A [256,..), O_B [384,..).
 template <int HD>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     k_attn_fa(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnTc p) {
   constexpr int KB = kAttnKB;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(320, 1)
         const int kb = b0 + i;
         const int pa = p.pt[min(2 * kb, p.max_pages - 1)];
         const int pb = p.pt[min(2 * kb + 1, p.max_pages - 1)];
-        const int ks = i % KST, vs = i % VST;
+        const int ks = i % KST;
         tca::bar_wait(&k_empty[ks], ((i / KST) & 1) ^ 1);
         unsigned char* kd = sK + ks * K_BYTES;
         tca::bar_expect(&k_full[ks], K_BYTES);
@@ -282,6 +282,19 @@ __global__ void __launch_bounds__(320, 1)
           tca::tma2d(kd + j * (KB * 128), &tmK, &k_full[ks], 64 * j, pa * p.k_rows_pp + g * 64);
           tca::tma2d(kd + j * (KB * 128) + 64 * 128, &tmK, &k_full[ks], 64 * j, pb * p.k_rows_pp + g * 64);
         }
+      }
+      (void)voff;
+    }
+  } else if (warp == 10) {
+    // V producer: its own thread so a V slot still held by PV(i-2) never
+    // holds back the K prefetch that the next QK^T waits for
+    if (lane == 0 && nb > 0) {
+      const int voff = p.Hkv * HD + g * HD;
+      for (int i = 0; i < nb; ++i) {
+        const int kb = b0 + i;
+        const int pa = p.pt[min(2 * kb, p.max_pages - 1)];
+        const int pb = p.pt[min(2 * kb + 1, p.max_pages - 1)];
+        const int vs = i % VST;
         tca::bar_wait(&v_empty[vs], ((i / VST) & 1) ^ 1);
         unsigned char* vd = sV + vs * V_BYTES;
         tca::bar_expect(&v_full[vs], V_BYTES);
@@ -582,7 +595,7 @@ void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap&
     KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  kern<<<grid, 320, smem, s>>>(tq, tk, tv, p);
+  kern<<<grid, 352, smem, s>>>(tq, tk, tv, p);
   KB_LAUNCH();
 }
 
