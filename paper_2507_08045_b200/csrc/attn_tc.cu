@@ -149,6 +149,7 @@ struct AttnTc {
   double* mass;    // [H][rows] region mass, may be null
   int64_t il, rs;
   int strict_pv;   // wait for PV(i) before S(i+1) (default; KRUL_ATTN_RELAXED=1 skips it)
+  int dbg;         // tuning only: 1 = softmax skips its math, 3 = MMA thread issues no MMAs
 };
 
 constexpr int kAttnKB = 128;  // keys per block = two 64-token pages
@@ -310,6 +311,10 @@ __global__ void __launch_bounds__(352, 1)
                                (uint32_t(128 >> 4) << 24);
       const int nh = hasB ? 2 : 1;
       auto issue_s = [&](int h, int i) {  // S_h(i) = Q_h K_i^T -> TMEM [h*128, +128)
+        if (p.dbg == 3) {
+          tca::commit(&s_full[h]);
+          return;
+        }
         const unsigned char* kt = sK + (i % KST) * K_BYTES;
         const uint32_t dS = tmem + uint32_t(h * 128);
 #pragma unroll
@@ -321,6 +326,10 @@ __global__ void __launch_bounds__(352, 1)
         tca::commit(&s_full[h]);
       };
       auto issue_pv = [&](int h, int i) {  // O_h += P_h(i) V_i, P from TMEM
+        if (p.dbg == 3) {
+          tca::commit(&pv_done[h]);
+          return;
+        }
         const unsigned char* vt = sV + (i % VST) * V_BYTES;
         const uint32_t dO = tmem + 256 + uint32_t(h * 128);
         const uint32_t aP = tmem + uint32_t(h * 128);
@@ -376,6 +385,14 @@ __global__ void __launch_bounds__(352, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tca::ld32_async(tS + uint32_t(c * 32), v + 32 * c);
         tca::ld_wait();
+        if (p.dbg == 1) {  // tuning: P = S bits, no softmax arithmetic
+          tca::st32_async(tS, v);
+          tca::st32_async(tS + 32u, v + 32);
+          tca::st_wait();
+          tca::fence_before();
+          tca::bar_arrive(&p_ready[wg]);
+          continue;
+        }
         // visible keys of this row in the block: [k0, k0 + nv)
         const int nv = int(imax64(0, imin64(KB, min(qpos + 1, p.kv_total) - k0)));
 #pragma unroll
@@ -600,6 +617,7 @@ void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap&
 }
 
 int g_attn_target = 0;  // tuning knob (krul_debug_attn_bench): key blocks per work item
+int g_attn_dbg = 0;     // tuning knob (krul_debug_attn_bench): see AttnTc::dbg
 void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                          const AttnArgs& a, DevBuf& scratch) {
   const Cfg& g = c.cfg;
@@ -628,6 +646,7 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
     return v && v[0] == '1' ? 0 : 1;
   }();
   p.strict_pv = strict;
+  p.dbg = g_attn_dbg;
   // key blocks per work item: about one SM's fair share of all block-units,
   // at least 4 (splitting costs a partial round trip + the merge)
   const int units_y = (g.H + p.hpc - 1) / p.hpc;

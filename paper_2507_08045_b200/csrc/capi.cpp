@@ -992,15 +992,28 @@ int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t row
     a.pos0 = pos0;
     a.out = out.ensure(size_t(rows) * c.cfg.qd() * 2);
     a.part = &part;
-    (void)dbg;
     g_attn_target = target;
+    g_attn_dbg = dbg;
     for (int i = 0; i < 2; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
+    // the launches are captured into a graph and replayed, so the timing
+    // is device time (host tensor-map encoding would otherwise dominate)
+    KB_CUDA(cudaStreamSynchronize(s));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    KB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    for (int i = 0; i < iters; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
+    KB_CUDA(cudaStreamEndCapture(s, &graph));
+    KB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    KB_CUDA(cudaGraphLaunch(exec, s));  // warm
     cudaEvent_t e0 = c.event(), e1 = c.event();
     KB_CUDA(cudaEventRecord(e0, s));
-    for (int i = 0; i < iters; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
+    KB_CUDA(cudaGraphLaunch(exec, s));
     KB_CUDA(cudaEventRecord(e1, s));
     KB_CUDA(cudaEventSynchronize(e1));
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
     g_attn_target = 0;
+    g_attn_dbg = 0;
     float ms = 0;
     KB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     *ms_per_iter = ms / float(iters);
