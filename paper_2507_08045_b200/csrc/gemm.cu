@@ -1228,7 +1228,16 @@ void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, co
   const bool tc_ok = gemm_uses_tc(c, A, lda, B, ldb) && K >= 1;
   if (e.kind == Epi::QKV && !tc_ok) fail(KRUL_E_CUDA, "fused QKV epilogue requires the tcgen05 path");
   if (tc_ok) {
-    const GemmPlan gp = plan_gemm(M, N, K, c.sm_count > 0 ? c.sm_count : 148, true);
+    // SM budget per stream (experiment knob KRUL_NEW_SMS: the new-input
+    // prefill stream's persistent GEMMs use that many SMs, the recompute
+    // stream's the rest, so the two never wait for each other's CTAs)
+    static const int new_sms = [] {
+      const char* v = std::getenv("KRUL_NEW_SMS");
+      return v ? std::atoi(v) : 0;
+    }();
+    int sms = c.sm_count > 0 ? c.sm_count : 148;
+    if (new_sms > 0 && new_sms < sms) sms = (s == c.s_new) ? new_sms : sms - new_sms;
+    const GemmPlan gp = plan_gemm(M, N, K, sms, true);
     float* part = nullptr;
     if (gp.splits > 1) {
       DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;
