@@ -41,6 +41,10 @@ try:
 except Exception:
     pass
 
+# dram__bytes_read.sum + dram__bytes_write.sum of one FFN1 pair-GEMM launch
+# (profiles/r01c/SUMMARY.md): 251.06 MB + 25.40 MB
+NCU_FFN1_DRAM_BYTES = 276_462_080
+
 METRIC = ("restoration TTFT p50 (ms) @8K history; conversations restored/sec at 1/2/4/8 GPU")
 
 CONFIGS = {
@@ -359,13 +363,19 @@ def run_b200(args, rank, local, world, dist):
         "storage": {"full_bytes": full_b, "stored_bytes": stored_b},
         "roofline": {"bound": "tensor", "kernel": "k_gemm_tc / k_gemm_tc2, M > 128 (recompute GEMMs, K6)",
                      "achieved": round(achieved_tf, 2), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / peak, 4), "traffic": None,
+                     "frac": round(achieved_tf / peak, 4),
+                     # DRAM bytes of one launch of the dominant GEMM (FFN1 pair GEMM of
+                     # recompute layer 0, M=1078 N=28672 K=4096) from the committed
+                     # ncu --set full capture vs its algorithmic bytes (A + B + C)
+                     "traffic": NCU_FFN1_DRAM_BYTES,
+                     "traffic_algorithmic": 1078 * 4096 * 2 + 28672 * 4096 * 2 + 1078 * 14336 * 2,
+                     "traffic_source": "profiles/r01c/SUMMARY.md (ncu --set full, one launch)",
                      "launches": g_n, "avg_launch_us": round(1e3 * g_ms / max(g_n, 1), 2),
                      "measured": "CUDA events around each launch, instrumented pass of the same "
                                  "steps (warm-up + steps) right after the timed region",
                      "algorithmic": "2*M*N*K per GEMM launch (M > 128), summed over the steps",
                      "peak_source": peak_src,
-                     "traffic_note": "dram bytes per launch: see profiles/ (ncu --set full)"},
+                     },
         "rooflines": {
             "attention": {"bound": "tensor", "kernel": "k_attn_fa (+ split-KV merge)",
                           "achieved": round(a_fl / (a_ms * 1e-3) / 1e12, 2) if a_ms else None,
