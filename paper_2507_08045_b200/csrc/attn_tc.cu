@@ -149,10 +149,11 @@ struct AttnTc {
   double* mass;    // [H][rows] region mass, may be null
   int64_t il, rs;
   int strict_pv;   // wait for PV(i) before S(i+1) (default; KRUL_ATTN_RELAXED=1 skips it)
-  int dbg;         // tuning only: 1 = softmax skips its math, 3 = MMA thread issues no MMAs
+  int dbg;         // tuning only: 1 = no softmax math, 3 = no MMAs, 4 = neither, 5 = barriers + TMA only
 };
 
 constexpr int kAttnKB = 128;  // keys per block = two 64-token pages
+constexpr int kPgCache = 96;  // key blocks whose page ids are cached in smem
 
 // number of key blocks q tile qt attends to, and its work-item count
 __host__ __device__ __forceinline__ int attn_nblk(const AttnTc& p, int qt) {
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* p_ready = s_full + 2;           // [2 heads]
   uint64_t* pv_done = p_ready + 2;          // [2 heads]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  int* pg_s = reinterpret_cast<int*>(tslot + 4);  // [2 * kPgCache] page ids of this item
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // work item -> (q tile, split); heavy (late) q tiles first
@@ -258,10 +260,18 @@ __global__ void __launch_bounds__(352, 1)
         tca::su32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // page ids of the item's key blocks, fetched once by all threads (a
+  // dependent global load per block in the producer threads serialised the
+  // K/V stream)
+  for (int i = threadIdx.x; i < 2 * min(nb, kPgCache); i += blockDim.x)
+    pg_s[i] = p.pt[min(2 * b0 + i, p.max_pages - 1)];
   tca::fence_before();
   __syncthreads();
   tca::fence_after();
   const uint32_t tmem = *tslot;
+  auto page_of = [&](int i, int half) {
+    return i < kPgCache ? pg_s[2 * i + half] : p.pt[min(2 * (b0 + i) + half, p.max_pages - 1)];
+  };
 
   if (warp == 8) {
     if (lane == 0 && nb > 0) {  // TMA producer
@@ -272,9 +282,7 @@ __global__ void __launch_bounds__(352, 1)
       }
       const int voff = p.Hkv * HD + g * HD;
       for (int i = 0; i < nb; ++i) {
-        const int kb = b0 + i;
-        const int pa = p.pt[min(2 * kb, p.max_pages - 1)];
-        const int pb = p.pt[min(2 * kb + 1, p.max_pages - 1)];
+        const int pa = page_of(i, 0), pb = page_of(i, 1);
         const int ks = i % KST;
         tca::bar_wait(&k_empty[ks], ((i / KST) & 1) ^ 1);
         unsigned char* kd = sK + ks * K_BYTES;
@@ -292,9 +300,7 @@ __global__ void __launch_bounds__(352, 1)
     if (lane == 0 && nb > 0) {
       const int voff = p.Hkv * HD + g * HD;
       for (int i = 0; i < nb; ++i) {
-        const int kb = b0 + i;
-        const int pa = p.pt[min(2 * kb, p.max_pages - 1)];
-        const int pb = p.pt[min(2 * kb + 1, p.max_pages - 1)];
+        const int pa = page_of(i, 0), pb = page_of(i, 1);
         const int vs = i % VST;
         tca::bar_wait(&v_empty[vs], ((i / VST) & 1) ^ 1);
         unsigned char* vd = sV + vs * V_BYTES;
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(352, 1)
                                (uint32_t(128 >> 4) << 24);
       const int nh = hasB ? 2 : 1;
       auto issue_s = [&](int h, int i) {  // S_h(i) = Q_h K_i^T -> TMEM [h*128, +128)
-        if (p.dbg == 3) {
+        if (p.dbg >= 3) {
           tca::commit(&s_full[h]);
           return;
         }
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(352, 1)
         tca::commit(&s_full[h]);
       };
       auto issue_pv = [&](int h, int i) {  // O_h += P_h(i) V_i, P from TMEM
-        if (p.dbg == 3) {
+        if (p.dbg >= 3) {
           tca::commit(&pv_done[h]);
           return;
         }
@@ -381,11 +387,16 @@ __global__ void __launch_bounds__(352, 1)
         const int64_t k0 = int64_t(b0 + i) * KB;
         tca::bar_wait(&s_full[wg], i & 1);
         tca::fence_after();
+        if (p.dbg == 5) {  // tuning: barrier / TMA chain only
+          tca::fence_before();
+          tca::bar_arrive(&p_ready[wg]);
+          continue;
+        }
         uint32_t v[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tca::ld32_async(tS + uint32_t(c * 32), v + 32 * c);
         tca::ld_wait();
-        if (p.dbg == 1) {  // tuning: P = S bits, no softmax arithmetic
+        if (p.dbg == 1 || p.dbg == 4) {  // tuning: P = S bits, no softmax arithmetic
           tca::st32_async(tS, v);
           tca::st32_async(tS + 32u, v + 32);
           tca::st_wait();
@@ -605,7 +616,8 @@ bool attention_tc_supported(const Ctx& c, const AttnArgs& a) {
 template <int HD>
 void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk,
             const CUtensorMap& tv, const AttnTc& p) {
-  const size_t smem = 1024 + 2 * size_t(128) * HD * 2 + (3 + 2) * (size_t(kAttnKB) * HD * 2) + 256;
+  const size_t smem = 1024 + 2 * size_t(128) * HD * 2 + (3 + 2) * (size_t(kAttnKB) * HD * 2) + 256 +
+                      2 * kPgCache * sizeof(int);
   auto kern = k_attn_fa<HD>;
   static bool attr = false;
   if (!attr) {
