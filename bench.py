@@ -591,6 +591,9 @@ def main():
     ap.add_argument("--convs", type=int, default=0,
                     help="batch configs: conversations per rank (0 = the whole LPT shard)")
     args = ap.parse_args()
+    if os.environ.get("KRUL_BENCH_WATCHDOG"):  # debugging aid: dump the stack if a phase hangs
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["KRUL_BENCH_WATCHDOG"]), exit=True)
     # the CPU legs (reference arm, cpu_baseline) use every host thread, also
     # under torchrun (which exports OMP_NUM_THREADS=1); the oracle's OpenMP
     # runtime reads this when its library loads

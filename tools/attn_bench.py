@@ -25,8 +25,8 @@ def main():
     for rows, pos0, name in ((128, 8192, "new-prefill 128x8320"), (1024, 0, "recompute 1024 causal")):
         vis = rows * pos0 + rows * (rows + 1) / 2
         fl = 4 * 128 * 32 * vis
-        for dbg in (0, 1, 3, 4, 5):
-            for target in (0, 32):
+        for dbg in (0,):
+            for target in (0, 8, 16, 32):
                 ms = C.c_float()
                 rc = lib.krul_debug_attn_bench(ctx.h, conv.h, 0, C.c_int64(rows), C.c_int64(pos0),
                                                dbg, target, 20, C.byref(ms))
