@@ -286,6 +286,10 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps,
 /* C[M,N] = A[M,K] B[N,K]^T through the engine GEMM (inputs rounded to the
  * ctx dtype; tcgen05 path for bf16). epi: 0 = f32 store, 2 = resid (C +=),
  * 3 = tanh(acc + bias), 4 = swiglu over column pairs (C is [M, N/2]). */
+/* Restore scheduling: 1 (default) = new-input prefill concurrent with the
+ * recompute on its own stream; 0 = serialised behind it. */
+int krul_set_concurrency(krul_ctx* ctx, int two_stream);
+
 /* ---- measurement support (not on the reference's interface) ----------
  * krul_launch_count: number of kernels this library has launched (process
  * wide). krul_ktime_*: per-launch CUDA-event timing of instrumented kernel
@@ -296,6 +300,9 @@ int krul_launch_count(uint64_t* n);
 int krul_ktime_enable(krul_ctx* ctx, int on);
 int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, double* flops,
                     double* bytes);
+/* sum over the timed launches of a class of max(flops / peak, bytes / peak) */
+int krul_ktime_roofline(krul_ctx* ctx, int tag, double peak_tflops, double peak_gbs,
+                        double* ideal_ms);
 
 /* Device time of one decode fold (K1) on the last captured decode rows,
  * `iters` back to back into a scratch accumulator (estimator state untouched). */

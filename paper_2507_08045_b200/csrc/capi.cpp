@@ -1059,4 +1059,35 @@ int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* by
   });
 }
 
+
+// Restore scheduling mode: 1 (default) runs the new-input prefill on its own
+// stream, concurrent with the recompute; 0 serialises it behind the
+// recompute (kernel-efficiency measurements without SM sharing).
+int krul_set_concurrency(krul_ctx* ctx, int two_stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->two_stream = two_stream != 0;
+  });
+}
+
+
+// Roofline-normalised time of the timed launches of a kernel class: the sum
+// over launches of max(flops / peak_flops, bytes / peak_bytes) -- what the
+// launches would take at the binding roof (tensor or HBM) of each shape.
+int krul_ktime_roofline(krul_ctx* ctx, int tag, double peak_tflops, double peak_gbs, double* ideal_ms) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(ideal_ms, "ideal_ms");
+    Ctx& c = *ctx->c;
+    double t = 0;
+    for (const auto& r : c.kt.recs) {
+      if (r.tag != tag) continue;
+      const double tf = peak_tflops > 0 ? r.flops / (peak_tflops * 1e12) : 0.0;
+      const double tb = peak_gbs > 0 ? r.bytes / (peak_gbs * 1e9) : 0.0;
+      t += 1e3 * std::max(tf, tb);
+    }
+    *ideal_ms = t;
+  });
+}
+
 }  // extern "C"

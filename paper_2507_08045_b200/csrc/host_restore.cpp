@@ -221,10 +221,11 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   // ---- new-input prefill (K7) on its own stream, layer l behind
   // computed[l] and loaded[l], so it tracks the load events while the
   // recompute runs (KRUL_TWO_STREAM=0: same stream, after the recompute).
-  static const bool two_stream = [] {
+  static const bool two_stream_env = [] {
     const char* v = std::getenv("KRUL_TWO_STREAM");
     return !(v && v[0] == '0');
   }();
+  const bool two_stream = two_stream_env && c.two_stream;
   if (tp_new) {
     cudaStream_t sn = two_stream ? c.s_new : sc;
     if (two_stream) KB_CUDA(cudaStreamWaitEvent(sn, tok_ready, 0));
@@ -284,7 +285,8 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   auto& G = c.rg;
   const bool same = G.snap_serial == snap.serial && G.conv == &conv && G.L == L && G.n_new == nn &&
                     G.kt_on == c.kt.on && G.logits == (lp != nullptr) &&
-                    G.capture_probs == c.capture_probs && G.buf_gen == g_buf_gen.load();
+                    G.capture_probs == c.capture_probs && G.buf_gen == g_buf_gen.load() &&
+                    G.two_stream == c.two_stream;
   if (!same) {
     c.drop_graph();
     G.snap_serial = snap.serial;
@@ -294,6 +296,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     G.kt_on = c.kt.on;
     G.logits = lp != nullptr;
     G.capture_probs = c.capture_probs;
+    G.two_stream = c.two_stream;
     G.ev.resize(size_t(5 + 3 * g.N));
     for (auto& m : G.ev) {
       KB_CUDA(cudaEventCreateWithFlags(&m.dep, cudaEventDisableTiming));

@@ -216,6 +216,7 @@ struct Ctx {
     bool kt_on = false, logits = false;
     int capture_probs = -1;
     uint64_t buf_gen = 0;
+    bool two_stream = true;
     int seen = 0;  // eager runs with this key (capture on the second)
     cudaGraphExec_t exec = nullptr;
     uint64_t launches = 0;
@@ -223,6 +224,7 @@ struct Ctx {
     double h2d = 0, expand_bytes = 0;
   } rg;
   bool use_graphs = true;
+  bool two_stream = true;  // new-input prefill concurrent with the recompute (krul_set_concurrency)
   std::vector<double> tl_compute, tl_load, tl_new;
   double tl_h2d_ms = 0;
   std::vector<cudaEvent_t> ev_pool;

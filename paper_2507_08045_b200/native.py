@@ -305,6 +305,11 @@ class Context:
                                             mode, reps, C.byref(r), _p(tt)))
         return r.value, tt
 
+    def set_concurrency(self, two_stream: bool):
+        """Restore DAG mode: new-input prefill concurrent with the recompute (default)
+        or serialised behind it."""
+        _check(lib().krul_set_concurrency(self.h, int(bool(two_stream))))
+
     def ktime_enable(self, on: bool):
         _check(lib().krul_ktime_enable(self.h, int(bool(on))))
 
@@ -313,6 +318,13 @@ class Context:
         n, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
         _check(lib().krul_ktime_read(self.h, tag, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
         return n.value, ms.value, fl.value, by.value
+
+    def ktime_roofline(self, tag: int, peak_tflops: float, peak_gbs: float) -> float:
+        """ms the timed launches of a class would take at their binding roof."""
+        v = C.c_double()
+        _check(lib().krul_ktime_roofline(self.h, tag, C.c_double(peak_tflops), C.c_double(peak_gbs),
+                                         C.byref(v)))
+        return v.value
 
     def measure_rates(self, scratch):
         b, f = C.c_double(), C.c_double()
