@@ -357,6 +357,7 @@ def run_b200(args, rank, local, world, dist):
     pol = policies_leg(K, ctx, prev, conv, cfg, hist, new, L, r_c, pairs) if (
         rank == 0 and not args.no_policies) else None
     est = estimator_leg(K, ctx, conv, cfg, spec) if rank == 0 else None
+    ctr = container_leg(K, ctx, snap) if rank == 0 else None
     out = {
         "metric": METRIC,
         "value": round(conv_s, 4),
@@ -434,6 +435,7 @@ def run_b200(args, rank, local, world, dist):
                 "note": "algorithmic pyramid flops / recompute-stream makespan (shares SMs with the "
                         "new-input prefill and expand streams)"},
             **({"estimator_decode_fold": est["fold"], "selector": est["select"]} if est else {}),
+            **({"container": ctr} if ctr else {}),
         },
         "e2e": {"value": round(e2e_conv_s, 4), "unit": "conversations/s",
                 "ttft_p50_ms": round(float(np.median(walls)), 4),
@@ -532,6 +534,35 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
 # ---------------------------------------------------------------- CPU legs
 
 _ORACLE_MODELS = {}
+
+
+def container_leg(K, ctx, snap, reps=3):
+    """KRUL v1 container (kvstore.cpp:360-511) of this workload's
+    snapshot, in host memory: save (bf16 store -> f32 payload + nlohmann-exact
+    metadata + crc32) and load (crc32 + checks + f32 -> bf16 into a fresh
+    pinned store), all host threads. Reference: one-thread memcpy of the same
+    bytes."""
+    n = snap.save_size()
+    buf = np.empty(n, np.uint8)
+    ts, tl = [], []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        snap.save_to(buf)
+        ts.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        back = K.KVSnapshot.load(buf, ctx)
+        tl.append(time.perf_counter() - t0)
+        del back
+    dst = np.empty_like(buf)
+    t0 = time.perf_counter()
+    np.copyto(dst, buf)
+    tm = time.perf_counter() - t0
+    ok = K.KVSnapshot.load(buf, ctx).save_size() == n
+    return {"bytes": int(n), "save_ms": round(1e3 * min(ts), 2), "load_ms": round(1e3 * min(tl), 2),
+            "save_gbs": round(n / min(ts) / 1e9, 2), "load_gbs": round(n / min(tl) / 1e9, 2),
+            "memcpy_1thread_gbs": round(n / tm / 1e9, 2), "threads": len(os.sched_getaffinity(0)),
+            "round_trip_ok": bool(ok),
+            "note": "load = crc32 + checks + f32->bf16 into fresh host memory (threads first-touch) + cudaHostRegister; save = bf16->f32 + metadata + crc32"}
 
 
 def cpu_baseline(args, spec, plan, pairs, budget_s=20.0):

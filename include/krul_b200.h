@@ -235,6 +235,53 @@ int krul_snapshot_set_plan(krul_snapshot* snap, const int64_t* recompute_len);
 int krul_expand(krul_snapshot* snap, int layer, float* k, float* v,
                 int64_t* start, int64_t* end);
 
+/* ---- KRUL v1 container (kvstore.hpp:88-98; kvstore.cpp:360-511) ---------
+ * "KRUL" | u32 version | u64 config_hash | u64 metadata_len | metadata
+ * (key-sorted compact JSON, byte-identical to the reference's nlohmann dump)
+ * | u32 blob_count | blobs (owners, span, f32 payload keys then values,
+ * [heads][rows][head_dim]) | u32 crc32 of all preceding bytes.
+ * "n_heads" in the container is the number of KV heads (= heads in the
+ * reference's MHA model). The bf16 store widens exactly to f32 on save and
+ * rounds to nearest-even on load; an f32 store round-trips bit-exactly. */
+/* The container metadata beside the store (kvstore.hpp:46-59). */
+typedef struct {
+  const char* conversation_id; /* UTF-8, NUL-terminated */
+  int exhausted_before_quota;  /* CompressionStrategy::exhausted_before_quota */
+  const int32_t* ir_layers;    /* LayerClassReport (analysis.hpp:23-27) */
+  int n_ir_layers;
+  const int32_t* non_ir_layers;
+  int n_non_ir_layers;
+  const double* avg_weight_sum;
+  int n_avg_weight_sum;
+} krul_snapshot_meta;
+int krul_snapshot_set_meta(krul_snapshot* snap, const krul_snapshot_meta* meta);
+/* Pointers stay valid until the snapshot is destroyed or its meta is reset. */
+int krul_snapshot_get_meta(krul_snapshot* snap, krul_snapshot_meta* meta);
+/* Header fields of a snapshot (n_heads = KV heads). Any pointer may be NULL. */
+int krul_snapshot_header(krul_snapshot* snap, uint64_t* config_hash, int* n_layers,
+                         int* n_heads, int* head_dim, int64_t* history_len,
+                         int* mode, int* n_pairs);
+/* strategy.pairs in selection order (n_pairs from krul_snapshot_header). */
+int krul_snapshot_pairs(krul_snapshot* snap, krul_pair* out);
+/* kvstore::save (kvstore.cpp:360-392) into buf. *len = container bytes; buf
+ * NULL = size query; cap smaller than the container = KRUL_E_ARG. */
+int krul_snapshot_save(krul_snapshot* snap, void* buf, uint64_t cap, uint64_t* len);
+int krul_snapshot_save_file(krul_snapshot* snap, const char* path);
+/* kvstore::load (kvstore.cpp:394-511): the same checks in the same order.
+ * ctx non-NULL: the store is pinned host memory in the ctx dtype, ready for
+ * krul_restore. ctx NULL: host-only f32 snapshot (inspect / expand / save;
+ * krul_restore rejects it). expected_config_hash may be NULL. On
+ * KRUL_E_SNAPSHOT_LOAD the failing field ("magic", "checksum", "version",
+ * "config", "metadata", "plan", "blob", "coverage") is copied to field. */
+int krul_snapshot_load(krul_ctx* ctx, const void* buf, uint64_t len,
+                       const uint64_t* expected_config_hash, krul_snapshot** out,
+                       char* field, int field_cap);
+int krul_snapshot_load_file(krul_ctx* ctx, const char* path,
+                            const uint64_t* expected_config_hash,
+                            krul_snapshot** out, char* field, int field_cap);
+/* crc32 (common.cpp:34-42), all host threads for large buffers. */
+uint32_t krul_crc32(const void* data, uint64_t len, uint32_t crc);
+
 /* ---- restoration (scheduler.cpp:320-400) ------------------------------ */
 /* Restores conv to full-span KV [0, L): recompute stream rebuilds the
  * per-layer prefixes while the load stream streams blobs H2D and expands

@@ -4,6 +4,7 @@
 // compute"), runs device work through kb::, and maps kb::Error codes to
 // krul_status. The estimator and selector live here because they are thin:
 // their arithmetic is the K1/K2/K3 kernels in kernels.cu.
+#include <functional>
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -615,7 +616,7 @@ int krul_snapshot_storage(krul_snapshot* s, uint64_t* full, uint64_t* stored) {
   return guard([&] {
     need(s, "snapshot");
     const Snapshot& sn = *s->s;
-    const uint64_t row = 2ull * uint64_t(sn.Hkv) * uint64_t(sn.hd) * uint64_t(sn.ctx->esz);
+    const uint64_t row = 2ull * uint64_t(sn.Hkv) * uint64_t(sn.hd) * uint64_t(sn.esz);
     *full = uint64_t(sn.N) * uint64_t(sn.L) * row;
     *stored = 0;
     for (const auto& b : sn.blobs) *stored += uint64_t(b.end - b.start) * row;
@@ -634,6 +635,115 @@ int krul_snapshot_set_plan(krul_snapshot* s, const int64_t* p) {
     std::copy(p, p + s->s->N, s->s->p.begin());
     s->s->serial = next_serial();
   });
+}
+// ------------------------------------------------ KRUL v1 container (f3)
+int krul_snapshot_set_meta(krul_snapshot* s, const krul_snapshot_meta* m) {
+  return guard([&] {
+    need(s, "snapshot");
+    need(m, "meta");
+    SnapMeta& t = s->s->meta;
+    t.conversation_id = m->conversation_id ? m->conversation_id : "";
+    t.exhausted_before_quota = m->exhausted_before_quota != 0;
+    if ((m->n_ir_layers > 0 && !m->ir_layers) || (m->n_non_ir_layers > 0 && !m->non_ir_layers) ||
+        (m->n_avg_weight_sum > 0 && !m->avg_weight_sum))
+      fail(KRUL_E_ARG, "null meta array with a positive length");
+    t.ir_layers.assign(m->ir_layers, m->ir_layers + std::max(m->n_ir_layers, 0));
+    t.non_ir_layers.assign(m->non_ir_layers, m->non_ir_layers + std::max(m->n_non_ir_layers, 0));
+    t.avg_weight_sum.assign(m->avg_weight_sum, m->avg_weight_sum + std::max(m->n_avg_weight_sum, 0));
+  });
+}
+int krul_snapshot_get_meta(krul_snapshot* s, krul_snapshot_meta* m) {
+  return guard([&] {
+    need(s, "snapshot");
+    need(m, "meta");
+    const SnapMeta& t = s->s->meta;
+    m->conversation_id = t.conversation_id.c_str();
+    m->exhausted_before_quota = t.exhausted_before_quota ? 1 : 0;
+    m->ir_layers = t.ir_layers.data();
+    m->n_ir_layers = int(t.ir_layers.size());
+    m->non_ir_layers = t.non_ir_layers.data();
+    m->n_non_ir_layers = int(t.non_ir_layers.size());
+    m->avg_weight_sum = t.avg_weight_sum.data();
+    m->n_avg_weight_sum = int(t.avg_weight_sum.size());
+  });
+}
+int krul_snapshot_header(krul_snapshot* s, uint64_t* config_hash, int* n_layers, int* n_heads,
+                         int* head_dim, int64_t* history_len, int* mode, int* n_pairs) {
+  return guard([&] {
+    need(s, "snapshot");
+    const Snapshot& sn = *s->s;
+    if (config_hash) *config_hash = sn.config_hash;
+    if (n_layers) *n_layers = sn.N;
+    if (n_heads) *n_heads = sn.Hkv;
+    if (head_dim) *head_dim = sn.hd;
+    if (history_len) *history_len = sn.L;
+    if (mode) *mode = sn.mode;
+    if (n_pairs) *n_pairs = int(sn.pairs.size());
+  });
+}
+int krul_snapshot_pairs(krul_snapshot* s, krul_pair* out) {
+  return guard([&] {
+    need(s, "snapshot");
+    need(out, "out");
+    std::copy(s->s->pairs.begin(), s->s->pairs.end(), out);
+  });
+}
+int krul_snapshot_save(krul_snapshot* s, void* buf, uint64_t cap, uint64_t* len) {
+  return guard([&] {
+    need(s, "snapshot");
+    need(len, "len");
+    const uint64_t n = container_size(*s->s);
+    *len = n;
+    if (!buf) return;
+    if (cap < n) fail(KRUL_E_ARG, "buffer smaller than the container");
+    container_write(*s->s, static_cast<char*>(buf));
+  });
+}
+int krul_snapshot_save_file(krul_snapshot* s, const char* path) {
+  return guard([&] {
+    need(s, "snapshot");
+    need(path, "path");
+    container_write_file(*s->s, path);
+  });
+}
+static int load_common(krul_ctx* ctx, char* field, int field_cap, const std::function<Snapshot*(Ctx*)>& f,
+                       krul_snapshot** out) {
+  std::string fld;
+  if (field && field_cap > 0) field[0] = 0;
+  const int rc = guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    Ctx* c = ctx ? ctx->c : nullptr;
+    if (c) KB_CUDA(cudaSetDevice(c->device));
+    try {
+      *out = new krul_snapshot{f(c)};
+    } catch (const LoadError& e) {
+      fld = e.field;
+      throw;
+    }
+  });
+  if (field && field_cap > 0 && !fld.empty()) {
+    std::strncpy(field, fld.c_str(), size_t(field_cap) - 1);
+    field[field_cap - 1] = 0;
+  }
+  return rc;
+}
+int krul_snapshot_load(krul_ctx* ctx, const void* buf, uint64_t len, const uint64_t* expected_config_hash,
+                       krul_snapshot** out, char* field, int field_cap) {
+  if (!buf && len) return guard([] { fail(KRUL_E_ARG, "null buffer"); });
+  return load_common(ctx, field, field_cap, [&](Ctx* c) {
+    return container_read(c, buf ? static_cast<const char*>(buf) : "", size_t(len), expected_config_hash);
+  }, out);
+}
+int krul_snapshot_load_file(krul_ctx* ctx, const char* path, const uint64_t* expected_config_hash,
+                            krul_snapshot** out, char* field, int field_cap) {
+  if (!path) return guard([] { fail(KRUL_E_ARG, "null path"); });
+  return load_common(ctx, field, field_cap, [&](Ctx* c) {
+    return container_read_file(c, path, expected_config_hash);
+  }, out);
+}
+uint32_t krul_crc32(const void* data, uint64_t len, uint32_t crc) {
+  return data || !len ? kb::crc32(data ? data : "", size_t(len), crc) : crc;
 }
 int krul_expand(krul_snapshot* s, int layer, float* k, float* v, int64_t* start, int64_t* end) {
   return guard([&] {
@@ -883,9 +993,13 @@ int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int ep
     cudaStream_t s = c.s_comp;
     DevBuf a, b, out, res, out2, bias;
     void* da = a.ensure(size_t(M * K) * 2);
-    void* db = b.ensure(size_t(N * K) * 2);
+    // weights rotate over >= 320 MB so every launch streams them from HBM as
+    // in the restore DAG (one layer's weights fit the 126 MB L2)
+    const size_t wbytes = size_t(N * K) * 2;
+    const int nb = int(std::max<size_t>(1, ((size_t(320) << 20) + wbytes - 1) / wbytes));
+    char* db0 = static_cast<char*>(b.ensure(wbytes * nb));
     launch_init_uniform(c, s, da, M * K, 1, 1, 1.0f);
-    launch_init_uniform(c, s, db, N * K, 1, 2, 0.02f);
+    launch_init_uniform(c, s, db0, N * K * nb, 1, 2, 0.02f);
     Epi e;
     e.kind = epi;
     e.out = out.ensure(size_t(M * N) * 4 + 16);
@@ -904,10 +1018,10 @@ int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int ep
     g_gemm_force = force;
     g_gemm_splits = splits;
     try {
-      for (int i = 0; i < 2; ++i) gemm(c, s, M, N, K, da, K, db, K, e);
+      for (int i = 0; i < 2; ++i) gemm(c, s, M, N, K, da, K, db0 + wbytes * (i % nb), K, e);
       cudaEvent_t e0 = c.event(), e1 = c.event();
       KB_CUDA(cudaEventRecord(e0, s));
-      for (int i = 0; i < iters; ++i) gemm(c, s, M, N, K, da, K, db, K, e);
+      for (int i = 0; i < iters; ++i) gemm(c, s, M, N, K, da, K, db0 + wbytes * (i % nb), K, e);
       KB_CUDA(cudaEventRecord(e1, s));
       KB_CUDA(cudaEventSynchronize(e1));
       float ms = 0;

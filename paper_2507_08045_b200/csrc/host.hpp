@@ -1,5 +1,6 @@
 // host.hpp — host-side building blocks shared by the C ABI translation units.
 #pragma once
+#include <string>
 #include <vector>
 
 #include "kb.hpp"
@@ -55,8 +56,21 @@ std::vector<double> default_grid(double step);
 int validate_plan(int64_t L, const std::vector<int64_t>& p, const krul_pair* pairs, int np);
 
 // ---- compressed KV store ---------------------------------------------------
+// Container metadata the hot path does not use but the KRUL v1 container
+// carries (kvstore.hpp:46-59): conversation id, the selector's quota flag
+// and the layer classifier report.
+struct SnapMeta {
+  std::string conversation_id;
+  bool exhausted_before_quota = false;
+  std::vector<int> ir_layers, non_ir_layers;
+  std::vector<double> avg_weight_sum;
+  std::vector<int> shared;  // strategy.shared as loaded; empty = derived from the pairs
+};
+
 struct Snapshot {
-  Ctx* ctx = nullptr;
+  Ctx* ctx = nullptr;  // null for a host-only snapshot (container load without a device)
+  size_t esz = 4;      // element bytes of `host` (ctx compute dtype; 4 when host-only)
+  SnapMeta meta;
   uint64_t config_hash = 0;
   int N = 0, Hkv = 0, hd = 0;
   int64_t L = 0;
@@ -76,6 +90,17 @@ struct Snapshot {
 };
 uint64_t next_serial();
 int validate_plan_snapshot(const std::vector<int64_t>& p, int64_t L, const Snapshot& s);
+// KRUL v1 container (host_container.cpp).
+struct LoadError : Error {
+  std::string field;
+  LoadError(std::string f, const std::string& m) : Error(KRUL_E_SNAPSHOT_LOAD, f + ": " + m), field(std::move(f)) {}
+};
+uint32_t crc32(const void* p, size_t n, uint32_t crc = 0);
+uint64_t container_size(const Snapshot& s);
+void container_write(const Snapshot& s, char* out);  // exactly container_size bytes
+void container_write_file(const Snapshot& s, const char* path);
+Snapshot* container_read(Ctx* c, const char* buf, size_t n, const uint64_t* expected_hash);
+Snapshot* container_read_file(Ctx* c, const char* path, const uint64_t* expected_hash);
 void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
              krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
              double* ttft_ms);

@@ -63,15 +63,38 @@ void* DevBuf::ensure(size_t n) {
   }
   return p;
 }
+void PinnedBuf::pin() {
+  if (!p || !pageable || registered) return;
+  KB_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  registered = true;
+}
 PinnedBuf::~PinnedBuf() {
-  if (p) cudaFreeHost(p);
+  if (p) {
+    if (registered) cudaHostUnregister(p);
+    if (pageable)
+      std::free(p);
+    else
+      cudaFreeHost(p);
+  }
 }
 void* PinnedBuf::ensure(size_t n) {
   if (n > bytes) {
-    if (p) cudaFreeHost(p);
+    if (p) {
+      if (registered) cudaHostUnregister(p);
+      registered = false;
+      if (pageable)
+        std::free(p);
+      else
+        cudaFreeHost(p);
+    }
     p = nullptr;
     bytes = 0;
-    KB_CUDA(cudaMallocHost(&p, n));
+    if (pageable) {
+      p = std::malloc(n);
+      if (!p) throw std::bad_alloc();
+    } else {
+      KB_CUDA(cudaMallocHost(&p, n));
+    }
     bytes = n;
     g_buf_gen.fetch_add(1);
   }

@@ -61,6 +61,7 @@ static Snapshot* new_snapshot(Ctx& c, const krul_pair* pairs, int np, const int6
                               int mode) {
   auto* s = new Snapshot;
   s->ctx = &c;
+  s->esz = c.esz;
   s->config_hash = config_hash(c.cfg);
   s->N = c.cfg.N;
   s->Hkv = c.cfg.Hkv;
@@ -120,7 +121,7 @@ Snapshot* snapshot_from_host(Ctx& c, const krul_pair* pairs, int np, const int64
 void snapshot_blob_f32(const Snapshot& s, int b, int64_t row0, int64_t rows, float* k, float* v) {
   const auto& bl = s.blobs[size_t(b)];
   const int64_t brows = bl.end - bl.start;
-  const size_t esz = s.ctx->esz;
+  const size_t esz = s.esz;
   const char* base = static_cast<const char*>(s.host.p) + bl.off;
   for (int kv = 0; kv < 2; ++kv) {
     float* out = kv == 0 ? k : v;
@@ -256,6 +257,8 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
              double* ttft_ms) {
   const Cfg& g = c.cfg;
   if (snap.config_hash != config_hash(g)) fail(KRUL_E_SNAPSHOT, "snapshot was taken under a different model config");
+  if (snap.esz != c.esz || (snap.host.pageable && !snap.host.registered))
+    fail(KRUL_E_SNAPSHOT, "snapshot store is not pinned in this context's dtype (load it with the context)");
   if (L != snap.L) fail(KRUL_E_RESTORATION_GAP, "history length does not match the snapshot");
   const std::vector<int64_t>& p = snap.p;
   const int m = validate_plan_snapshot(p, L, snap);

@@ -93,6 +93,9 @@ struct DevBuf {
 struct PinnedBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool pageable = false;    // plain host memory (host-only snapshots, no device needed)
+  bool registered = false;  // pageable memory page-locked with cudaHostRegister
+  void pin();               // pageable -> registered (H2D-ready like cudaMallocHost)
   PinnedBuf() = default;
   PinnedBuf(const PinnedBuf&) = delete;
   PinnedBuf& operator=(const PinnedBuf&) = delete;

@@ -57,7 +57,10 @@ class SnapshotError(KrulError):
 
 
 class SnapshotLoadError(KrulError):
+    """kvstore::load failure; `field` names the container field that failed
+    (kvstore.hpp SnapshotLoadError::field)."""
     code = 8
+    field = ""
 
 
 class CudaError(KrulError):
@@ -96,6 +99,13 @@ class BlobSpecC(C.Structure):
     _fields_ = [("owners", C.c_int * 2), ("start", C.c_int64), ("end", C.c_int64)]
 
 
+class SnapshotMetaC(C.Structure):
+    _fields_ = [("conversation_id", C.c_char_p), ("exhausted_before_quota", C.c_int),
+                ("ir_layers", C.c_void_p), ("n_ir_layers", C.c_int),
+                ("non_ir_layers", C.c_void_p), ("n_non_ir_layers", C.c_int),
+                ("avg_weight_sum", C.c_void_p), ("n_avg_weight_sum", C.c_int)]
+
+
 class RestoreStats(C.Structure):
     _fields_ = [("restore_ms", C.c_double), ("compute_ms", C.c_double), ("load_ms", C.c_double),
                 ("bubble_compute", C.c_double), ("bubble_load", C.c_double),
@@ -118,7 +128,14 @@ def lib():
                               "(the CUDA extension is required; there is no CPU path)")
         _lib = C.CDLL(LIB_PATH)
         _lib.krul_snapshot_n_blobs.argtypes = [C.c_void_p]
+        _lib.krul_crc32.restype = C.c_uint32
+        _lib.krul_crc32.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32]
     return _lib
+
+
+def crc32(data: bytes, crc: int = 0) -> int:
+    """common.cpp:34-42 (host threads for large buffers)."""
+    return lib().krul_crc32(data, len(data), crc)
 
 
 def _check(rc):
@@ -617,9 +634,9 @@ class KVSnapshot:
     def blob(self, b):
         spec = BlobSpecC()
         _check(lib().krul_snapshot_blob(self.h, b, C.byref(spec), None, None))
-        cfg = self.ctx.cfg
+        hd = self.header()
         rows = spec.end - spec.start
-        k = np.empty((cfg.kv_heads, rows, cfg.head_dim), np.float32)
+        k = np.empty((hd["n_heads"], rows, hd["head_dim"]), np.float32)
         v = np.empty_like(k)
         _check(lib().krul_snapshot_blob(self.h, b, C.byref(spec), _p(k), _p(v)))
         o = [spec.owners[0]] + ([spec.owners[1]] if spec.owners[1] >= 0 else [])
@@ -631,23 +648,117 @@ class KVSnapshot:
         return f.value, s.value
 
     def plan(self):
-        N = self.ctx.cfg.n_layers
-        p = np.empty(N, np.int64)
+        N = self.header()["n_layers"]
+        p = np.empty(max(N, 1), np.int64)
         L = C.c_int64()
         _check(lib().krul_snapshot_plan(self.h, _p(p), C.byref(L)))
-        return p, L.value
+        return p[:N], L.value
 
     def set_plan(self, p):
         pp = np.ascontiguousarray(p, np.int64)
         _check(lib().krul_snapshot_set_plan(self.h, _p(pp)))
 
     def expand(self, layer):
-        cfg = self.ctx.cfg
+        hd = self.header()
         p, L = self.plan()
         rows = max(0, L - int(p[layer])) if 0 <= layer < len(p) else L
-        k = np.empty((cfg.kv_heads, max(rows, 1), cfg.head_dim), np.float32)
+        k = np.empty((hd["n_heads"], max(rows, 1), hd["head_dim"]), np.float32)
         v = np.empty_like(k)
         s, e = C.c_int64(), C.c_int64()
         _check(lib().krul_expand(self.h, layer, _p(k), _p(v), C.byref(s), C.byref(e)))
         r = e.value - s.value
         return (s.value, e.value), k[:, :r], v[:, :r]
+
+    # ---- KRUL v1 container (kvstore.cpp:360-511) ----
+    def header(self) -> dict:
+        h, n, kvh, hd, L, mode, npairs = (C.c_uint64(), C.c_int(), C.c_int(), C.c_int(),
+                                          C.c_int64(), C.c_int(), C.c_int())
+        _check(lib().krul_snapshot_header(self.h, C.byref(h), C.byref(n), C.byref(kvh), C.byref(hd),
+                                          C.byref(L), C.byref(mode), C.byref(npairs)))
+        return {"config_hash": h.value, "n_layers": n.value, "n_heads": kvh.value,
+                "head_dim": hd.value, "history_len": L.value, "mode": mode.value,
+                "n_pairs": npairs.value}
+
+    def pairs(self):
+        n = self.header()["n_pairs"]
+        arr = (Pair * max(1, n))()
+        _check(lib().krul_snapshot_pairs(self.h, arr))
+        return [(arr[i].shallow, arr[i].deep, arr[i].distance) for i in range(n)]
+
+    def set_meta(self, conversation_id: str = "", exhausted_before_quota: bool = False,
+                 ir_layers=(), non_ir_layers=(), avg_weight_sum=()):
+        ir = np.ascontiguousarray(list(ir_layers) or [0], np.int32)
+        nir = np.ascontiguousarray(list(non_ir_layers) or [0], np.int32)
+        avg = np.ascontiguousarray(list(avg_weight_sum) or [0.0], np.float64)
+        m = SnapshotMetaC(conversation_id.encode("utf-8", "surrogateescape"), int(bool(exhausted_before_quota)),
+                          ir.ctypes.data, len(ir_layers), nir.ctypes.data, len(non_ir_layers),
+                          avg.ctypes.data, len(avg_weight_sum))
+        _check(lib().krul_snapshot_set_meta(self.h, C.byref(m)))
+
+    def meta(self) -> dict:
+        m = SnapshotMetaC()
+        _check(lib().krul_snapshot_get_meta(self.h, C.byref(m)))
+
+        def arr(ptr, n, t):
+            return [] if n == 0 else list(C.cast(ptr, C.POINTER(t))[:n])
+
+        return {"conversation_id": (m.conversation_id or b"").decode("utf-8", "surrogateescape"),
+                "exhausted_before_quota": bool(m.exhausted_before_quota),
+                "ir_layers": arr(m.ir_layers, m.n_ir_layers, C.c_int32),
+                "non_ir_layers": arr(m.non_ir_layers, m.n_non_ir_layers, C.c_int32),
+                "avg_weight_sum": arr(m.avg_weight_sum, m.n_avg_weight_sum, C.c_double)}
+
+    def save(self) -> bytes:
+        """kvstore::save into memory: the container bytes."""
+        n = C.c_uint64()
+        _check(lib().krul_snapshot_save(self.h, None, C.c_uint64(0), C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        _check(lib().krul_snapshot_save(self.h, buf, C.c_uint64(n.value), C.byref(n)))
+        return buf.raw[:n.value]
+
+    def save_size(self) -> int:
+        n = C.c_uint64()
+        _check(lib().krul_snapshot_save(self.h, None, C.c_uint64(0), C.byref(n)))
+        return n.value
+
+    def save_to(self, buf: np.ndarray) -> int:
+        """Save into a caller-owned contiguous uint8 array; returns the bytes written."""
+        n = C.c_uint64()
+        _check(lib().krul_snapshot_save(self.h, _p(buf), C.c_uint64(buf.nbytes), C.byref(n)))
+        return n.value
+
+    def save_file(self, path: str):
+        _check(lib().krul_snapshot_save_file(self.h, os.fsencode(path)))
+
+    @classmethod
+    def _load(cls, fn, ctx, expected_config_hash):
+        h = C.c_void_p()
+        field = C.create_string_buffer(32)
+        eh = C.byref(C.c_uint64(expected_config_hash)) if expected_config_hash is not None else None
+        rc = fn(ctx.h if ctx is not None else None, eh, C.byref(h), field)
+        if rc != 0:
+            try:
+                _check(rc)
+            except SnapshotLoadError as e:
+                e.field = field.value.decode()
+                raise
+        return cls(h, ctx)
+
+    @classmethod
+    def load(cls, data: bytes, ctx: "Context | None" = None, expected_config_hash: int | None = None):
+        """kvstore::load. With ctx: pinned store in the ctx dtype, ready to
+        restore. Without: host-only f32 snapshot (inspect / expand / save)."""
+        if isinstance(data, np.ndarray):
+            if not data.flags.c_contiguous:
+                raise ValueError("container buffer must be contiguous")
+            ptr, n = _p(data), data.nbytes
+        else:
+            data = bytes(data)
+            ptr, n = data, len(data)
+        return cls._load(lambda c, eh, out, f: lib().krul_snapshot_load(
+            c, ptr, C.c_uint64(n), eh, out, f, 32), ctx, expected_config_hash)
+
+    @classmethod
+    def load_file(cls, path: str, ctx: "Context | None" = None, expected_config_hash: int | None = None):
+        return cls._load(lambda c, eh, out, f: lib().krul_snapshot_load_file(
+            c, os.fsencode(path), eh, out, f, 32), ctx, expected_config_hash)

@@ -531,3 +531,98 @@ def test_full_size_restore_properties(K, pairs, mode, monkeypatch):
     want = ctx.prefill(full, np.concatenate([hist, new]))
     if not pairs:
         assert rel_fro(outs[0], want) < 3e-2
+
+
+# ------------------------------------------------ KRUL v1 container (f3)
+def test_container_matches_oracle_f32(K, oracle, tmp_path):
+    """krul_snapshot_save / _load against oracle/container.py (kvstore.cpp:360-511):
+    bit-exact bytes for the same f32 store, exact metadata for a device
+    compress, and a loaded container restores like the oracle's restore."""
+    from oracle import container as OC
+    kw = dict(n_layers=4, n_heads=2, head_dim=4, d_model=8, vocab_size=13, seed=21)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
+    hist = oracle.tokens(70, 77, 13)
+    conv = ctx.conversation(128)
+    ctx.prefill(conv, hist)
+    okv = om.prefill(hist).take_kv()
+    pairs = [(1, 3, 0.25)]
+    p = K.build_plan(70, 4, 0.4, pairs)
+    cls = ([0, 1, 2, 3], [], [0.75, 0.5, 1.0 / 3.0, 1e-5])
+    for mode in (0, 1):
+        st = oracle.Strategy(pairs)
+        osnap = oracle.Snapshot(okv, ocfg, st, p, 70, mode=mode)
+        want = OC.from_oracle(osnap, ocfg, st, p, 70, mode, b"conv-7", cls)
+        # the oracle's blobs in the device store -> identical container bytes
+        blobs = [osnap.blob(b)[2:] for b in range(osnap.n_blobs())]
+        s1 = K.KVSnapshot.from_blobs(ctx, pairs, p, 70, mode, blobs)
+        s1.set_meta("conv-7", False, *cls)
+        raw = s1.save()
+        assert raw == OC.save(want)
+        # device compress -> same metadata, payload within the f32 tolerance
+        s2 = K.KVSnapshot.compress(ctx, conv, pairs, p, 70, mode)
+        s2.set_meta("conv-7", False, *cls)
+        got = OC.load(s2.save(), ocfg.hash())
+        assert OC.meta_text(got) == OC.meta_text(want)
+        for (o1, sp1, k1, v1), (o2, sp2, k2, v2) in zip(got.blobs, want.blobs):
+            assert o1 == o2 and sp1 == sp2
+            assert np.abs(k1 - k2).max() < 1e-5 and np.abs(v1 - v2).max() < 1e-5
+        # load into the context (pinned f32 store) and restore
+        s3 = K.KVSnapshot.load(raw, ctx, ocfg.hash())
+        assert s3.save() == raw and s3.meta()["conversation_id"] == "conv-7"
+        conv2 = ctx.conversation(128)
+        ctx.execute_restore(conv2, hist, s3)
+        rest = om.restore(hist, osnap)
+        for l in range(4):
+            k, v = conv2.kv(l, 0, 70)
+            (a, e), ko, vo = rest.span(l), *rest.layer(l)
+            assert (a, e) == (0, 70)
+            assert np.abs(k - ko).max() < 1e-4 and np.abs(v - vo).max() < 1e-4
+        # file path, config guard
+        path = str(tmp_path / f"m{mode}.krul")
+        s3.save_file(path)
+        assert open(path, "rb").read() == raw
+        with pytest.raises(K.SnapshotLoadError) as e:
+            K.KVSnapshot.load_file(path, ctx, ocfg.hash() + 1)
+        assert e.value.field == "config"
+    # a host-only snapshot cannot feed the restore DAG
+    host = K.KVSnapshot.load(raw)
+    with pytest.raises(K.SnapshotError):
+        ctx.execute_restore(ctx.conversation(128), hist, host)
+
+
+def test_container_bf16_round_trip_restores_bit_exact(K, oracle, tmp_path, monkeypatch):
+    """bf16 store -> f32 container (exact widening) -> bf16 store: the same bits,
+    so the restore + new-input prefill from the reloaded snapshot gives the
+    same logits bit for bit; a container from another config is rejected."""
+    monkeypatch.setenv("KRUL_KV_POOL_CONVS", "6")
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, **kw)
+    hist = oracle.tokens(512, 11, 256)
+    new = oracle.tokens(64, 12, 256)
+    conv = ctx.conversation(1024)
+    ctx.prefill(conv, hist)
+    pairs = [(1, 2, 0.5)]
+    p = K.build_plan(512, 4, 0.3, pairs)
+    snap = K.KVSnapshot.compress(ctx, conv, pairs, p, 512, K.MERGE_MEAN)
+    snap.set_meta("turn-3", True, [1, 2], [0, 3], [0.9, 0.8, 0.7, 0.2])
+    path = str(tmp_path / "bf16.krul")
+    snap.save_file(path)
+    raw = open(path, "rb").read()
+    assert raw == snap.save()
+    back = K.KVSnapshot.load_file(path, ctx, ocfg.hash())
+    assert back.save() == raw
+    for b in range(snap.n_blobs()):
+        assert snap.blob(b)[2].tobytes() == back.blob(b)[2].tobytes()
+    ctx.set_capture(False)
+    c1, c2 = ctx.conversation(1024), ctx.conversation(1024)
+    l1, _, _ = ctx.restore_and_prefill(c1, hist, snap, new)
+    l2, _, _ = ctx.restore_and_prefill(c2, hist, back, new)
+    assert np.array_equal(l1, l2)
+    # header says another model: restore refuses (scheduler.cpp:324)
+    other = bytearray(raw)
+    other[8:16] = (ocfg.hash() ^ 1).to_bytes(8, "little")
+    from oracle import oracle as O
+    other = bytes(other[:-4]) + O.crc32(bytes(other[:-4])).to_bytes(4, "little")
+    alien = K.KVSnapshot.load(other, ctx)
+    with pytest.raises(K.SnapshotError):
+        ctx.restore_and_prefill(ctx.conversation(1024), hist, alien, new)

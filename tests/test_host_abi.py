@@ -21,7 +21,7 @@ def K():
 
 def test_exports_every_declared_symbol(K):
     hdr = open(os.path.join(ROOT, "include", "krul_b200.h")).read()
-    names = set(re.findall(r"^int\s+(krul_\w+)\s*\(", hdr, re.M))
+    names = set(re.findall(r"^(?:int|uint32_t|uint64_t)\s+(krul_\w+)\s*\(", hdr, re.M))
     assert len(names) > 40
     lib = ctypes.CDLL(K.LIB_PATH)
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
