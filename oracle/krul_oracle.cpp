@@ -232,8 +232,11 @@ Mat layer_forward(const ModelConfig& cfg, const LayerW& w, const Mat& h_in,
     for (int64_t r = 0; r < out.r; ++r)
       for (int64_t j = 0; j < out.c; ++j)
         out.at(r, j) += y.at(r, j) + w.b2[size_t(j)];
-  } else {  // SwiGLU extension: h_mid + (silu(h_mid Wg) * (h_mid Wu)) W2
-    Mat g = matmul(hmid, w.w1), u = matmul(hmid, w.wu);
+  } else {  // SwiGLU extension, Llama's FFN block: h_mid + (silu(n Wg) * (n Wu)) W2,
+            // n = rmsnorm(h_mid) (gain-less like engine.cpp:117-124); without the
+            // norm the quadratic gate makes the residual grow doubly exponentially
+    const Mat hn = rmsnorm(hmid);
+    Mat g = matmul(hn, w.w1), u = matmul(hn, w.wu);
     for (size_t i = 0; i < g.v.size(); ++i) {
       const float x = g.v[i];
       g.v[i] = x / (1.0f + std::exp(-x)) * u.v[i];

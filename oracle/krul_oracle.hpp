@@ -85,7 +85,8 @@ struct Mat {
 
 // ---- engine (proj/include/krul/engine.hpp, proj/src/engine.cpp) ---------
 // Extensions beyond the reference (documented in DESIGN.md): n_kv_heads
-// (GQA), ffn_kind (0 = tanh+bias reference FFN, 1 = SwiGLU), rope_theta.
+// (GQA), ffn_kind (0 = tanh+bias reference FFN, 1 = SwiGLU with a gain-less
+// RMSNorm before it, as Llama), rope_theta.
 // Defaults reproduce the reference architecture exactly.
 struct ModelConfig {
   int n_layers = 4, n_heads = 2, head_dim = 8, d_model = 16, vocab = 64;

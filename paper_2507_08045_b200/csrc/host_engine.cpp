@@ -301,6 +301,9 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
     e1.bias = lw.b1;
     gemm(c, s, out_rows, g.F, g.d, w.hmidc, g.d, lw.w1, g.d, e1);
   } else {
+    // Llama FFN block: RMSNorm (gain-less, as the attention pre-norm) before
+    // the gated FFN; the residual keeps the un-normalised h_mid
+    launch_rmsnorm(c, s, w.hmid, out_rows, w.hmidc);
     e1.kind = Epi::SWIGLU;
     gemm(c, s, out_rows, 2 * int64_t(g.F), g.d, w.hmidc, g.d, lw.w1, g.d, e1);
   }

@@ -506,6 +506,7 @@ def test_full_size_restore_properties(K, pairs, mode, monkeypatch):
     snap = K.KVSnapshot.compress(ctx, prev, pairs, plan, L, mode)
     conv = ctx.conversation(L + n + 64)
     outs = [ctx.restore_and_prefill(conv, hist, snap, new)[0] for _ in range(3)]
+    assert np.isfinite(outs[0]).all()
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     bf = lambda x: (x.astype(np.float32).view(np.uint32) + 0x7FFF +  # noqa: E731
                     ((x.astype(np.float32).view(np.uint32) >> 16) & 1)) >> 16 << 16
@@ -531,6 +532,27 @@ def test_full_size_restore_properties(K, pairs, mode, monkeypatch):
     want = ctx.prefill(full, np.concatenate([hist, new]))
     if not pairs:
         assert rel_fro(outs[0], want) < 3e-2
+
+
+def test_llama_depth_stays_finite(K, monkeypatch):
+    """All 32 layers of the bench model (Llama-3-8B shape, random init): the
+    residual stream must stay bounded with depth (the SwiGLU block runs on
+    RMSNorm(h_mid), as Llama) -- every layer's K/V and the logits finite."""
+    monkeypatch.setenv("KRUL_KV_POOL_CONVS", "1")
+    L = 512
+    cfg = K.ModelConfig(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096,
+                        vocab_size=128256, ffn_mult=3.5, ffn_kind=1, rope_theta=500000.0, seed=1234,
+                        dtype=K.KRUL_BF16, max_tokens=L + 64)
+    ctx = K.Context(cfg, 0)
+    ctx.init_weights(1234)
+    hist = np.random.default_rng(1000).integers(0, cfg.vocab_size, L, dtype=np.int32)
+    conv = ctx.conversation(L + 64)
+    logits = ctx.prefill(conv, hist)
+    assert np.isfinite(logits).all()
+    for l in range(32):
+        k, v = conv.kv(l, 0, L)
+        assert np.isfinite(k).all() and np.isfinite(v).all(), l
+        assert 0 < np.abs(k).max() < 64 and 0 < np.abs(v).max() < 64, l
 
 
 # ------------------------------------------------ KRUL v1 container (f3)
