@@ -270,7 +270,7 @@ def run_b200(args, rank, local, world, dist):
     # around the coarse argmin of |T_C - T_L| (acceptance.cpp:478-487 style)
     # objective: measured TTFT of the restore + new-input prefill DAG
     coarse = [round(0.02 * k, 4) for k in range(0, 21)]
-    r0, _ = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, coarse)
+    r0, tt_coarse = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, coarse)
     fine = sorted({min(1.0, max(0.0, round(r0 + 0.004 * k, 4))) for k in range(-5, 6)})
     r_c, ttft_fine = ctx.calibrate_rc_ttft(prev, conv, hist, new, pairs, fine, reps=7)
     r_bal, _, _ = ctx.calibrate_rc_measured(prev, conv, hist, pairs, fine)
@@ -379,7 +379,9 @@ def run_b200(args, rank, local, world, dist):
                    "r_c": r_c, "r_c_analytic": r_analytic, "r_c_balanced_restore": r_bal,
                    "plan_head": [int(x) for x in plan[:4]], "pairs": len(pairs),
                    "h2d_gbs_measured": round(b_h2d / 1e9, 2),
-                   "recompute_tflops_measured": round(f_rec / 1e12, 1)},
+                   "recompute_tflops_measured": round(f_rec / 1e12, 1),
+                   "calibration_ttft_ms": {str(r): round(float(t), 3) for r, t in zip(coarse, tt_coarse)},
+                   "kv_store": snap.coding()},
         "restore": {k: round(v, 4) for k, v in st.items()},
         "timeline_ms": {"compute_done": [round(x, 3) for x in tl_c],
                         "load_done": [round(x, 3) for x in tl_l],

@@ -235,6 +235,30 @@ int krul_snapshot_set_plan(krul_snapshot* snap, const int64_t* recompute_len);
 int krul_expand(krul_snapshot* snap, int layer, float* k, float* v,
                 int64_t* start, int64_t* end);
 
+/* ---- exponent-coded store (B200 extension of the kvstore snapshot) -------
+ * The restore is PCIe-bound; a bf16 KV element's exponent carries ~2.6 bits
+ * of entropy. A coded store keeps each element's sign+mantissa byte raw and
+ * Huffman-codes its exponent (<= 12-bit canonical codes, 32 interleaved
+ * streams per 8192-element chunk); the restore copies the coded image H2D
+ * and decodes it on the expand stream. Lossless: the restored KV is
+ * bit-identical to the raw store. On by default for bf16 contexts at
+ * krul_snapshot_compress (KRUL_KV_CODING=0 or krul_set_kv_coding(ctx, 0)
+ * disables it). */
+int krul_set_kv_coding(krul_ctx* ctx, int on);
+/* Re-encode a raw bf16 snapshot bound to a context (from host / container). */
+int krul_snapshot_encode(krul_snapshot* snap);
+/* coded: 1 when the store is coded; raw/coded bytes of all blobs (coded ==
+ * raw for a raw store). */
+int krul_snapshot_coding(krul_snapshot* snap, int* coded, uint64_t* raw_bytes,
+                         uint64_t* coded_bytes);
+/* Codec checks: the host codec round trip (no device) and the device
+ * encoder/decoder on one array; img (NULL = size query) receives the coded
+ * image, decoded the decoded elements. */
+int krul_ec_host_roundtrip(const uint16_t* x, uint64_t n, void* img, uint64_t cap,
+                           uint64_t* img_bytes, uint16_t* decoded);
+int krul_debug_ec_device(krul_ctx* ctx, const uint16_t* x, uint64_t n, void* img,
+                         uint64_t cap, uint64_t* img_bytes, uint16_t* decoded);
+
 /* ---- KRUL v1 container (kvstore.hpp:88-98; kvstore.cpp:360-511) ---------
  * "KRUL" | u32 version | u64 config_hash | u64 metadata_len | metadata
  * (key-sorted compact JSON, byte-identical to the reference's nlohmann dump)

@@ -636,6 +636,95 @@ int krul_snapshot_set_plan(krul_snapshot* s, const int64_t* p) {
     s->s->serial = next_serial();
   });
 }
+// ------------------------------------------ exponent-coded store (kvcode)
+int krul_set_kv_coding(krul_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->kv_coding = on != 0;
+  });
+}
+int krul_snapshot_encode(krul_snapshot* s) {
+  return guard([&] {
+    need(s, "snapshot");
+    Snapshot& sn = *s->s;
+    if (sn.coded) return;
+    if (!sn.ctx || sn.host.pageable) fail(KRUL_E_SNAPSHOT, "encoding needs a snapshot bound to a context");
+    if (sn.esz != 2) fail(KRUL_E_CONFIG, "exponent coding needs a bf16 store");
+    Ctx& c = *sn.ctx;
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.s_load;
+    char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(sn.total, 256)));
+    if (sn.total) KB_CUDA(cudaMemcpyAsync(stg, sn.host.p, sn.total, cudaMemcpyHostToDevice, st));
+    snapshot_encode(c, sn, stg, st);
+  });
+}
+int krul_snapshot_coding(krul_snapshot* s, int* coded, uint64_t* raw_bytes, uint64_t* coded_bytes) {
+  return guard([&] {
+    need(s, "snapshot");
+    const Snapshot& sn = *s->s;
+    uint64_t raw = 0, cod = 0;
+    for (const auto& b : sn.blobs) {
+      raw += b.bytes;
+      cod += sn.coded ? b.cbytes : b.bytes;
+    }
+    if (coded) *coded = sn.coded ? 1 : 0;
+    if (raw_bytes) *raw_bytes = raw;
+    if (coded_bytes) *coded_bytes = cod;
+  });
+}
+// Host codec round trip (no device): histogram -> code -> ec_encode_host ->
+// ec_decode_host. img may be NULL (size query via *img_bytes).
+int krul_ec_host_roundtrip(const uint16_t* x, uint64_t n, void* img, uint64_t cap, uint64_t* img_bytes,
+                           uint16_t* decoded) {
+  return guard([&] {
+    need(img_bytes, "img_bytes");
+    if (n && !x) fail(KRUL_E_ARG, "null input");
+    uint64_t hist[256] = {0};
+    for (uint64_t i = 0; i < n; ++i) ++hist[(x[i] >> 7) & 0xFF];
+    const auto code = std::make_unique<EcCode>(ec_build_code(hist));
+    const std::vector<uint8_t> enc = ec_encode_host(x, n, *code);
+    *img_bytes = enc.size();
+    if (img) {
+      if (cap < enc.size()) fail(KRUL_E_ARG, "buffer smaller than the coded image");
+      std::memcpy(img, enc.data(), enc.size());
+    }
+    if (decoded && n) ec_decode_host(enc.data(), code->lut, decoded);
+  });
+}
+// The device encoder + decoder on one host array (GPU parity of the codec).
+int krul_debug_ec_device(krul_ctx* ctx, const uint16_t* x, uint64_t n, void* img, uint64_t cap,
+                         uint64_t* img_bytes, uint16_t* decoded) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(img_bytes, "img_bytes");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t st = c.s_load;
+    Snapshot sn;
+    sn.ctx = &c;
+    sn.esz = 2;
+    sn.blobs.push_back(Snapshot::Blob{{0, -1}, 0, 0, 0, size_t(n) * 2});
+    sn.total = size_t(n) * 2;
+    DevBuf raw, out, cimg;
+    char* d = static_cast<char*>(raw.ensure(std::max<size_t>(sn.total, 256)));
+    if (n) KB_CUDA(cudaMemcpyAsync(d, x, sn.total, cudaMemcpyHostToDevice, st));
+    snapshot_encode(c, sn, d, st);
+    const auto& b = sn.blobs[0];
+    *img_bytes = b.cbytes;
+    if (img) {
+      if (cap < b.cbytes) fail(KRUL_E_ARG, "buffer smaller than the coded image");
+      std::memcpy(img, static_cast<char*>(sn.host.p) + b.coff, b.cbytes);
+    }
+    if (decoded && n) {
+      char* ci = static_cast<char*>(cimg.ensure(std::max<size_t>(b.cbytes, 256)));
+      KB_CUDA(cudaMemcpyAsync(ci, static_cast<char*>(sn.host.p) + b.coff, b.cbytes, cudaMemcpyHostToDevice, st));
+      void* o = out.ensure(sn.total);
+      launch_ec_decode(st, ci, int64_t(b.ec_chunks), sn.lut_dev.as<uint16_t>(), o);
+      KB_CUDA(cudaMemcpyAsync(decoded, o, sn.total, cudaMemcpyDeviceToHost, st));
+    }
+    KB_CUDA(cudaStreamSynchronize(st));
+  });
+}
 // ------------------------------------------------ KRUL v1 container (f3)
 int krul_snapshot_set_meta(krul_snapshot* s, const krul_snapshot_meta* m) {
   return guard([&] {

@@ -4,6 +4,7 @@
 #include <vector>
 
 #include "kb.hpp"
+#include "kvcode.hpp"
 
 namespace kb {
 
@@ -80,12 +81,19 @@ struct Snapshot {
   struct Blob {
     int owners[2];
     int64_t start, end;
-    size_t off;    // byte offset in `host`
-    size_t bytes;
+    size_t off;    // byte offset of the raw blob (device staging; `host` when raw)
+    size_t bytes;  // raw bytes
+    size_t coff = 0, cbytes = 0;  // coded image in `host` (coded stores)
+    uint32_t ec_chunks = 0;
   };
   std::vector<Blob> blobs;
-  PinnedBuf host;  // all blobs, compute dtype, [K: Hkv][rows][hd][V: ...]
-  size_t total = 0;
+  PinnedBuf host;  // raw: all blobs, compute dtype, [K: Hkv][rows][hd][V: ...];
+                   // coded: the exponent-coded images (kvcode.hpp)
+  size_t total = 0;   // raw bytes of all blobs (device staging size)
+  bool coded = false;
+  std::unique_ptr<EcCode> code;  // the snapshot's exponent code (coded stores)
+  DevBuf lut_dev;                // its decode LUT on the device
+  size_t ctotal = 0;             // coded image bytes
   uint64_t serial = 0;  // changes whenever blobs or plan change (graph cache key)
 };
 uint64_t next_serial();
@@ -96,6 +104,9 @@ struct LoadError : Error {
   LoadError(std::string f, const std::string& m) : Error(KRUL_E_SNAPSHOT_LOAD, f + ": " + m), field(std::move(f)) {}
 };
 uint32_t crc32(const void* p, size_t n, uint32_t crc = 0);
+// exponent-coded store (host_kvcode.cpp)
+void snapshot_encode(Ctx& c, Snapshot& s, const char* dev_raw, cudaStream_t st);
+const char* snapshot_raw_blob(const Snapshot& s, int b, std::vector<uint16_t>& tmp);
 uint64_t container_size(const Snapshot& s);
 void container_write(const Snapshot& s, char* out);  // exactly container_size bytes
 void container_write_file(const Snapshot& s, const char* path);

@@ -868,11 +868,12 @@ uint64_t container_size(const Snapshot& s) {
 void container_write(const Snapshot& s, char* out) {
   const std::string meta = meta_text(s);
   char* o = out + header_into(s, meta, out);
-  const char* base = static_cast<const char*>(s.host.p);
-  for (const auto& b : s.blobs) {
+  std::vector<uint16_t> tmp;
+  for (size_t bi = 0; bi < s.blobs.size(); ++bi) {
+    const auto& b = s.blobs[bi];
     o += blob_header_into(s, b, o);
     const size_t n = payload_elems(s, b);
-    to_f32(base + b.off, s.esz, o, n);
+    to_f32(snapshot_raw_blob(s, int(bi), tmp), s.esz, o, n);
     o += n * 4;
   }
   const uint32_t c = crc32(out, size_t(o - out));
@@ -892,15 +893,17 @@ void container_write_file(const Snapshot& s, const char* path) {
   emit(hb.data(), header_into(s, meta, hb.data()));
   constexpr size_t kBounce = size_t(64) << 20;  // f32 bytes per conversion chunk
   std::vector<char> bounce;
-  const char* base = static_cast<const char*>(s.host.p);
-  for (const auto& b : s.blobs) {
+  std::vector<uint16_t> tmp;
+  for (size_t bi = 0; bi < s.blobs.size(); ++bi) {
+    const auto& b = s.blobs[bi];
+    const char* raw = snapshot_raw_blob(s, int(bi), tmp);
     char bh[64];
     emit(bh, blob_header_into(s, b, bh));
     const size_t n = payload_elems(s, b);
     if (bounce.size() < std::min(n * 4, kBounce)) bounce.resize(std::min(n * 4, kBounce));
     for (size_t i = 0; i < n; i += kBounce / 4) {
       const size_t m = std::min(kBounce / 4, n - i);
-      to_f32(base + b.off + i * s.esz, s.esz, bounce.data(), m);
+      to_f32(raw + i * s.esz, s.esz, bounce.data(), m);
       emit(bounce.data(), m * 4);
     }
   }

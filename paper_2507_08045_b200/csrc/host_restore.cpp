@@ -38,7 +38,7 @@ static uint16_t f32_to_bf16(float f) {  // round to nearest even (== __float2bfl
 }
 
 // Layout blobs of a snapshot from (strategy, plan).
-static void layout_blobs(Ctx& c, Snapshot& s) {
+static void layout_blobs(Ctx& c, Snapshot& s, bool alloc_host = true) {
   const auto specs = blob_specs(s.p, s.L, s.pairs.data(), int(s.pairs.size()));
   size_t off = 0;
   s.blobs.clear();
@@ -54,7 +54,15 @@ static void layout_blobs(Ctx& c, Snapshot& s) {
     s.blobs.push_back(b);
   }
   s.total = off;
-  s.host.ensure(std::max<size_t>(off, 256));
+  if (alloc_host) s.host.ensure(std::max<size_t>(off, 256));
+}
+
+static bool coding_on(const Ctx& c) {
+  static const bool env = [] {
+    const char* v = std::getenv("KRUL_KV_CODING");
+    return !(v && v[0] == '0');
+  }();
+  return env && c.kv_coding && c.esz == 2;
 }
 
 static Snapshot* new_snapshot(Ctx& c, const krul_pair* pairs, int np, const int64_t* p, int64_t L,
@@ -81,7 +89,8 @@ Snapshot* snapshot_compress(Ctx& c, Conv& conv, const krul_pair* pairs, int np, 
   if (mode != KRUL_MERGE_MEAN && mode != KRUL_MERGE_KEEP_DEEPER) fail(KRUL_E_CONFIG, "unknown merge mode");
   if (conv.len != L) fail(KRUL_E_SNAPSHOT, "cache span does not cover the plan's history");
   std::unique_ptr<Snapshot> s(new_snapshot(c, pairs, np, p, L, mode));
-  layout_blobs(c, *s);
+  const bool code = coding_on(c);
+  layout_blobs(c, *s, !code);
   KB_CUDA(cudaSetDevice(c.device));
   cudaStream_t st = c.s_load;
   char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(s->total, 256)));
@@ -92,7 +101,12 @@ Snapshot* snapshot_compress(Ctx& c, Conv& conv, const krul_pair* pairs, int np, 
     const int64_t merge_from = pair ? p[b.owners[0]] : L;
     launch_compress(c, st, conv, deep, shallow, b.start, L, merge_from, stg + b.off);
   }
-  if (s->total) KB_CUDA(cudaMemcpyAsync(s->host.p, stg, s->total, cudaMemcpyDeviceToHost, st));
+  if (code && s->total) {
+    snapshot_encode(c, *s, stg, st);  // coded host store, one D2H of the coded image
+  } else {
+    s->host.ensure(std::max<size_t>(s->total, 256));
+    if (s->total) KB_CUDA(cudaMemcpyAsync(s->host.p, stg, s->total, cudaMemcpyDeviceToHost, st));
+  }
   KB_CUDA(cudaStreamSynchronize(st));
   return s.release();
 }
@@ -122,7 +136,8 @@ void snapshot_blob_f32(const Snapshot& s, int b, int64_t row0, int64_t rows, flo
   const auto& bl = s.blobs[size_t(b)];
   const int64_t brows = bl.end - bl.start;
   const size_t esz = s.esz;
-  const char* base = static_cast<const char*>(s.host.p) + bl.off;
+  std::vector<uint16_t> tmp;
+  const char* base = snapshot_raw_blob(s, b, tmp);
   for (int kv = 0; kv < 2; ++kv) {
     float* out = kv == 0 ? k : v;
     if (!out) continue;
@@ -174,6 +189,7 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   const Mark* newp = loaded + g.N;
   cudaStream_t sc = c.s_comp, sl = c.s_load;
   char* stg = static_cast<char*>(c.staging.p);
+  char* cstg = static_cast<char*>(c.cstaging.p);
   float* d_logits = static_cast<float*>(c.ws_logits.p);
 
   // token uploads first: a small H2D queued behind the blob copies on the
@@ -193,7 +209,11 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
     const auto& b = snap.blobs[bi];
     copied[bi] = c.event();
-    if (b.bytes) {
+    if (snap.coded && b.cbytes) {  // coded image -> cstaging, decoded on the expand stream
+      KB_CUDA(cudaMemcpyAsync(cstg + b.coff, static_cast<char*>(snap.host.p) + b.coff, b.cbytes,
+                              cudaMemcpyHostToDevice, sl));
+      h2d += double(b.cbytes);
+    } else if (!snap.coded && b.bytes) {
       KB_CUDA(cudaMemcpyAsync(stg + b.off, static_cast<char*>(snap.host.p) + b.off, b.bytes,
                               cudaMemcpyHostToDevice, sl));
       h2d += double(b.bytes);
@@ -204,6 +224,8 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
     const auto& b = snap.blobs[bi];
     KB_CUDA(cudaStreamWaitEvent(c.s_exp, copied[bi], 0));
+    if (snap.coded && b.cbytes)
+      launch_ec_decode(c.s_exp, cstg + b.coff, int64_t(b.ec_chunks), snap.lut_dev.as<uint16_t>(), stg + b.off);
     for (int o : b.owners) {
       if (o < 0) continue;
       launch_expand(c, c.s_exp, stg + b.off, b.start, L, conv, o, p[size_t(o)]);
@@ -283,6 +305,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   if (nn) std::memcpy(tp + nh, new_tok, size_t(nn) * 4);
   float* lp = (logits && new_tok) ? static_cast<float*>(c.logits_pin.ensure(size_t(g.V) * 4)) : nullptr;
   c.staging.ensure(std::max<size_t>(snap.total, 256));
+  if (snap.coded) c.cstaging.ensure(std::max<size_t>(snap.ctotal, 256));
   c.ws_logits.ensure(size_t(g.V) * 4);
 
   auto& G = c.rg;

@@ -209,6 +209,8 @@ struct Ctx {
 
   // restore staging + last measured timeline (ms from launch)
   DevBuf staging;
+  DevBuf cstaging;       // coded blob images (H2D target; decoded into `staging`)
+  bool kv_coding = true; // exponent-code bf16 snapshots at compress (KRUL_KV_CODING=0: off)
   PinnedBuf tok_pin;     // pinned token staging (history | new input) for async / graph H2D
   PinnedBuf logits_pin;  // pinned logits landing buffer
   // CUDA graph of the last restore DAG (replayed when the key repeats)

@@ -1,0 +1,60 @@
+// kvcode.hpp — format of the exponent-coded bf16 KV store (kvcode.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace kb {
+
+constexpr int kEcChunk = 8192;  // elements per chunk (32 lanes x 256)
+constexpr int kEcMaxLen = 12;   // longest code; LUT = 2^12 entries
+
+struct EcHeader {
+  uint32_t magic;      // 'E','C','1','6'
+  uint32_t n_elems;
+  uint32_t n_chunks;
+  uint32_t sm_off;     // byte offset of the sign+mantissa plane
+  uint32_t exp_off;    // byte offset of the exponent words
+  uint32_t exp_words;  // words in the exponent streams (+1 pad word follows)
+  uint32_t pad[2];
+};
+static_assert(sizeof(EcHeader) == 32, "EcHeader is 32 bytes");
+constexpr uint32_t kEcMagic = 0x36314345u;  // "EC16"
+
+// Canonical, length-limited (<= kEcMaxLen) Huffman code of an exponent
+// histogram: code[s] (right-aligned, len[s] bits), len 0 = absent symbol,
+// and the 4096-entry decode LUT (symbol | len << 8).
+struct EcCode {
+  uint32_t code[256];
+  uint8_t len[256];
+  uint16_t lut[1 << kEcMaxLen];
+};
+EcCode ec_build_code(const uint64_t* hist);
+
+inline size_t ec_align16(size_t x) { return (x + 15) & ~size_t(15); }
+// Section offsets of a coded blob of n elements whose streams hold exp_words.
+inline void ec_layout(uint64_t n, uint64_t exp_words, EcHeader* h, size_t* total) {
+  const uint64_t chunks = (n + kEcChunk - 1) / kEcChunk;
+  h->magic = kEcMagic;
+  h->n_elems = uint32_t(n);
+  h->n_chunks = uint32_t(chunks);
+  h->sm_off = uint32_t(ec_align16(sizeof(EcHeader) + 4 * 32 * chunks));
+  h->exp_off = uint32_t(ec_align16(h->sm_off + n));
+  h->exp_words = uint32_t(exp_words);
+  h->pad[0] = h->pad[1] = 0;
+  *total = ec_align16(size_t(h->exp_off) + 4 * (size_t(exp_words) + 1));
+}
+// Host codec (tests, inspection, container save): identical bytes / values
+// to the device kernels.
+std::vector<uint8_t> ec_encode_host(const uint16_t* x, uint64_t n, const EcCode& code);
+void ec_decode_host(const uint8_t* blob, const uint16_t* lut, uint16_t* out);
+
+void launch_exp_hist(cudaStream_t s, const void* x, int64_t n, unsigned long long* hist);
+void launch_ec_lane_words(cudaStream_t s, const void* x, int64_t n, const uint8_t* len, uint32_t* words);
+void launch_ec_encode(cudaStream_t s, const void* x, int64_t n, const uint32_t* code, const uint8_t* len,
+                      const uint32_t* lane_off, uint8_t* sm, uint32_t* ex);
+void launch_ec_decode(cudaStream_t s, const void* blob, int64_t n_chunks, const uint16_t* lut, void* out);
+
+}  // namespace kb

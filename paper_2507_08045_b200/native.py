@@ -225,6 +225,10 @@ class Context:
     def conversation(self, capacity=None) -> "Conversation":
         return Conversation(self, capacity or self.cfg.max_tokens)
 
+    def set_kv_coding(self, on: bool):
+        """Exponent-code bf16 snapshots at compress (lossless; default on)."""
+        _check(lib().krul_set_kv_coding(self.h, int(bool(on))))
+
     def set_capture(self, probs: bool):
         _check(lib().krul_set_capture(self.h, int(bool(probs))))
 
@@ -668,6 +672,16 @@ class KVSnapshot:
         _check(lib().krul_expand(self.h, layer, _p(k), _p(v), C.byref(s), C.byref(e)))
         r = e.value - s.value
         return (s.value, e.value), k[:, :r], v[:, :r]
+
+    def encode(self):
+        """Exponent-code a raw bf16 store (lossless)."""
+        _check(lib().krul_snapshot_encode(self.h))
+
+    def coding(self) -> dict:
+        c, r, k = C.c_int(), C.c_uint64(), C.c_uint64()
+        _check(lib().krul_snapshot_coding(self.h, C.byref(c), C.byref(r), C.byref(k)))
+        return {"coded": bool(c.value), "raw_bytes": r.value, "coded_bytes": k.value,
+                "ratio": (k.value / r.value) if r.value else 1.0}
 
     # ---- KRUL v1 container (kvstore.cpp:360-511) ----
     def header(self) -> dict:

@@ -648,3 +648,70 @@ def test_container_bf16_round_trip_restores_bit_exact(K, oracle, tmp_path, monke
     alien = K.KVSnapshot.load(other, ctx)
     with pytest.raises(K.SnapshotError):
         ctx.restore_and_prefill(ctx.conversation(1024), hist, alien, new)
+
+
+# ---------------------------------------------- exponent-coded KV store
+@pytest.mark.parametrize("n", [1, 33, 8192, 8193, 5 * 8192 + 1000, 1 << 22])
+def test_kvcode_device_matches_host(K, n):
+    """Device histogram + encode produce the host codec's image byte for byte;
+    the device decoder restores every element."""
+    import ctypes as C
+    cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
+                        dtype=K.KRUL_BF16, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(n)
+    u = (rng.standard_normal(n) * 0.5).astype(np.float32).view(np.uint32)
+    x = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    if n > 100:
+        x[::97] = np.uint16(0x0001)  # denormal exponent 0 -> long codes
+    lib = K.lib()
+    nb = C.c_uint64()
+    assert lib.krul_ec_host_roundtrip(K._p(x), C.c_uint64(n), None, C.c_uint64(0), C.byref(nb), None) == 0
+    himg = np.zeros(nb.value, np.uint8)
+    lib.krul_ec_host_roundtrip(K._p(x), C.c_uint64(n), K._p(himg), C.c_uint64(himg.size), C.byref(nb), None)
+    dimg = np.zeros(nb.value + 64, np.uint8)
+    dec = np.zeros(n, np.uint16)
+    rc = lib.krul_debug_ec_device(ctx.h, K._p(x), C.c_uint64(n), K._p(dimg), C.c_uint64(dimg.size),
+                                  C.byref(nb), K._p(dec))
+    assert rc == 0 and nb.value == himg.size
+    assert np.array_equal(dimg[:nb.value], himg)
+    assert np.array_equal(dec, x)
+
+
+def test_coded_store_restores_bit_exact(K, oracle, monkeypatch):
+    """The coded store (H2D of the coded image + device decode) restores the
+    same bits as the raw store: identical logits, KV, blob values and
+    container bytes; the load stream moves fewer bytes."""
+    monkeypatch.setenv("KRUL_KV_POOL_CONVS", "6")
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, **kw)
+    hist = oracle.tokens(700, 11, 256)
+    new = oracle.tokens(64, 12, 256)
+    conv = ctx.conversation(1024)
+    ctx.prefill(conv, hist)
+    pairs = [(1, 2, 0.5)]
+    p = K.build_plan(700, 4, 0.3, pairs)
+    ctx.set_kv_coding(False)
+    raw = K.KVSnapshot.compress(ctx, conv, pairs, p, 700, K.MERGE_MEAN)
+    ctx.set_kv_coding(True)
+    cod = K.KVSnapshot.compress(ctx, conv, pairs, p, 700, K.MERGE_MEAN)
+    assert not raw.coding()["coded"] and cod.coding()["coded"]
+    assert cod.coding()["ratio"] < 0.8
+    for b in range(raw.n_blobs()):
+        assert raw.blob(b)[2].tobytes() == cod.blob(b)[2].tobytes()
+        assert raw.blob(b)[3].tobytes() == cod.blob(b)[3].tobytes()
+    assert raw.save() == cod.save()
+    ctx.set_capture(False)
+    c1, c2 = ctx.conversation(1024), ctx.conversation(1024)
+    for _ in range(3):  # eager, capture, graph replay
+        l1, s1, _ = ctx.restore_and_prefill(c1, hist, raw, new)
+        l2, s2, _ = ctx.restore_and_prefill(c2, hist, cod, new)
+        assert np.array_equal(l1, l2)
+        assert s2["h2d_bytes"] < s1["h2d_bytes"]
+    for l in range(4):
+        k1, v1 = c1.kv(l, 0, 764)
+        k2, v2 = c2.kv(l, 0, 764)
+        assert np.array_equal(k1, k2) and np.array_equal(v1, v2)
+    # a raw store re-encoded later is the same code / image
+    raw.encode()
+    assert raw.coding() == cod.coding()
