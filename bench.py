@@ -44,6 +44,12 @@ except Exception:
 # dram__bytes_read.sum + dram__bytes_write.sum of one FFN1 pair-GEMM launch
 # (profiles/r01c/SUMMARY.md): 251.06 MB + 25.40 MB
 NCU_FFN1_DRAM_BYTES = 276_462_080
+# ncu --set full DRAM bytes (read + write) of one launch per kernel class vs
+# its algorithmic bytes, from the committed captures under profiles/
+NCU_TRAFFIC = {
+    "gemm": (NCU_FFN1_DRAM_BYTES, 1078 * 4096 * 2 + 28672 * 4096 * 2 + 1078 * 14336 * 2,
+             "profiles/r01c/SUMMARY.md (FFN1 pair GEMM, M=1078 N=28672 K=4096)"),
+}
 
 METRIC = ("restoration TTFT p50 (ms) @8K history; conversations restored/sec at 1/2/4/8 GPU")
 
@@ -305,7 +311,8 @@ def run_b200(args, rank, local, world, dist):
     # runs on. Kept out of the headline steps because an event between two
     # kernels costs their launch overlap (~+35% on the step, measured).
     ctx.ktime_enable(True)
-    tags = (("gemm", 0), ("attention", 1), ("expand", 2), ("gemm_stream", 7))
+    tags = (("gemm", 0), ("attention", 1), ("expand", 2), ("gemm_stream", 7), ("decode", 8),
+            ("logits", 9))
     kt = {name: [0, 0.0, 0.0, 0.0] for name, _ in tags}
     peak_t = PEAKS.get("bf16_tflops_sustained", 1397.8)
     peak_b = PEAKS.get("hbm_gbs", 6547.2)
@@ -337,23 +344,60 @@ def run_b200(args, rank, local, world, dist):
     conv_s = world * args.steps / (total_ms / 1e3)
     e2e_conv_s = world * args.steps / (wall_total / 1e3)
     st = {k: float(np.median([s[k] for s in stats])) for k in stats[0]}
-    # dominant kernel (by device time): the tcgen05 GEMM, timed per launch
-    # with CUDA events on its own stream (instrumented pass above)
+    # Per kernel class: algorithmic work / CUDA-event time per launch, summed
+    # over the instrumented steps; the dominant class (by device time in the
+    # DAG) is the `roofline` object, the rest go to `rooflines`.
     peak = PEAKS.get("bf16_tflops_sustained", 1397.8)
-    peak_src = ("MEASURED_PEAKS.json bf16_tflops_sustained" if "MEASURED_PEAKS_FILE" in PEAKS
-                else "fallback (B200_PROFILING.md: sustained bf16 ~1.4 PFLOP/s; MEASURED_PEAKS.json absent)")
+    peak_src = ("MEASURED_PEAKS.json bf16_tflops_sustained / hbm_gbs" if "MEASURED_PEAKS_FILE" in PEAKS
+                else "fallback (B200_PROFILING.md: sustained bf16 ~1.4 PFLOP/s, 6547 GB/s copy; "
+                     "MEASURED_PEAKS.json absent)")
     hbm = PEAKS.get("hbm_gbs", 6547.2)
-    g_n, g_ms, g_fl, _ = kt["gemm"]
-    a_n, a_ms, a_fl, _ = kt["attention"]
-    e_n, e_ms, _, e_by = kt["expand"]
-    s_n, s_ms, _, s_by = kt["gemm_stream"]
-    achieved_tf = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-    iso = {}
-    for name, kind in (("gemm", "tf"), ("attention", "tf"), ("gemm_stream", "gbs"), ("expand", "gbs")):
-        n_, ms_, fl_, by_ = kti[name]
-        if ms_ > 0:
-            iso[name] = (round(fl_ / (ms_ * 1e-3) / 1e12, 2) if kind == "tf"
-                         else round(by_ / (ms_ * 1e-3) / 1e9, 1))
+    classes = {
+        "gemm": ("tensor", "k_gemm_tc / k_gemm_tc2, M > 128 (recompute GEMMs, K6)", "2*M*N*K flop per launch"),
+        "gemm_stream": ("hbm", "k_gemm_tc (+ split-K reduce), M <= 128 (new-input prefill, K7)",
+                        "weights N*K*2 + A M*K*2 + C M*N*4 bytes per launch"),
+        "attention": ("tensor", "k_attn_fa (+ split-KV merge)", "4*hd*H*sum(visible keys) flop per launch"),
+        "decode": ("hbm", "k_ec_decode (exponent-coded blob -> raw bf16, K4b)",
+                   "coded image bytes read + raw bytes written per blob"),
+        "expand": ("hbm", "k_expand (K5)", "rows*2*Hkv*hd*2 bytes x (read + write) per owner"),
+        "logits": ("hbm", "k_logits_vec (last-row LM head)", "V*d*2 + V*4 bytes"),
+    }
+
+    def rate(v, bound):
+        n_, ms_, fl_, by_ = v
+        if ms_ <= 0:
+            return None
+        return round(fl_ / (ms_ * 1e-3) / 1e12, 2) if bound == "tensor" else round(by_ / (ms_ * 1e-3) / 1e9, 1)
+
+    roof = {}
+    for name, (bound, kern, alg) in classes.items():
+        n_, ms_, fl_, by_ = kt[name]
+        if n_ == 0:
+            continue
+        pk = peak if bound == "tensor" else hbm
+        a = rate(kt[name], bound)
+        roof[name] = {"bound": bound, "kernel": kern, "achieved": a, "peak": pk,
+                      "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+                      "frac": round(a / pk, 4) if a else None, "launches": int(n_) // max(args.steps, 1),
+                      "ms_per_step": round(ms_ / args.steps, 4),
+                      "avg_launch_us": round(1e3 * ms_ / max(n_, 1), 2), "algorithmic": alg,
+                      "achieved_serialised": rate(kti[name], bound),
+                      "frac_of_roofline": round(ideal[name] / ms_, 4) if name in ideal and ms_ else None}
+    dominant = max(roof, key=lambda k: roof[k]["ms_per_step"])
+    head = dict(roof[dominant])
+    tr = NCU_TRAFFIC.get(dominant)
+    head.update({"class": dominant,
+                 "traffic": tr[0] if tr else None,
+                 "traffic_algorithmic": tr[1] if tr else None,
+                 "traffic_source": tr[2] if tr else "no ncu capture of this class yet",
+                 "frac_of_roofline_note": "sum over launches of max(flops / tensor peak, bytes / HBM peak) "
+                                          "/ measured time",
+                 "serialised_note": "same launches timed with the new-input prefill serialised behind "
+                                    "the recompute (no SM sharing)",
+                 "measured": "CUDA events around each launch on its own stream, instrumented pass of the "
+                             "same steps right after the timed region",
+                 "peak_source": peak_src})
+    h2d_gbs = round(st["h2d_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9, 2)
     pol = policies_leg(K, ctx, prev, conv, cfg, hist, new, L, r_c, pairs) if (
         rank == 0 and not args.no_policies) else None
     est = estimator_leg(K, ctx, conv, cfg, spec) if rank == 0 else None
@@ -387,53 +431,17 @@ def run_b200(args, rank, local, world, dist):
                         "load_done": [round(x, 3) for x in tl_l],
                         "new_prefill_done": [round(x, 3) for x in tl_n]},
         "storage": {"full_bytes": full_b, "stored_bytes": stored_b},
-        "roofline": {"bound": "tensor", "kernel": "k_gemm_tc / k_gemm_tc2, M > 128 (recompute GEMMs, K6)",
-                     "achieved": round(achieved_tf, 2), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved_tf / peak, 4),
-                     # DRAM bytes of one launch of the dominant GEMM (FFN1 pair GEMM of
-                     # recompute layer 0, M=1078 N=28672 K=4096) from the committed
-                     # ncu --set full capture vs its algorithmic bytes (A + B + C)
-                     "traffic": NCU_FFN1_DRAM_BYTES,
-                     "traffic_algorithmic": 1078 * 4096 * 2 + 28672 * 4096 * 2 + 1078 * 14336 * 2,
-                     "traffic_source": "profiles/r01c/SUMMARY.md (ncu --set full, one launch)",
-                     "frac_of_roofline": round(ideal["gemm"] / g_ms, 4) if g_ms else None,
-                     "frac_of_roofline_note": "sum over launches of max(2MNK / tensor peak, "
-                                              "(A+B+C bytes) / HBM peak) / measured time: the "
-                                              "small-M pyramid layers are weight-streaming bound",
-                     "achieved_serialised": iso.get("gemm"),
-                     "frac_serialised": round(iso["gemm"] / peak, 4) if "gemm" in iso else None,
-                     "serialised_note": "same launches timed with the new-input prefill serialised "
-                                        "behind the recompute (no SM sharing)",
-                     "launches": g_n, "avg_launch_us": round(1e3 * g_ms / max(g_n, 1), 2),
-                     "measured": "CUDA events around each launch, instrumented pass of the same "
-                                 "steps (warm-up + steps) right after the timed region",
-                     "algorithmic": "2*M*N*K per GEMM launch (M > 128), summed over the steps",
-                     "peak_source": peak_src,
-                     },
+        "roofline": head,
         "rooflines": {
-            "serialised": {"gemm_tflops": iso.get("gemm"), "attention_tflops": iso.get("attention"),
-                           "gemm_stream_gbs": iso.get("gemm_stream"), "expand_gbs": iso.get("expand")},
-            "attention": {"bound": "tensor", "kernel": "k_attn_fa (+ split-KV merge)",
-                          "achieved": round(a_fl / (a_ms * 1e-3) / 1e12, 2) if a_ms else None,
-                          "unit": "TFLOP/s", "peak": peak,
-                          "frac": round(a_fl / (a_ms * 1e-3) / 1e12 / peak, 4) if a_ms else None,
-                          "launches": a_n},
-            "gemm_weight_streaming": {
-                "bound": "hbm", "kernel": "k_gemm_tc (+ split-K reduce), M <= 128 (new-input prefill, K7)",
-                "achieved": round(s_by / (s_ms * 1e-3) / 1e9, 1) if s_ms else None, "unit": "GB/s",
-                "peak": hbm, "frac": round(s_by / (s_ms * 1e-3) / 1e9 / hbm, 4) if s_ms else None,
-                "launches": s_n, "algorithmic": "weights N*K*2 + A M*K*2 + C M*N*4 bytes per launch"},
-            "expand": {"bound": "hbm", "kernel": "k_expand (K5)",
-                       "achieved": round(e_by / (e_ms * 1e-3) / 1e9, 1) if e_ms else None,
-                       "unit": "GB/s", "peak": hbm,
-                       "frac": round(e_by / (e_ms * 1e-3) / 1e9 / hbm, 4) if e_ms else None,
-                       "launches": e_n},
+            **{k: v for k, v in roof.items() if k != dominant},
             "h2d_load": {"bound": "pcie", "kernel": "cudaMemcpyAsync pinned->device (K4)",
-                         "achieved": round(st["h2d_bytes"] / (st["h2d_ms"] * 1e-3) / 1e9, 2),
-                         "unit": "GB/s", "peak": round(b_h2d / 1e9, 2),
-                         "peak_source": "measured 256 MiB pinned H2D copy on this box"},
+                         "achieved": h2d_gbs, "unit": "GB/s", "peak": round(b_h2d / 1e9, 2),
+                         "frac": round(h2d_gbs / (b_h2d / 1e9), 4),
+                         "peak_source": "measured 256 MiB pinned H2D copy on this box",
+                         "note": "the restore's binding resource: TTFT = load stream + tail"},
             "recompute_stream": {"bound": "tensor", "achieved": round(
-                st["recompute_flops"] / (st["compute_ms"] * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+                st["recompute_flops"] / (st["compute_ms"] * 1e-3) / 1e12, 2) if st["recompute_flops"] else None,
+                "unit": "TFLOP/s",
                 "note": "algorithmic pyramid flops / recompute-stream makespan (shares SMs with the "
                         "new-input prefill and expand streams)"},
             **({"estimator_decode_fold": est["fold"], "selector": est["select"]} if est else {}),

@@ -68,48 +68,66 @@ EcCode ec_build_code(const uint64_t* hist) {
   return c;
 }
 
-std::vector<uint8_t> ec_encode_host(const uint16_t* x, uint64_t n, const EcCode& code) {
-  const uint64_t chunks = (n + kEcChunk - 1) / kEcChunk;
-  std::vector<uint32_t> lane_off(chunks * 32);
-  uint64_t words = 0;
+// Fills the chunk base table and lane counts of an image from per-stream
+// word counts (stream t = chunk * 32 + lane); returns the absolute word
+// offset of every stream and the total words.
+static std::vector<uint32_t> ec_offsets(const std::vector<uint32_t>& words, uint64_t chunks, uint32_t* base,
+                                        uint8_t* cnt, uint64_t* total) {
+  std::vector<uint32_t> off(chunks * 32);
+  uint64_t w = 0;
   for (uint64_t ch = 0; ch < chunks; ++ch) {
-    const uint64_t base = ch * kEcChunk, cnt = std::min<uint64_t>(kEcChunk, n - base);
+    base[ch] = uint32_t(w);
     for (int lane = 0; lane < 32; ++lane) {
-      uint64_t bits = 0;
-      for (uint64_t j = uint64_t(lane); j < cnt; j += 32) bits += code.len[(x[base + j] >> 7) & 0xFF];
-      lane_off[ch * 32 + uint64_t(lane)] = uint32_t(words);
-      words += (bits + 31) / 32;
+      const uint32_t k = words[ch * 32 + uint64_t(lane)];
+      off[ch * 32 + uint64_t(lane)] = uint32_t(w);
+      cnt[ch * 32 + uint64_t(lane)] = uint8_t(k);
+      w += k;
     }
   }
+  base[chunks] = uint32_t(w);
+  *total = w;
+  return off;
+}
+
+std::vector<uint8_t> ec_encode_host(const uint16_t* x, uint64_t n, const EcCode& code) {
+  const uint64_t chunks = (n + kEcChunk - 1) / kEcChunk;
+  std::vector<uint32_t> words(chunks * 32, 0);
+  for (uint64_t t = 0; t * kEcLaneSyms < n; ++t) {
+    uint64_t bits = 0;
+    for (uint64_t j = t * kEcLaneSyms; j < std::min<uint64_t>(n, (t + 1) * kEcLaneSyms); ++j)
+      bits += code.len[(x[j] >> 7) & 0xFF];
+    words[t] = uint32_t((bits + 31) / 32);
+  }
+  uint64_t total_words = 0;
+  for (auto k : words) total_words += k;
   EcHeader h;
   size_t total = 0;
-  ec_layout(n, words, &h, &total);
+  ec_layout(n, total_words, &h, &total);
   std::vector<uint8_t> out(total, 0);
   std::memcpy(out.data(), &h, sizeof h);
-  std::memcpy(out.data() + sizeof h, lane_off.data(), lane_off.size() * 4);
+  uint64_t tw = 0;
+  const std::vector<uint32_t> off =
+      ec_offsets(words, chunks, reinterpret_cast<uint32_t*>(out.data() + h.base_off), out.data() + h.cnt_off, &tw);
   uint8_t* sm = out.data() + h.sm_off;
   uint32_t* ex = reinterpret_cast<uint32_t*>(out.data() + h.exp_off);
-  for (uint64_t ch = 0; ch < chunks; ++ch) {
-    const uint64_t base = ch * kEcChunk, cnt = std::min<uint64_t>(kEcChunk, n - base);
-    for (int lane = 0; lane < 32; ++lane) {
-      uint32_t* o = ex + lane_off[ch * 32 + uint64_t(lane)];
-      uint64_t acc = 0;
-      int nb = 0;
-      for (uint64_t j = uint64_t(lane); j < cnt; j += 32) {
-        const uint32_t v = x[base + j];
-        sm[base + j] = uint8_t(((v >> 8) & 0x80u) | (v & 0x7Fu));
-        const uint32_t e = (v >> 7) & 0xFF;
-        const int l = code.len[e];
-        acc |= uint64_t(code.code[e]) << (64 - nb - l);
-        nb += l;
-        if (nb >= 32) {
-          *o++ = uint32_t(acc >> 32);
-          acc <<= 32;
-          nb -= 32;
-        }
+  for (uint64_t t = 0; t * kEcLaneSyms < n; ++t) {
+    uint32_t* o = ex + off[t];
+    uint64_t acc = 0;
+    int nb = 0;
+    for (uint64_t j = t * kEcLaneSyms; j < std::min<uint64_t>(n, (t + 1) * kEcLaneSyms); ++j) {
+      const uint32_t v = x[j];
+      sm[j] = uint8_t(((v >> 8) & 0x80u) | (v & 0x7Fu));
+      const uint32_t e = (v >> 7) & 0xFF;
+      const int l = code.len[e];
+      acc |= uint64_t(code.code[e]) << (64 - nb - l);
+      nb += l;
+      if (nb >= 32) {
+        *o++ = uint32_t(acc >> 32);
+        acc <<= 32;
+        nb -= 32;
       }
-      if (nb > 0) *o = uint32_t(acc >> 32);
     }
+    if (nb > 0) *o = uint32_t(acc >> 32);
   }
   return out;
 }
@@ -118,18 +136,21 @@ void ec_decode_host(const uint8_t* blob, const uint16_t* lut, uint16_t* out) {
   EcHeader h;
   std::memcpy(&h, blob, sizeof h);
   if (h.magic != kEcMagic) fail(KRUL_E_STATE_CORRUPTION, "coded KV blob has a bad header");
-  const uint32_t* lane_off = reinterpret_cast<const uint32_t*>(blob + sizeof h);
+  const uint32_t* base = reinterpret_cast<const uint32_t*>(blob + h.base_off);
+  const uint8_t* cnt = blob + h.cnt_off;
   const uint8_t* sm = blob + h.sm_off;
   const uint32_t* ex = reinterpret_cast<const uint32_t*>(blob + h.exp_off);
   const uint64_t n = h.n_elems;
   auto work = [&](uint64_t c0, uint64_t c1) {
     for (uint64_t ch = c0; ch < c1; ++ch) {
-      const uint64_t base = ch * kEcChunk, cnt = std::min<uint64_t>(kEcChunk, n - base);
+      uint32_t w = base[ch];
       for (int lane = 0; lane < 32; ++lane) {
-        const uint32_t* p = ex + lane_off[ch * 32 + uint64_t(lane)];
+        const uint64_t e0 = ch * kEcChunk + uint64_t(lane) * kEcLaneSyms;
+        const uint32_t* p = ex + w;
+        w += cnt[ch * 32 + uint64_t(lane)];
         uint64_t buf = 0;
         int have = 0;
-        for (uint64_t j = uint64_t(lane); j < cnt; j += 32) {
+        for (uint64_t j = e0; j < std::min<uint64_t>(n, e0 + kEcLaneSyms); ++j) {
           if (have < kEcMaxLen) {
             buf |= uint64_t(*p++) << (32 - have);
             have += 32;
@@ -138,15 +159,15 @@ void ec_decode_host(const uint8_t* blob, const uint16_t* lut, uint16_t* out) {
           const int l = int(e >> 8);
           buf <<= l;
           have -= l;
-          const uint32_t s = sm[base + j];
-          out[base + j] = uint16_t(((s & 0x80u) << 8) | ((e & 0xFFu) << 7) | (s & 0x7Fu));
+          const uint32_t s = sm[j];
+          out[j] = uint16_t(((s & 0x80u) << 8) | ((e & 0xFFu) << 7) | (s & 0x7Fu));
         }
       }
     }
   };
   const uint64_t chunks = h.n_chunks;
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  if (chunks < 16 || hw == 1) {
+  if (chunks < 64 || hw == 1) {
     work(0, chunks);
     return;
   }
@@ -205,21 +226,30 @@ void snapshot_encode(Ctx& c, Snapshot& s, const char* dev_raw, cudaStream_t st) 
   if (!hw.empty())
     KB_CUDA(cudaMemcpyAsync(hw.data(), words, hw.size() * 4, cudaMemcpyDeviceToHost, st));
   KB_CUDA(cudaStreamSynchronize(st));
-  // layout of the coded image (blobs 256-B aligned, like the raw store)
+  // layout of the coded image (blobs 256-B aligned, like the raw store):
+  // per blob the chunk base table + lane counts (host, from the word
+  // counts), and the absolute stream offsets the encode kernel writes at
   std::vector<EcHeader> hdr(s.blobs.size());
+  std::vector<std::vector<uint8_t>> tables(s.blobs.size());
+  std::vector<uint32_t> offs(chunks_total * 32);
   size_t off = 0;
   for (size_t bi = 0; bi < s.blobs.size(); ++bi) {
     auto& b = s.blobs[bi];
     const uint64_t n = b.bytes / 2;
     const uint64_t ch = (n + kEcChunk - 1) / kEcChunk;
+    std::vector<uint32_t> wv(hw.begin() + int64_t(chunk0[bi] * 32), hw.begin() + int64_t((chunk0[bi] + ch) * 32));
     uint64_t w = 0;
-    for (uint64_t i = 0; i < ch * 32; ++i) {
-      const uint32_t k = hw[chunk0[bi] * 32 + i];
-      hw[chunk0[bi] * 32 + i] = uint32_t(w);  // exclusive scan in place
-      w += k;
-    }
+    for (auto k : wv) w += k;
     size_t total = 0;
     ec_layout(n, w, &hdr[bi], &total);
+    // header + base table + counts: bytes [0, sm_off) of the image
+    tables[bi].assign(hdr[bi].sm_off, 0);
+    std::memcpy(tables[bi].data(), &hdr[bi], sizeof(EcHeader));
+    uint64_t tw = 0;
+    const std::vector<uint32_t> o = ec_offsets(
+        wv, ch, reinterpret_cast<uint32_t*>(tables[bi].data() + hdr[bi].base_off),
+        tables[bi].data() + hdr[bi].cnt_off, &tw);
+    std::copy(o.begin(), o.end(), offs.begin() + int64_t(chunk0[bi] * 32));
     b.coff = off;
     b.cbytes = n ? total : 0;
     b.ec_chunks = uint32_t(ch);
@@ -228,29 +258,28 @@ void snapshot_encode(Ctx& c, Snapshot& s, const char* dev_raw, cudaStream_t st) 
   const size_t ctotal = std::max<size_t>(off, 256);
   char* img = static_cast<char*>(d_img.ensure(ctotal));
   KB_CUDA(cudaMemsetAsync(img, 0, ctotal, st));
-  // header + lane table per blob, staged through pinned memory
+  // tables + stream offsets, staged through pinned memory
   PinnedBuf meta;
-  size_t meta_bytes = 0;
-  for (size_t bi = 0; bi < s.blobs.size(); ++bi)
-    meta_bytes += sizeof(EcHeader) + size_t(s.blobs[bi].ec_chunks) * 128;
+  size_t meta_bytes = offs.size() * 4;
+  for (const auto& t : tables) meta_bytes += t.size();
   char* mp = static_cast<char*>(meta.ensure(std::max<size_t>(meta_bytes, 64)));
-  size_t mo = 0;
+  std::memcpy(mp, offs.data(), offs.size() * 4);
+  uint32_t* d_offs = static_cast<uint32_t*>(d_words.p);  // reuse: same size as the word counts
+  if (!offs.empty()) KB_CUDA(cudaMemcpyAsync(d_offs, mp, offs.size() * 4, cudaMemcpyHostToDevice, st));
+  size_t mo = offs.size() * 4;
   for (size_t bi = 0; bi < s.blobs.size(); ++bi) {
     const auto& b = s.blobs[bi];
     if (!b.cbytes) continue;
-    const size_t nb = sizeof(EcHeader) + size_t(b.ec_chunks) * 128;
-    std::memcpy(mp + mo, &hdr[bi], sizeof(EcHeader));
-    std::memcpy(mp + mo + sizeof(EcHeader), hw.data() + chunk0[bi] * 32, size_t(b.ec_chunks) * 128);
-    KB_CUDA(cudaMemcpyAsync(img + b.coff, mp + mo, nb, cudaMemcpyHostToDevice, st));
-    mo += nb;
+    std::memcpy(mp + mo, tables[bi].data(), tables[bi].size());
+    KB_CUDA(cudaMemcpyAsync(img + b.coff, mp + mo, tables[bi].size(), cudaMemcpyHostToDevice, st));
+    mo += tables[bi].size();
   }
   for (size_t bi = 0; bi < s.blobs.size(); ++bi) {
     const auto& b = s.blobs[bi];
     if (!b.cbytes) continue;
     char* base = img + b.coff;
     launch_ec_encode(st, dev_raw + b.off, int64_t(b.bytes / 2), reinterpret_cast<const uint32_t*>(dc),
-                     reinterpret_cast<const uint8_t*>(dc + 1024),
-                     reinterpret_cast<const uint32_t*>(base + sizeof(EcHeader)),
+                     reinterpret_cast<const uint8_t*>(dc + 1024), d_offs + chunk0[bi] * 32,
                      reinterpret_cast<uint8_t*>(base + hdr[bi].sm_off),
                      reinterpret_cast<uint32_t*>(base + hdr[bi].exp_off));
   }

@@ -224,8 +224,11 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
     const auto& b = snap.blobs[bi];
     KB_CUDA(cudaStreamWaitEvent(c.s_exp, copied[bi], 0));
-    if (snap.coded && b.cbytes)
+    if (snap.coded && b.cbytes) {
+      cudaEvent_t kt0 = kt_begin(c, c.s_exp);
       launch_ec_decode(c.s_exp, cstg + b.coff, int64_t(b.ec_chunks), snap.lut_dev.as<uint16_t>(), stg + b.off);
+      kt_end(c, c.s_exp, kt0, KT_DECODE, 0.0, double(b.cbytes) + double(b.bytes));  // coded read + raw write
+    }
     for (int o : b.owners) {
       if (o < 0) continue;
       launch_expand(c, c.s_exp, stg + b.off, b.start, L, conv, o, p[size_t(o)]);

@@ -135,7 +135,8 @@ struct Est;
 // are attached so the bench derives achieved TFLOP/s and GB/s per kernel
 // class from the same timed step.
 enum KTag { KT_GEMM = 0, KT_ATTN = 1, KT_EXPAND = 2, KT_FOLD_DECODE = 3, KT_FOLD_PREFILL = 4,
-            KT_SELECT = 5, KT_COMPRESS = 6, KT_GEMM_STREAM = 7, KT_NTAGS = 8 };
+            KT_SELECT = 5, KT_COMPRESS = 6, KT_GEMM_STREAM = 7, KT_DECODE = 8, KT_LOGITS = 9,
+            KT_NTAGS = 10 };
 struct KTime {
   bool on = false;
   struct Rec {

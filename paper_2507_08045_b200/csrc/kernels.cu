@@ -363,11 +363,13 @@ void launch_logits(const Ctx& c, cudaStream_t s, const float* h_last, float* log
   const unsigned blocks = unsigned((V + 7) / 8);
   if (c.cfg.dtype == KRUL_BF16 && c.cfg.d % 256 == 0 && (c.cfg.d == 4096 || c.cfg.d == 8192)) {
     const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count > 0 ? c.sm_count : 148) * 8));
+    cudaEvent_t kt0 = kt_begin(c, s);
     if (c.cfg.d == 4096)
       k_logits_vec<16><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
     else
       k_logits_vec<32><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
     KB_LAUNCH();
+    kt_end(c, s, kt0, KT_LOGITS, 2.0 * double(V) * c.cfg.d, double(V) * c.cfg.d * 2.0 + double(V) * 4.0);
     return;
   }
   if (c.cfg.dtype == KRUL_BF16)

@@ -8,20 +8,29 @@
 
 namespace kb {
 
-constexpr int kEcChunk = 8192;  // elements per chunk (32 lanes x 256)
-constexpr int kEcMaxLen = 12;   // longest code; LUT = 2^12 entries
+constexpr int kEcLaneSyms = 128;                // elements per lane stream
+constexpr int kEcChunk = 32 * kEcLaneSyms;      // elements per chunk (one warp)
+constexpr int kEcMaxLen = 12;                   // longest code; LUT = 2^12 entries
+constexpr int kEcMaxLaneWords = (kEcLaneSyms * kEcMaxLen + 31) / 32;  // 48 (fits the u8 counts)
 
+// Coded blob image (all offsets in bytes from the image start, 16-B aligned):
+//   EcHeader | chunk base u32[n_chunks + 1] (word offset of each chunk's
+//   first lane stream) | lane word counts u8[n_chunks][32] | sign+mantissa
+//   bytes [n_elems] | exponent words u32[exp_words] + 1 pad word.
+// Lane j of a chunk codes the chunk's elements [128 j, 128 j + 128) MSB-first;
+// its stream starts at base[chunk] + sum of the counts of lanes < j.
 struct EcHeader {
-  uint32_t magic;      // 'E','C','1','6'
+  uint32_t magic;      // 'E','C','1','7'
   uint32_t n_elems;
   uint32_t n_chunks;
-  uint32_t sm_off;     // byte offset of the sign+mantissa plane
-  uint32_t exp_off;    // byte offset of the exponent words
+  uint32_t base_off;   // chunk base table
+  uint32_t cnt_off;    // lane word counts
+  uint32_t sm_off;     // sign+mantissa plane
+  uint32_t exp_off;    // exponent words
   uint32_t exp_words;  // words in the exponent streams (+1 pad word follows)
-  uint32_t pad[2];
 };
 static_assert(sizeof(EcHeader) == 32, "EcHeader is 32 bytes");
-constexpr uint32_t kEcMagic = 0x36314345u;  // "EC16"
+constexpr uint32_t kEcMagic = 0x37314345u;  // "EC17"
 
 // Canonical, length-limited (<= kEcMaxLen) Huffman code of an exponent
 // histogram: code[s] (right-aligned, len[s] bits), len 0 = absent symbol,
@@ -40,10 +49,11 @@ inline void ec_layout(uint64_t n, uint64_t exp_words, EcHeader* h, size_t* total
   h->magic = kEcMagic;
   h->n_elems = uint32_t(n);
   h->n_chunks = uint32_t(chunks);
-  h->sm_off = uint32_t(ec_align16(sizeof(EcHeader) + 4 * 32 * chunks));
+  h->base_off = uint32_t(sizeof(EcHeader));
+  h->cnt_off = uint32_t(ec_align16(h->base_off + 4 * (chunks + 1)));
+  h->sm_off = uint32_t(ec_align16(h->cnt_off + 32 * chunks));
   h->exp_off = uint32_t(ec_align16(h->sm_off + n));
   h->exp_words = uint32_t(exp_words);
-  h->pad[0] = h->pad[1] = 0;
   *total = ec_align16(size_t(h->exp_off) + 4 * (size_t(exp_words) + 1));
 }
 // Host codec (tests, inspection, container save): identical bytes / values
@@ -52,7 +62,9 @@ std::vector<uint8_t> ec_encode_host(const uint16_t* x, uint64_t n, const EcCode&
 void ec_decode_host(const uint8_t* blob, const uint16_t* lut, uint16_t* out);
 
 void launch_exp_hist(cudaStream_t s, const void* x, int64_t n, unsigned long long* hist);
+// words per (chunk, lane) stream -> words[chunk * 32 + lane]
 void launch_ec_lane_words(cudaStream_t s, const void* x, int64_t n, const uint8_t* len, uint32_t* words);
+// lane_off: absolute word offset of every (chunk, lane) stream
 void launch_ec_encode(cudaStream_t s, const void* x, int64_t n, const uint32_t* code, const uint8_t* len,
                       const uint32_t* lane_off, uint8_t* sm, uint32_t* ex);
 void launch_ec_decode(cudaStream_t s, const void* blob, int64_t n_chunks, const uint16_t* lut, void* out);

@@ -35,20 +35,25 @@ def bf16_bits(a):
     return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 8191, 8192, 8193, 3 * 8192 + 77])
+@pytest.mark.parametrize("n", [0, 1, 31, 63, 64, 65, 2047, 2048, 2049, 3 * 2048 + 77, 5 * 8192 + 5])
 def test_gaussian_roundtrip_and_layout(K, n):
     x = bf16_bits(np.random.default_rng(n).standard_normal(n) * 0.7)
     img, dec = roundtrip(K, x)
     assert np.array_equal(dec, x)
-    magic, ne, nch, sm_off, exp_off, words = struct.unpack("<6I", img[:24].tobytes())
-    assert magic == 0x36314345 and ne == n and nch == (n + 8191) // 8192
+    magic, ne, nch, base_off, cnt_off, sm_off, exp_off, words = struct.unpack("<8I", img[:32].tobytes())
+    assert magic == 0x37314345 and ne == n and nch == (n + 4095) // 4096
+    assert base_off == 32 and cnt_off >= base_off + 4 * (nch + 1)
     assert sm_off % 16 == 0 and exp_off % 16 == 0 and exp_off >= sm_off + n
     assert img.size == ((exp_off + 4 * (words + 1) + 15) // 16) * 16
+    base = np.frombuffer(img[base_off:base_off + 4 * (nch + 1)].tobytes(), np.uint32)
+    cnt = img[cnt_off:cnt_off + 32 * nch].astype(np.int64)
+    assert base[0] == 0 and base[-1] == words and cnt.sum() == words and cnt.max(initial=0) <= 48
+    assert np.array_equal(np.diff(base), cnt.reshape(nch, 32).sum(axis=1))
     # sign+mantissa plane is the raw low bits
     sm = img[sm_off:sm_off + n]
     assert np.array_equal(sm, (((x >> 8) & 0x80) | (x & 0x7F)).astype(np.uint8))
-    if n >= 8192:  # ~10.6 of 16 bits per element on Gaussian data
-        assert img.size < 0.75 * 2 * n
+    if n >= 8192:  # ~10.7 of 16 bits per element on Gaussian data
+        assert img.size < 0.72 * 2 * n
 
 
 def test_all_exponents_force_length_limit(K):

@@ -22,7 +22,7 @@ from paper_2507_08045_b200 import native as K  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="llama3-8b-8k")
-    ap.add_argument("--rc", type=float, default=0.06)
+    ap.add_argument("--rc", type=float, default=0.0)
     ap.add_argument("--steps", type=int, default=1)
     args = ap.parse_args()
     spec = CONFIGS[args.config]
