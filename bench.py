@@ -49,6 +49,8 @@ NCU_FFN1_DRAM_BYTES = 276_462_080
 NCU_TRAFFIC = {
     "gemm": (NCU_FFN1_DRAM_BYTES, 1078 * 4096 * 2 + 28672 * 4096 * 2 + 1078 * 14336 * 2,
              "profiles/r01c/SUMMARY.md (FFN1 pair GEMM, M=1078 N=28672 K=4096)"),
+    "gemm_stream": (241502208, 28672 * 4096 * 2 + 128 * 4096 * 2 + 128 * 14336 * 2,
+                    "profiles/r01d/ncu_gstream.md (new-input FFN1, M=128 N=28672 K=4096, SwiGLU epilogue)"),
 }
 
 METRIC = ("restoration TTFT p50 (ms) @8K history; conversations restored/sec at 1/2/4/8 GPU")

@@ -40,7 +40,14 @@ Ctx* ctx_create(int device, const krul_model_desc& desc) {
       }
     }
     KB_CUDA(cudaStreamCreateWithFlags(&c->s_est, cudaStreamNonBlocking));
-    KB_CUDA(cudaStreamCreateWithFlags(&c->s_exp, cudaStreamNonBlocking));
+    {
+      // decode + expand of the blob the load stream just landed gate the
+      // new-input prefill of that layer: their CTAs go first when SMs free up
+      int lo = 0, hi = 0;
+      KB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const char* ev = std::getenv("KRUL_EXP_PRIO");
+      KB_CUDA(cudaStreamCreateWithPriority(&c->s_exp, cudaStreamNonBlocking, ev && ev[0] == 'l' ? lo : hi));
+    }
     KB_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     // RoPE table: angles in double, cast to float (engine.cpp:131-136).
     const int half = cfg.hd / 2;

@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) k_logits_vec(const float* __restrict__ h,
                                                     const bf16* __restrict__ wT, int V,
                                                     float* __restrict__ out) {
   constexpr int D = 256 * NV;
-  __shared__ float hs[D];
+  __shared__ __align__(16) float hs[D];
   for (int i = threadIdx.x; i < D; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -343,18 +343,23 @@ __global__ void __launch_bounds__(256) k_logits_vec(const float* __restrict__ h,
     uint4 x[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) x[j] = __ldg(w + lane + 32 * j);
-    float acc = 0.f;
+    // h as two float4 shared loads per weight vector (the scalar form was an
+    // 8-way bank conflict: lanes 32 B apart)
+    float acc0 = 0.f, acc1 = 0.f;
+    const float4* h4 = reinterpret_cast<const float4*>(hs);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int k0 = (lane + 32 * j) * 8;
+      const int k4 = (lane + 32 * j) * 2;
+      const float4 ha = h4[k4], hb = h4[k4 + 1];
       const uint32_t u[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[q]));
-        acc += hs[k0 + 2 * q] * f.x + hs[k0 + 2 * q + 1] * f.y;
-      }
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[0]));
+      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[1]));
+      const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[2]));
+      const float2 f3 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[3]));
+      acc0 += ha.x * f0.x + ha.y * f0.y + ha.z * f1.x + ha.w * f1.y;
+      acc1 += hb.x * f2.x + hb.y * f2.y + hb.z * f3.x + hb.w * f3.y;
     }
-    acc = warp_sum(acc);
+    float acc = warp_sum(acc0 + acc1);
     if (lane == 0) out[v] = acc;
   }
 }
@@ -362,7 +367,19 @@ void launch_logits(const Ctx& c, cudaStream_t s, const float* h_last, float* log
   const int V = c.cfg.V;
   const unsigned blocks = unsigned((V + 7) / 8);
   if (c.cfg.dtype == KRUL_BF16 && c.cfg.d % 256 == 0 && (c.cfg.d == 4096 || c.cfg.d == 8192)) {
-    const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count > 0 ? c.sm_count : 148) * 8));
+    // exactly one wave of resident CTAs (grid-stride over the rows): a
+    // second partial wave left a third of the GEMV at a third of the SMs
+    static int per_sm[2] = {0, 0};
+    const int vi = c.cfg.d == 4096 ? 0 : 1;
+    if (!per_sm[vi]) {
+      if (vi == 0)
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], k_logits_vec<16>, 256, 0));
+      else
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], k_logits_vec<32>, 256, 0));
+      per_sm[vi] = std::max(per_sm[vi], 1);
+    }
+    const unsigned grid =
+        unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count > 0 ? c.sm_count : 148) * per_sm[vi]));
     cudaEvent_t kt0 = kt_begin(c, s);
     if (c.cfg.d == 4096)
       k_logits_vec<16><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
