@@ -320,7 +320,10 @@ int krul_restore_and_prefill(krul_ctx* ctx, krul_conv* conv,
                              float* logits, krul_restore_stats* stats,
                              double* ttft_ms);
 
-/* Per-layer timeline of the last restore (ms from launch, CUDA events):
+/* Record the per-layer timeline events in the restore DAG (default on). */
+int krul_set_timeline(krul_ctx* ctx, int on);
+/* Per-layer timeline of the last restore (ms from launch, CUDA events; zeros
+ * when krul_set_timeline is off):
  * compute[l] = recompute of layer l done, load[l] = layer l expanded,
  * new_prefill[l] = new-input prefill of layer l done (0 without one). */
 int krul_restore_timeline(krul_ctx* ctx, double* compute, double* load,
@@ -359,6 +362,12 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps,
  * 3 = tanh(acc + bias), 4 = swiglu over column pairs (C is [M, N/2]). */
 /* Restore scheduling: 1 (default) = new-input prefill concurrent with the
  * recompute on its own stream; 0 = serialised behind it. */
+/* Restore + prefill DAG: 1 folds the pyramid recompute rows into the
+ * new-input prefill's layer steps (one weight pass per layer, each step
+ * behind its layer's loaded suffix); 0 (default) runs the recompute on its
+ * own stream ahead of the loads. Restore without new input always uses the
+ * separate recompute stream. */
+int krul_set_fused_recompute(krul_ctx* ctx, int on);
 int krul_set_concurrency(krul_ctx* ctx, int two_stream);
 
 /* ---- measurement support (not on the reference's interface) ----------

@@ -1266,6 +1266,18 @@ int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* by
 // Restore scheduling mode: 1 (default) runs the new-input prefill on its own
 // stream, concurrent with the recompute; 0 serialises it behind the
 // recompute (kernel-efficiency measurements without SM sharing).
+int krul_set_timeline(krul_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->timeline = on != 0;
+  });
+}
+int krul_set_fused_recompute(krul_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->fused = on != 0;
+  });
+}
 int krul_set_concurrency(krul_ctx* ctx, int two_stream) {
   return guard([&] {
     need(ctx, "ctx");

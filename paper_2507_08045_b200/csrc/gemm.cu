@@ -333,7 +333,7 @@ __device__ __forceinline__ void epi_qkv(const Epi& e, uint32_t tbase, int64_t ro
   const int lane = threadIdx.x & 31;
   const int64_t r = row0 + lane;
   const bool rok = r < M;
-  const int64_t pos = kv.pos0 + r;
+  const int64_t pos = kv.pos(r);
   const int nq = kv.H * kv.hd, nkv = kv.Hkv * kv.hd, half = kv.hd / 2;
   bf16* page = rok ? reinterpret_cast<bf16*>(kv.pool + int64_t(kv.pt[pos / kPageTokens]) * kv.page_bytes)
                    : nullptr;
@@ -965,7 +965,7 @@ __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P,
       const int rr = ty + 8 * j;
       const int64_t r = r0 + rr;
       if (r >= M || (isq && r >= kv.q_rows)) continue;
-      const int64_t pos = kv.pos0 + r;
+      const int64_t pos = kv.pos(r);
       const float x0 = t[rr][tx & ~1], x1 = t[rr][tx | 1];
       const float cs = kv.cosT[pos * half + i], sn = kv.sinT[pos * half + i];
       const float y = (tx & 1) ? (x0 * sn + x1 * cs) : (x0 * cs - x1 * sn);
@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P,
     for (int u = 0; u < 8; ++u) {
       const int64_t r = r0 + tg + u;
       if (r >= M) break;
-      const int64_t pos = kv.pos0 + r;
+      const int64_t pos = kv.pos(r);
       bf16* page = reinterpret_cast<bf16*>(kv.pool + int64_t(kv.pt[pos / kPageTokens]) * kv.page_bytes);
       page[int64_t(kv.Hkv) * kPageTokens * kv.hd + (int64_t(g) * kv.hd + t0 + d) * kPageTokens +
            pos % kPageTokens] = __float2bfloat16_rn(t[tg + u][d]);

@@ -19,9 +19,23 @@ void weights_upload_f32(Ctx& c, const float* w, int64_t n);
 void weights_init_device(Ctx& c, uint64_t seed);
 Conv* conv_create(Ctx& c, int64_t capacity);
 WS ws_get(Ctx& c, int set, int64_t rows);
+// Fused recompute + new-input step of one layer: rows [0, n_new) are the new
+// input (at pos0 + r), rows [n_new, rows) the history prefix being recomputed
+// (positions 0..); rec_out of them feed the next layer. The step waits for
+// `waits` (the layer's loaded suffix) before it starts; `computed` is
+// recorded once the layer's recomputed K/V are in the pages.
+struct FusedSeg {
+  int64_t n_new = 0, rec_out = 0;
+  const cudaEvent_t* waits = nullptr;
+  int n_waits = 0;
+  const Mark* computed = nullptr;
+};
 void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const float* h_in,
                    int64_t rows, int64_t pos0, int64_t out_rows, float* h_out,
-                   const AttnArgs* cap);
+                   const AttnArgs* cap, const FusedSeg* fs = nullptr);
+void forward_fused(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_new, int64_t n,
+                   int64_t L, const int32_t* d_hist, const std::vector<int64_t>& p, float* d_logits,
+                   const Mark* loaded, const Mark* computed, const Mark* layer_done, const Mark* compute_end);
 void check_tokens(const Ctx& c, const int32_t* t, int64_t n);
 int32_t* upload_tokens(Ctx& c, cudaStream_t s, const int32_t* t, int64_t n, DevBuf& buf);
 void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_tok, int64_t n,

@@ -255,10 +255,15 @@ WS ws_get(Ctx& c, int set, int64_t rows) {
 // pages; attention + FFN for the leading out_rows rows -> h_out.
 void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const float* h_in,
                    int64_t rows, int64_t pos0, int64_t out_rows, float* h_out,
-                   const AttnArgs* cap) {
+                   const AttnArgs* cap, const FusedSeg* fs) {
   const Cfg& g = c.cfg;
   const LayerW& lw = c.L[size_t(l)];
   if (rows <= 0) return;
+  // the fused step waits for the layer's loaded suffix before it starts: a
+  // QKV GEMM launched early holds every SM's shared memory while the blob's
+  // decode + expand (the critical path) need them
+  if (fs)
+    for (int k = 0; k < fs->n_waits; ++k) KB_CUDA(cudaStreamWaitEvent(s, fs->waits[k], 0));
   launch_rmsnorm(c, s, h_in, rows, w.xn);
   Epi e;
   if (gemm_uses_tc(c, w.xn, g.d, lw.wqkv, g.d) && g.hd % 32 == 0) {
@@ -272,6 +277,10 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
     e.kv.hd = g.hd;
     e.kv.pos0 = pos0;
     e.kv.q_rows = out_rows;
+    if (fs) {
+      e.kv.seg_rows = fs->n_new;
+      e.kv.pos1 = 0;
+    }
     e.kv.cosT = c.rope_cos;
     e.kv.sinT = c.rope_sin;
     e.kv.q = w.q;
@@ -281,15 +290,30 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
     e.out = w.qkv;
     e.ldo = g.nqkv();
     gemm(c, s, rows, g.nqkv(), g.d, w.xn, g.d, lw.wqkv, g.d, e);
-    launch_rope_scatter(c, s, w.qkv, rows, pos0, out_rows, w.q, conv, l);
+    launch_rope_scatter(c, s, w.qkv, rows, pos0, out_rows, w.q, conv, l, fs ? fs->n_new : INT64_MAX, 0);
   }
+  if (fs && fs->computed) record_mark(*fs->computed, s);
   if (out_rows <= 0) return;
   AttnArgs a = cap ? *cap : AttnArgs{};
   a.part = w.part;
   a.q = w.q;
-  a.rows = out_rows;
+  a.rows = fs ? fs->n_new : out_rows;
   a.pos0 = pos0;
   a.out = w.attn;
+  if (fs) {
+    // recomputed rows first (their keys are this step's own), then the new
+    // rows once the layer's loaded suffix is in the pages
+    if (fs->rec_out > 0) {
+      AttnArgs ar{};
+      ar.part = w.part;
+      const size_t off = size_t(fs->n_new) * size_t(g.qd()) * c.esz;
+      ar.q = static_cast<const char*>(w.q) + off;
+      ar.rows = fs->rec_out;
+      ar.pos0 = 0;
+      ar.out = static_cast<char*>(w.attn) + off;
+      launch_attention(c, s, conv, l, ar);
+    }
+  }
   launch_attention(c, s, conv, l, a);
   Epi eo;
   eo.kind = Epi::RESID;
@@ -390,6 +414,45 @@ void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_
     if (layer_done) record_mark(layer_done[l], s);
     std::swap(hin, hout);
   }
+  launch_logits(c, s, hin + (n - 1) * g.d, d_logits);
+}
+
+// Restore + new-input prefill with the pyramid recompute folded into the
+// prefill's layer steps: layer l runs rows [new input | history prefix
+// [0, p_l)] through one norm + QKV GEMM (two position segments in the fused
+// RoPE/scatter epilogue), attends the recomputed rows over their own prefix,
+// waits for layer l's loaded suffix, attends the new rows over the whole
+// cache, and carries the new rows plus the p_{l+1} prefix rows the next layer
+// needs through the O and FFN GEMMs. Each layer's weights stream from HBM
+// once for both; the recompute rows fill the weight-bound small-M GEMMs.
+void forward_fused(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_new, int64_t n,
+                   int64_t L, const int32_t* d_hist, const std::vector<int64_t>& p, float* d_logits,
+                   const Mark* loaded, const Mark* computed, const Mark* layer_done,
+                   const Mark* compute_end) {
+  const Cfg& g = c.cfg;
+  const int64_t p0 = std::max<int64_t>(p[0], 0);
+  WS w = ws_get(c, set, n + p0);
+  AttnArgs cap{};
+  prepare_capture(c, s, n, L + n, L, cap);
+  launch_embed(c, s, d_new, n, w.h);
+  if (p0 > 0) launch_embed(c, s, d_hist, p0, w.h + n * g.d);
+  float* hin = w.h;
+  float* hout = w.h2;
+  for (int l = 0; l < g.N; ++l) {
+    const int64_t pl = p[size_t(l)], pn = l + 1 < g.N ? p[size_t(l + 1)] : 0;
+    const cudaEvent_t wl = loaded[l].dep;
+    FusedSeg fs;
+    fs.n_new = n;
+    fs.rec_out = pn;
+    fs.waits = &wl;
+    fs.n_waits = 1;
+    fs.computed = &computed[l];
+    AttnArgs a = capture_for_layer(c, cap, l);
+    layer_forward(c, s, w, conv, l, hin, n + pl, L, n + pn, hout, &a, &fs);
+    if (layer_done) record_mark(layer_done[l], s);
+    std::swap(hin, hout);
+  }
+  if (compute_end) record_mark(*compute_end, s);
   launch_logits(c, s, hin + (n - 1) * g.d, d_logits);
 }
 

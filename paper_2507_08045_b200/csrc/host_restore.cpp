@@ -237,6 +237,27 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     }
   }
   record_mark(ev_l_end, c.s_exp);
+  static const bool fused_env = [] {
+    const char* v = std::getenv("KRUL_FUSED");
+    return !(v && v[0] == '0');
+  }();
+  const bool fused = tp_new && fused_env && c.fused;
+  if (fused) {
+    // ---- K6 + K7 fused: the recompute rows ride in the new-input prefill's
+    // layer steps (forward_fused), one weight pass per layer
+    cudaStream_t sn = c.s_new;
+    KB_CUDA(cudaStreamWaitEvent(sn, tok_ready, 0));
+    conv.len = L;
+    forward_fused(c, sn, 1, conv, d_new, n_new, L, d_tok, p, d_logits, loaded, computed, newp, &ev_c_end);
+    record_mark(ev_end, sn);
+    KB_CUDA(cudaStreamWaitEvent(sc, ev_end.dep, 0));
+    KB_CUDA(cudaStreamWaitEvent(sc, ev_l_end.dep, 0));
+    KB_CUDA(cudaStreamWaitEvent(sc, ev_h2d_end.dep, 0));
+    if (lp) KB_CUDA(cudaMemcpyAsync(lp, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sc));
+    *h2d_out = h2d;
+    *expand_out = expand_bytes;
+    return;
+  }
   // ---- compute stream: K6 pyramid recompute
   if (p[0] > 0) {
     enqueue_partial(c, sc, conv, d_tok, p, false, computed);
@@ -315,7 +336,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   const bool same = G.snap_serial == snap.serial && G.conv == &conv && G.L == L && G.n_new == nn &&
                     G.kt_on == c.kt.on && G.logits == (lp != nullptr) &&
                     G.capture_probs == c.capture_probs && G.buf_gen == g_buf_gen.load() &&
-                    G.two_stream == c.two_stream;
+                    G.two_stream == c.two_stream && G.fused == c.fused && G.timeline == c.timeline;
   if (!same) {
     c.drop_graph();
     G.snap_serial = snap.serial;
@@ -326,10 +347,13 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     G.logits = lp != nullptr;
     G.capture_probs = c.capture_probs;
     G.two_stream = c.two_stream;
+    G.fused = c.fused;
+    G.timeline = c.timeline;
     G.ev.resize(size_t(5 + 3 * g.N));
-    for (auto& m : G.ev) {
+    for (size_t i = 0; i < G.ev.size(); ++i) {
+      auto& m = G.ev[i];
       KB_CUDA(cudaEventCreateWithFlags(&m.dep, cudaEventDisableTiming));
-      KB_CUDA(cudaEventCreate(&m.tim));
+      if (i < 5 || c.timeline) KB_CUDA(cudaEventCreate(&m.tim));  // per-layer timing on request
     }
     G.buf_gen = g_buf_gen.load();
   }
@@ -396,7 +420,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   c.tl_compute.assign(size_t(g.N), 0.0);
   c.tl_load.assign(size_t(g.N), 0.0);
   c.tl_new.assign(size_t(g.N), 0.0);
-  for (int l = 0; l < g.N; ++l) {
+  for (int l = 0; l < g.N && G.timeline; ++l) {
     float a = 0, b = 0, e = 0;
     KB_CUDA(cudaEventElapsedTime(&a, E[0], E[5 + l]));
     KB_CUDA(cudaEventElapsedTime(&b, E[0], E[5 + g.N + l]));

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <climits>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -223,6 +224,8 @@ struct Ctx {
     int capture_probs = -1;
     uint64_t buf_gen = 0;
     bool two_stream = true;
+    bool fused = false;
+    bool timeline = false;
     int seen = 0;  // eager runs with this key (capture on the second)
     cudaGraphExec_t exec = nullptr;
     uint64_t launches = 0;
@@ -231,6 +234,16 @@ struct Ctx {
   } rg;
   bool use_graphs = true;
   bool two_stream = true;  // new-input prefill concurrent with the recompute (krul_set_concurrency)
+  // restore + prefill DAG variant: the recompute rows ride in the new-input
+  // prefill's GEMMs layer by layer (one weight pass per layer) instead of a
+  // separate recompute stream (krul_set_fused_recompute). Measured slower on
+  // the bench workload, so off by default.
+  bool fused = false;
+  // per-layer timing events in the restore graph (computed / loaded /
+  // new-prefill timeline). On by default: measured, the graph without the
+  // per-layer external event-record nodes runs the restore 4-7 ms slower
+  // at r_c > 0 (the nodes keep the streams' kernels interleaved).
+  bool timeline = true;
   std::vector<double> tl_compute, tl_load, tl_new;
   double tl_h2d_ms = 0;
   std::vector<cudaEvent_t> ev_pool;
@@ -250,6 +263,10 @@ struct EpiKV {  // QKV epilogue: RoPE + paged K / V^T scatter + rotated Q
   int64_t page_bytes = 0;
   int H = 0, Hkv = 0, hd = 0;
   int64_t pos0 = 0, q_rows = 0;
+  // two row segments (fused recompute + new-input step): rows < seg_rows sit
+  // at pos0 + r, rows >= seg_rows at pos1 + (r - seg_rows)
+  int64_t seg_rows = INT64_MAX, pos1 = 0;
+  __host__ __device__ int64_t pos(int64_t r) const { return r < seg_rows ? pos0 + r : pos1 + (r - seg_rows); }
   const float* cosT = nullptr;  // [pos][hd/2]
   const float* sinT = nullptr;
   void* q = nullptr;  // [q_rows][H*hd] cdt
@@ -283,7 +300,8 @@ void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, 
 // qkv f32 [rows][(H+2Hkv)hd] -> rope, K/V^T into pages at [pos0, pos0+rows),
 // Q (roped, cdt) for rows < q_rows.
 void launch_rope_scatter(const Ctx& c, cudaStream_t s, const float* qkv, int64_t rows,
-                         int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer);
+                         int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer,
+                         int64_t seg_rows = INT64_MAX, int64_t pos1 = 0);
 struct DevBuf;
 struct AttnArgs {
   const void* q = nullptr;  // [rows][H*hd] cdt

@@ -118,10 +118,10 @@ static PageView page_view(const Ctx& c, const Conv& conv, int layer) {
 // :162-170 (K/V of every block row appended before attention).
 template <class T>
 __global__ void k_rope_scatter(const float* qkv, int64_t pos0, int64_t q_rows, T* q, PageView pv,
-                               const float* cosT, const float* sinT, int H) {
+                               const float* cosT, const float* sinT, int H, int64_t seg_rows, int64_t pos1) {
   const int64_t r = blockIdx.x;
   const int hd = pv.hd, Hkv = pv.Hkv, half = hd / 2;
-  const int64_t pos = pos0 + r;
+  const int64_t pos = r < seg_rows ? pos0 + r : pos1 + (r - seg_rows);
   const int nq = H * hd, nkv = Hkv * hd;
   const float* row = qkv + r * int64_t(nq + 2 * nkv);
   const float* cs = cosT + pos * half;
@@ -158,15 +158,16 @@ __global__ void k_rope_scatter(const float* qkv, int64_t pos0, int64_t q_rows, T
   }
 }
 void launch_rope_scatter(const Ctx& c, cudaStream_t s, const float* qkv, int64_t rows,
-                         int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer) {
+                         int64_t pos0, int64_t q_rows, void* q, const Conv& conv, int layer,
+                         int64_t seg_rows, int64_t pos1) {
   if (rows <= 0) return;
   PageView pv = page_view(c, conv, layer);
   if (c.cfg.dtype == KRUL_BF16)
     k_rope_scatter<<<unsigned(rows), 128, 0, s>>>(qkv, pos0, q_rows, (bf16*)q, pv, c.rope_cos,
-                                                  c.rope_sin, c.cfg.H);
+                                                  c.rope_sin, c.cfg.H, seg_rows, pos1);
   else
     k_rope_scatter<<<unsigned(rows), 128, 0, s>>>(qkv, pos0, q_rows, (float*)q, pv, c.rope_cos,
-                                                  c.rope_sin, c.cfg.H);
+                                                  c.rope_sin, c.cfg.H, seg_rows, pos1);
   KB_LAUNCH();
 }
 

@@ -326,6 +326,14 @@ class Context:
                                             mode, reps, C.byref(r), _p(tt)))
         return r.value, tt
 
+    def set_timeline(self, on: bool):
+        """Record per-layer timeline events in the restore DAG (diagnostic)."""
+        _check(lib().krul_set_timeline(self.h, int(bool(on))))
+
+    def set_fused_recompute(self, on: bool):
+        """Fold the recompute rows into the new-input prefill's layer steps (default off)."""
+        _check(lib().krul_set_fused_recompute(self.h, int(bool(on))))
+
     def set_concurrency(self, two_stream: bool):
         """Restore DAG mode: new-input prefill concurrent with the recompute (default)
         or serialised behind it."""

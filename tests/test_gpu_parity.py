@@ -715,3 +715,50 @@ def test_coded_store_restores_bit_exact(K, oracle, monkeypatch):
     # a raw store re-encoded later is the same code / image
     raw.encode()
     assert raw.coding() == cod.coding()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_fused_recompute_matches_separate_stream(K, oracle, dtype, monkeypatch):
+    """The fused DAG (recompute rows inside the new-input prefill's layer
+    steps) restores the same KV and logits as the separate recompute stream:
+    loaded spans bit-identical, recomputed spans and logits within the
+    f32 / bf16 tolerances; both against the oracle's restore + prefill."""
+    monkeypatch.setenv("KRUL_KV_POOL_CONVS", "6")
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    dt = K.KRUL_F32 if dtype == "f32" else K.KRUL_BF16
+    ocfg, om, cfg, ctx = make_pair(K, oracle, dt, **kw)
+    L = 517  # not page aligned: the segments share pages
+    hist = oracle.tokens(L, 11, 256)
+    new = oracle.tokens(48, 12, 256)
+    conv = ctx.conversation(1024)
+    ctx.prefill(conv, hist)
+    pairs = [(1, 2, 0.5)]
+    p = K.build_plan(L, 4, 0.35, pairs)
+    assert p[0] > 0
+    snap = K.KVSnapshot.compress(ctx, conv, pairs, p, L, K.MERGE_MEAN)
+    ctx.set_capture(False)
+    outs = {}
+    for fused in (True, False):
+        ctx.set_fused_recompute(fused)
+        cv = ctx.conversation(1024)
+        for _ in range(3):  # eager, capture, replay
+            lg, st, _ = ctx.restore_and_prefill(cv, hist, snap, new)
+        outs[fused] = (lg, [cv.kv(l, 0, L + 48) for l in range(4)])
+    ctx.set_fused_recompute(True)
+    (lf, kvf), (ls, kvs) = outs[True], outs[False]
+    for l in range(4):
+        a = int(p[l])
+        assert np.array_equal(kvf[l][0][:, a:L], kvs[l][0][:, a:L])  # loaded suffix
+        tol = 1e-4 if dtype == "f32" else None
+        for x, y in ((kvf[l][0], kvs[l][0]), (kvf[l][1], kvs[l][1])):
+            if tol:
+                assert np.abs(x - y).max() < tol
+            else:
+                assert rel_fro(x, y) < 2e-2
+    okv = om.prefill(hist).take_kv()
+    osnap = oracle.Snapshot(okv, ocfg, oracle.Strategy(pairs), p, L, mode=0)
+    want = om.prefill(np.concatenate([hist, new]), preload=om.restore(hist, osnap).suffix([0] * 4)).logits()
+    if dtype == "f32":
+        assert np.abs(lf - want).max() < 1e-4 and np.abs(ls - want).max() < 1e-4
+    else:
+        assert rel_fro(lf, want) < 3e-2 and rel_fro(lf, ls) < 2e-2
