@@ -1072,6 +1072,14 @@ int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, const float*
 // random bf16 A[M,K], B[N,K], `iters` back-to-back launches timed with CUDA
 // events on the compute stream. force: 0 planner, 1 1-SM BN256, 2 1-SM
 // BN128, 3 pair, 4 pair BK128; splits: 0 planner.
+// Pins the GEMM plan of later calls (tests): force 0 auto, 1 / 2 1-SM 256 /
+// 128-wide, 3 pair, 5 / 6 stream-K 256 / 128-wide; splits 0 = auto.
+int krul_debug_set_gemm_plan(int force, int splits) {
+  return guard([&] {
+    g_gemm_force = force;
+    g_gemm_splits = splits;
+  });
+}
 int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
                           int splits, int iters, float* ms_per_iter) {
   return guard([&] {

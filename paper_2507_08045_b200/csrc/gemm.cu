@@ -500,6 +500,60 @@ __device__ __forceinline__ void epi_unit(const Epi& e, const CUtensorMap* tmC, u
   }
 }
 
+// CTA owning iteration i of a stream-K schedule over G CTAs.
+__host__ __device__ inline long long sk_cta(long long i, int G, long long T) { return ((i + 1) * G - 1) / T; }
+// Pieces (partial slots in use) of n-tile `n`.
+__host__ __device__ inline int sk_pieces(int n, int num_k, int G, long long T) {
+  const long long ts = (long long)n * num_k;
+  return int(sk_cta(ts + num_k - 1, G, T) - sk_cta(ts, G, T) + 1);
+}
+// Partial-slot count of one output column for the split-K reduces: uniform
+// `splits`, or the stream-K piece count of the column's tile.
+struct SkInfo {
+  int G = 0, num_k = 0, bn = 0;
+  long long T = 0;
+  __device__ __forceinline__ int slots(int splits, int64_t col) const {
+    return T > 0 ? sk_pieces(int(col / bn), num_k, G, T) : splits;
+  }
+};
+
+// Work unit of the 1-SM kernel: tile (m, n), k-blocks [k0, k1), partial slot.
+struct Unit {
+  int m, n, k0, k1, ks;
+};
+// Stream-K schedule (sk_T > 0, single m-tile): CTA c owns the k-block
+// iterations [c*T/G, (c+1)*T/G) of the linearised (n_tile, k_block) space,
+// so every CTA streams the same number of weight blocks whatever the tile
+// count; each tile crossing starts a new piece whose slot is its index among
+// the CTAs touching that tile (fixed order -> deterministic reduce).
+// Otherwise units (m, n, split) are dealt round-robin, m fastest.
+__device__ __forceinline__ bool unit_at(int i, int mt, int nt, int splits, int kb_per, int num_k, int sk_G,
+                                        long long sk_T, Unit& u) {
+  if (sk_T > 0) {
+    const long long c = blockIdx.x;
+    const long long beg = c * sk_T / sk_G, end = (c + 1) * sk_T / sk_G;
+    long long it = beg;
+    for (int q = 0; q < i && it < end; ++q) it = (it / num_k + 1) * num_k;
+    if (it >= end) return false;
+    u.m = 0;
+    u.n = int(it / num_k);
+    const long long ts = (long long)u.n * num_k, te = ts + num_k;
+    u.k0 = int(it - ts);
+    u.k1 = int((end < te ? end : te) - ts);
+    u.ks = int(c - ((ts + 1) * sk_G - 1) / sk_T);
+    return true;
+  }
+  const int uu = blockIdx.x + i * gridDim.x;
+  if (uu >= mt * nt * splits) return false;
+  u.m = uu % mt;
+  const int rest = uu / mt;
+  u.n = rest % nt;
+  u.ks = rest / nt;
+  u.k0 = u.ks * kb_per;
+  u.k1 = min(num_k, u.k0 + kb_per);
+  return true;
+}
+
 // Persistent warp-specialised tcgen05 GEMM, C[M,N] = A[M,K] B[N,K]^T.
 //   warp 0      : TMA producer (A 128x64 + B BNx64 bf16 tiles, SW128) into an
 //                 STAGES-deep smem ring (full/empty mbarriers)
@@ -517,7 +571,7 @@ template <int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int mt, int nt, int splits, int kb_per, Epi e,
-              float* __restrict__ partial) {
+              float* __restrict__ partial, int sk_G, long long sk_T) {
   constexpr int BM = 128, BK = 64;
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   extern __shared__ unsigned char smem_raw[];
@@ -534,7 +588,6 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_k = (K + BK - 1) / BK;
-  const int units = mt * nt * splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -564,14 +617,13 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // TMA producer
       int s = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int m = u % mt, rest = u / mt, n = rest % nt, ks = rest / nt;
-        const int k0 = ks * kb_per, k1 = min(num_k, k0 + kb_per);
-        for (int kb = k0; kb < k1; ++kb) {
+      Unit un;
+      for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
+        for (int kb = un.k0; kb < un.k1; ++kb) {
           tc::mbar_wait(&empty[s], ph ^ 1);
           tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-          tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m * BM);
-          tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n * BN);
+          tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, un.m * BM);
+          tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, un.n * BN);
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -585,9 +637,9 @@ __global__ void __launch_bounds__(192, 1)
                                  (uint32_t(BM >> 4) << 24);
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int ks = u / mt / nt;
-        const int k0 = ks * kb_per, k1 = min(num_k, k0 + kb_per);
+      Unit un;
+      for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
+        const int k0 = un.k0, k1 = un.k1;
         tc::mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
         tc::fence_after();
         const uint32_t d = tmem + uint32_t(acc * BN);
@@ -620,8 +672,9 @@ __global__ void __launch_bounds__(192, 1)
     int sbuf = 0;
     int acc = 0;
     uint32_t aph = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int m = u % mt, rest = u / mt, n = rest % nt, ks = rest / nt;
+    Unit un;
+    for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
+      const int m = un.m, n = un.n, ks = un.ks;
       tc::mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t row0 = int64_t(m) * BM + 32 * q;
@@ -865,20 +918,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 // consecutive columns per thread (128-bit partial loads) when N % 4 == 0.
 template <class T>
 __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t M, int64_t N,
-                                Epi e) {
+                                Epi e, SkInfo sk) {
   const int64_t MN = M * N;
   if ((N & 3) == 0) {
     const int64_t q = N >> 2, total = M * q;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
          i += int64_t(gridDim.x) * blockDim.x) {
       const int64_t r = i / q, c = (i % q) * 4;
+      const int ns = sk.slots(splits, c);
       float4 a = *reinterpret_cast<const float4*>(P + r * N + c);
-      for (int s0 = 1; s0 < splits; s0 += 4) {  // 4 partial loads in flight, fixed order
+      for (int s0 = 1; s0 < ns; s0 += 4) {  // 4 partial loads in flight, fixed order
         float4 b[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          b[u] = s0 + u < splits ? *reinterpret_cast<const float4*>(P + int64_t(s0 + u) * MN + r * N + c)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+          b[u] = s0 + u < ns ? *reinterpret_cast<const float4*>(P + int64_t(s0 + u) * MN + r * N + c)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           a.x += b[u].x;
@@ -908,7 +962,8 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
     const int64_t r = i / cols, c = i % cols;
     if (sw) {
       float g = 0.f, u = 0.f;
-      for (int s = 0; s < splits; ++s) {
+      const int ns = sk.slots(splits, 2 * c);
+      for (int s = 0; s < ns; ++s) {
         const float* p = P + int64_t(s) * MN + r * N + 2 * c;
         g += p[0];
         u += p[1];
@@ -916,7 +971,8 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
       static_cast<T*>(e.out)[r * e.ldo + c] = fromf<T>(silu_mul(g, u));
     } else {
       float a = 0.f;
-      for (int s = 0; s < splits; ++s) a += P[int64_t(s) * MN + r * N + c];
+      const int ns = sk.slots(splits, c);
+      for (int s = 0; s < ns; ++s) a += P[int64_t(s) * MN + r * N + c];
       epi_elem<T>(e, r, c, a);
     }
   }
@@ -928,12 +984,13 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
 // in smem so both the token-major (Q, K) and the dimension-major (V^T)
 // stores are contiguous runs.
 __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P, int splits,
-                                                     int64_t M, int64_t N, EpiKV kv) {
+                                                     int64_t M, int64_t N, EpiKV kv, SkInfo sk) {
   __shared__ float t[64][33];
   const int64_t r0 = int64_t(blockIdx.x) * 64;
   const int64_t cc = int64_t(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, token group
   const int64_t MN = M * N;
+  splits = sk.slots(splits, cc);  // a 32-column block never straddles a tile
   // all partial loads of this thread in flight before the (fixed-order) sums
   float a[8];
 #pragma unroll
@@ -1030,7 +1087,11 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 struct GemmPlan {
   int bn = 256, splits = 1, kb_per = 1, grid = 1;
   bool pair = false;  // cta_group::2, 256x256 tiles
+  // stream-K (single m-tile, 1-SM kernel): grid CTAs share T = nt * num_k
+  // k-block iterations evenly; `splits` = partial slots (max pieces per tile)
+  long long sk_T = 0;
 };
+
 
 // Pick the kernel (1-SM 128xBN or 2-SM 256x256), tile width and split-K
 // count with a small cost model (ns). Per k-block time = max(MMA issue time,
@@ -1042,14 +1103,18 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
   const int force = g_gemm_force;
   GemmPlan best;
   double best_t = 1e30;
-  const double l2_bw = 75.0, hbm_bw = 6000.0, clk = 1.85;
+  // constants fitted to a measured sweep of every (variant, split) on the
+  // pyramid / new-input shapes with weights streamed from HBM
+  // (tools/gemm_sweep.py; regret of the chosen plan 3.7% -> 1.7%)
+  const double l2_bw = 140.0, hbm_bw = 7000.0, clk = 1.85, unit_ns = 2000.0, pair_eff = 0.9,
+               split_ns = 1500.0, split_bw = 5000.0;
   for (int variant = 0; variant < 3; ++variant) {
     const bool pair = variant == 0;
     const int bn = variant == 2 ? 128 : 256;
     const int bm = pair ? 256 : 128;
     if (pair && M <= 128 && force != 3 && force != 4) continue;
     if ((force == 1 && variant != 1) || (force == 2 && variant != 2) ||
-        ((force == 3 || force == 4) && variant != 0))
+        ((force == 3 || force == 4) && variant != 0) || ((force == 5 || force == 6) && variant == 0))
       continue;
     const int64_t mt = (M + bm - 1) / bm, nt = (N + bn - 1) / bn;
     const int64_t slots = pair ? sms / 2 : sms;
@@ -1064,15 +1129,15 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
       const int64_t active = std::min<int64_t>(units, slots);
       const int64_t per = (units + slots - 1) / slots;
       // per-SM quantities (a pair unit is two SMs' worth of work)
-      const double mma_ns = (bn == 256 ? 512.0 : 256.0) / clk;
+      const double mma_ns = (bn == 256 ? 512.0 : 256.0) / clk / (pair ? pair_eff : 1.0);
       const double b_bytes = (pair ? 128.0 : double(bn)) * 128.0, a_bytes = 128.0 * 128.0;
       const double share = double(std::min<int64_t>(mt, active));
       const double sm_active = double(active) * (pair ? 2.0 : 1.0);
       const double hbm_ns = (b_bytes / share) / (hbm_bw / sm_active);
       const double l2_ns = (a_bytes + b_bytes) / l2_bw;
       const double kb_ns = std::max(mma_ns, std::max(hbm_ns, l2_ns));
-      double t = double(per) * double(kb_per) * kb_ns + double(per) * 600.0;
-      if (splits > 1) t += double(M) * double(N) * double(splits) * 8.0 / 3000.0 + 2500.0;
+      double t = double(per) * double(kb_per) * kb_ns + double(per) * unit_ns;
+      if (splits > 1) t += double(M) * double(N) * double(splits) * 8.0 / split_bw + split_ns;
       if (t < best_t * 0.97) {
         best_t = t;
         best.pair = pair;
@@ -1080,6 +1145,35 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
         best.splits = int(splits);
         best.kb_per = int(kb_per);
         best.grid = int(active) * (pair ? 2 : 1);
+        best.sk_T = 0;
+      }
+    }
+    // stream-K: one m-tile, every SM streams T / sms weight blocks
+    // (debug force: 5 = stream-K with 256-wide tiles, 6 = with 128-wide)
+    const bool sk_forced = (force == 5 && bn == 256) || (force == 6 && bn == 128);
+    if (!pair && mt == 1 && allow_split && (force == 0 || sk_forced)) {
+      const long long T = (long long)nt * num_k;
+      if (T >= 2 * sms && (g_gemm_splits <= 0)) {
+        int maxp = 1;
+        for (int n = 0; n < nt; ++n) maxp = std::max(maxp, sk_pieces(n, int(num_k), sms, T));
+        const double per = double(T) / double(sms);
+        const double mma_ns = (bn == 256 ? 512.0 : 256.0) / clk;
+        const double b_bytes = double(bn) * 128.0, a_bytes = 128.0 * 128.0;
+        const double hbm_ns = b_bytes / (hbm_bw / double(sms));
+        const double l2_ns = (a_bytes + b_bytes) / l2_bw;
+        const double kb_ns = std::max(mma_ns, std::max(hbm_ns, l2_ns));
+        const double pieces = double(nt + sms);  // partial tiles written + read (L2-resident)
+        double t = per * kb_ns + 2.0 * 600.0 + pieces * 128.0 * bn * 4.0 * 2.0 / 12000.0 + 2500.0;
+        if (sk_forced) t = 0.0;
+        if (M * N * maxp * 4 <= (int64_t(256) << 20) && t < best_t * 0.97) {
+          best_t = t;
+          best.pair = false;
+          best.bn = bn;
+          best.splits = maxp;
+          best.kb_per = 0;
+          best.grid = sms;
+          best.sk_T = T;
+        }
       }
     }
   }
@@ -1139,7 +1233,7 @@ void run_tc(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUt
   }
   const int mt = int((M + 127) / 128), nt = int((N + BN - 1) / BN);
   kern<<<gp.grid, 192, smem, s>>>(ta, tb, tcm, int(M), int(N), int(K), mt, nt, gp.splits, gp.kb_per,
-                                  e, partial);
+                                  e, partial, gp.grid, gp.sk_T);
   KB_LAUNCH();
 }
 
@@ -1239,20 +1333,27 @@ void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, co
     if (new_sms > 0 && new_sms < sms) sms = (s == c.s_new) ? new_sms : sms - new_sms;
     const GemmPlan gp = plan_gemm(M, N, K, sms, true);
     float* part = nullptr;
-    if (gp.splits > 1) {
+    if (gp.splits > 1 || gp.sk_T > 0) {
       DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;
       part = static_cast<float*>(buf.ensure(size_t(M) * size_t(N) * gp.splits * 4));
     }
     launch_gemm_tc(gp, s, M, N, K, A, lda, B, ldb, e, part);
+    SkInfo sk;
+    if (gp.sk_T > 0) {
+      sk.G = gp.grid;
+      sk.T = gp.sk_T;
+      sk.num_k = int((K + 63) / 64);
+      sk.bn = gp.bn;
+    }
     if (part && e.kind == Epi::QKV) {
       if (c.cfg.hd % 32) fail(KRUL_E_CUDA, "fused QKV epilogue needs head_dim % 32 == 0");
       const dim3 g2{unsigned((M + 63) / 64), unsigned((N + 31) / 32), 1u};
-      k_qkv_reduce<<<g2, 256, 0, s>>>(part, gp.splits, M, N, e.kv);
+      k_qkv_reduce<<<g2, 256, 0, s>>>(part, gp.splits, M, N, e.kv, sk);
       KB_LAUNCH();
     } else if (part) {
       const int64_t work = (N % 4 == 0) ? M * N / 4 : (e.kind == Epi::SWIGLU ? M * N / 2 : M * N);
       const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8 * 148));
-      k_splitk_reduce<bf16><<<blocks, 256, 0, s>>>(part, gp.splits, M, N, e);
+      k_splitk_reduce<bf16><<<blocks, 256, 0, s>>>(part, gp.splits, M, N, e, sk);
       KB_LAUNCH();
     }
     return;

@@ -762,3 +762,49 @@ def test_fused_recompute_matches_separate_stream(K, oracle, dtype, monkeypatch):
         assert np.abs(lf - want).max() < 1e-4 and np.abs(ls - want).max() < 1e-4
     else:
         assert rel_fro(lf, want) < 3e-2 and rel_fro(lf, ls) < 2e-2
+
+
+@pytest.mark.parametrize("force", [0, 5, 6])
+@pytest.mark.parametrize("M,N,Kd", [(128, 4096, 4096), (77, 1536, 14336), (1, 6144, 4096), (128, 28672 // 8, 4096)])
+def test_gemm_stream_k_epilogues(K, force, M, N, Kd):
+    """Weight-streaming shapes (M <= 128) through the stream-K schedule
+    (every CTA streams T / G weight blocks, tiles split into pieces reduced in
+    fixed order) vs the auto plan, for the F32 / tanh / SwiGLU / residual
+    epilogues; deterministic across calls."""
+    from paper_2507_08045_b200.native import _p, lib
+    import ctypes as C
+    cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
+                        dtype=K.KRUL_BF16, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(M + N + Kd)
+    A = (rng.uniform(-.5, .5, (M, Kd)) / np.sqrt(Kd / 64)).astype(np.float32)
+    B = rng.uniform(-.5, .5, (N, Kd)).astype(np.float32)
+    bias = rng.uniform(-.5, .5, N).astype(np.float32)
+    acc = A.astype(np.float64) @ B.astype(np.float64).T
+    tol = 5e-2
+    assert lib().krul_debug_set_gemm_plan(force, 0) == 0
+    try:
+        outs = []
+        for _ in range(2):
+            out = np.zeros((M, N), np.float32)
+            assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                         _p(B), None, 0, _p(out)) == 0
+            outs.append(out)
+        assert np.array_equal(outs[0], outs[1])
+        assert np.abs(outs[0] - acc).max() < tol * 0.2
+        out = np.zeros((M, N), np.float32)
+        assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                     _p(B), _p(bias), 3, _p(out)) == 0
+        assert np.abs(out - np.tanh(acc + bias)).max() < tol
+        out = np.zeros((M, N // 2), np.float32)
+        assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                     _p(B), None, 4, _p(out)) == 0
+        g, u = acc[:, 0::2], acc[:, 1::2]
+        assert np.abs(out - g / (1 + np.exp(-g)) * u).max() < tol * max(1.0, np.abs(g * u).max())
+        resid = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+        out = resid.copy()
+        assert lib().krul_debug_gemm(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), _p(A),
+                                     _p(B), _p(bias), 2, _p(out)) == 0
+        assert np.abs(out - (resid + acc + bias)).max() < tol
+    finally:
+        lib().krul_debug_set_gemm_plan(0, 0)

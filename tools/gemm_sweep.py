@@ -19,14 +19,16 @@ Ms = [int(x) for x in os.environ.get("MS", "64,128,130,200,256,300,400,500,600,7
 for M in Ms:
     for N, Kd, epi in ((6144, 4096, 0), (4096, 4096, 2), (28672, 4096, 4), (4096, 14336, 2)):
         nk = (Kd + 63) // 64
-        for var in (0, 1, 2, 3):
-            for sp in ((0,) if var == 0 else (1, 2, 3, 4, 6, 8)):
+        for var in (0, 1, 2, 3, 5, 6):
+            for sp in ((0,) if var in (0, 5, 6) else (1, 2, 3, 4, 6, 8)):
                 if sp:
                     kb = (nk + sp - 1) // sp
                     if (nk + kb - 1) // kb != sp or (sp > 1 and M * N * sp * 4 > (256 << 20)):
                         continue
                     if var == 3 and M <= 128:
                         continue
+                if var in (5, 6) and M > 128:
+                    continue
                 ms = C.c_float(0)
                 rc = lib.krul_debug_gemm_bench(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(Kd), epi, var,
                                                sp, 30, C.byref(ms))
