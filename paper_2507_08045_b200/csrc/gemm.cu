@@ -985,47 +985,61 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
 // stores are contiguous runs.
 __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P, int splits,
                                                      int64_t M, int64_t N, EpiKV kv, SkInfo sk) {
-  __shared__ float t[64][33];
-  const int64_t r0 = int64_t(blockIdx.x) * 64;
+  // block = 32 tokens x 32 columns (M = 128 -> 768 CTAs: enough warps per
+  // SM to hide the partial loads); RoPE tables and page ids are fetched
+  // before the partial sums, off the dependent chain
+  constexpr int RB = 32, RJ = RB / 8;
+  __shared__ float t[RB][33];
+  const int64_t r0 = int64_t(blockIdx.x) * RB;
   const int64_t cc = int64_t(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, token group
   const int64_t MN = M * N;
   splits = sk.slots(splits, cc);  // a 32-column block never straddles a tile
-  // all partial loads of this thread in flight before the (fixed-order) sums
-  float a[8];
+  const int nq = kv.H * kv.hd, nkv = kv.Hkv * kv.hd, half = kv.hd / 2;
+  const bool isq = cc < nq, isk = !isq && cc < nq + nkv;
+  const int t0 = int((isq ? cc : cc - nq) % kv.hd);
+  const int i = (t0 + tx) >> 1;
+  float cs[RJ], sn[RJ];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) a[j] = 0.f;
+  for (int j = 0; j < RJ; ++j) {
+    const int64_t r = r0 + ty + 8 * j;
+    cs[j] = sn[j] = 0.f;
+    if ((isq || isk) && r < M) {
+      const int64_t pos = kv.pos(r);
+      cs[j] = __ldg(kv.cosT + pos * half + i);
+      sn[j] = __ldg(kv.sinT + pos * half + i);
+    }
+  }
+  // all partial loads of this thread in flight before the (fixed-order) sums
+  float a[RJ];
+#pragma unroll
+  for (int j = 0; j < RJ; ++j) a[j] = 0.f;
   for (int s0 = 0; s0 < splits; s0 += 4) {
-    float v[4][8];
+    float v[4][RJ];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < RJ; ++j) {
         const int64_t r = r0 + ty + 8 * j;
         v[u][j] = (s0 + u < splits && r < M && cc + tx < N) ? P[int64_t(s0 + u) * MN + r * N + cc + tx] : 0.f;
       }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) a[j] += v[u][j];
+      for (int j = 0; j < RJ; ++j) a[j] += v[u][j];
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) t[ty + 8 * j][tx] = a[j];
+  for (int j = 0; j < RJ; ++j) t[ty + 8 * j][tx] = a[j];
   __syncthreads();
-  const int nq = kv.H * kv.hd, nkv = kv.Hkv * kv.hd, half = kv.hd / 2;
-  const bool isq = cc < nq, isk = !isq && cc < nq + nkv;
   if (isq || isk) {
-    const int t0 = int((isq ? cc : cc - nq) % kv.hd);
-    const int i = (t0 + tx) >> 1;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < RJ; ++j) {
       const int rr = ty + 8 * j;
       const int64_t r = r0 + rr;
       if (r >= M || (isq && r >= kv.q_rows)) continue;
       const int64_t pos = kv.pos(r);
       const float x0 = t[rr][tx & ~1], x1 = t[rr][tx | 1];
-      const float cs = kv.cosT[pos * half + i], sn = kv.sinT[pos * half + i];
-      const float y = (tx & 1) ? (x0 * sn + x1 * cs) : (x0 * cs - x1 * sn);
+      const float y = (tx & 1) ? (x0 * sn[j] + x1 * cs[j]) : (x0 * cs[j] - x1 * sn[j]);
       if (isq) {
         static_cast<bf16*>(kv.q)[r * nq + cc + tx] = __float2bfloat16_rn(y);
       } else {
@@ -1036,16 +1050,16 @@ __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P,
     }
   } else {
     const int64_t vc = cc - nq - nkv;
-    const int g = int(vc / kv.hd), t0 = int(vc % kv.hd);
-    // thread -> (dimension d, 8 consecutive tokens)
-    const int d = threadIdx.x >> 3, tg = (threadIdx.x & 7) * 8;
+    const int g = int(vc / kv.hd), tv0 = int(vc % kv.hd);
+    // thread -> (dimension d, 4 consecutive tokens)
+    const int d = threadIdx.x >> 3, tg = (threadIdx.x & 7) * 4;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int64_t r = r0 + tg + u;
       if (r >= M) break;
       const int64_t pos = kv.pos(r);
       bf16* page = reinterpret_cast<bf16*>(kv.pool + int64_t(kv.pt[pos / kPageTokens]) * kv.page_bytes);
-      page[int64_t(kv.Hkv) * kPageTokens * kv.hd + (int64_t(g) * kv.hd + t0 + d) * kPageTokens +
+      page[int64_t(kv.Hkv) * kPageTokens * kv.hd + (int64_t(g) * kv.hd + tv0 + d) * kPageTokens +
            pos % kPageTokens] = __float2bfloat16_rn(t[tg + u][d]);
     }
   }
@@ -1347,7 +1361,7 @@ void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, co
     }
     if (part && e.kind == Epi::QKV) {
       if (c.cfg.hd % 32) fail(KRUL_E_CUDA, "fused QKV epilogue needs head_dim % 32 == 0");
-      const dim3 g2{unsigned((M + 63) / 64), unsigned((N + 31) / 32), 1u};
+      const dim3 g2{unsigned((M + 31) / 32), unsigned((N + 31) / 32), 1u};
       k_qkv_reduce<<<g2, 256, 0, s>>>(part, gp.splits, M, N, e.kv, sk);
       KB_LAUNCH();
     } else if (part) {

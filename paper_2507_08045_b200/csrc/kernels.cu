@@ -66,9 +66,42 @@ __global__ void __launch_bounds__(256) k_rmsnorm_warp(const float* __restrict__ 
     o[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
   }
 }
+// Few rows (the new-input prefill's 128): one 256-thread CTA per row so the
+// norm spreads over the SMs instead of 16 CTAs (measured 9 us -> the launch
+// floor); same arithmetic order per element, block reduction of the sum.
+template <int V>  // float4 vectors per thread: d = 1024 * V
+__global__ void __launch_bounds__(256) k_rmsnorm_cta(const float* __restrict__ h, int d,
+                                                     bf16* __restrict__ out) {
+  const int64_t r = blockIdx.x;
+  const float4* x = reinterpret_cast<const float4*>(h + r * d);
+  float4 v[V];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    v[i] = __ldg(x + threadIdx.x + 256 * i);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  ss = block_sum(ss);
+  const float denom = sqrtf(ss / float(d) + 1e-6f);
+  uint2* o = reinterpret_cast<uint2*>(out + r * d);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[i].x / denom, v[i].y / denom);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[i].z / denom, v[i].w / denom);
+    o[threadIdx.x + 256 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
 void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, void* xn) {
   if (rows <= 0) return;
   const int d = c.cfg.d;
+  if (c.cfg.dtype == KRUL_BF16 && rows <= 2 * 148 && (d == 4096 || d == 8192)) {
+    if (d == 4096)
+      k_rmsnorm_cta<4><<<unsigned(rows), 256, 0, s>>>(h, d, (bf16*)xn);
+    else
+      k_rmsnorm_cta<8><<<unsigned(rows), 256, 0, s>>>(h, d, (bf16*)xn);
+    KB_LAUNCH();
+    return;
+  }
   if (c.cfg.dtype == KRUL_BF16 && d % 128 == 0 && d <= 128 * 32) {
     const unsigned blocks = unsigned((rows + 7) / 8);
     switch (d / 128) {
