@@ -1017,6 +1017,7 @@ int krul_restore_timeline(krul_ctx* ctx, double* comp, double* load, double* new
     need(ctx, "ctx");
     Ctx& c = *ctx->c;
     if (c.tl_compute.empty()) fail(KRUL_E_STATE_CORRUPTION, "no restore has run on this context");
+    restore_timeline(c);
     const size_t n = c.tl_compute.size();
     if (comp) std::copy(c.tl_compute.begin(), c.tl_compute.end(), comp);
     if (load) std::copy(c.tl_load.begin(), c.tl_load.end(), load);

@@ -126,6 +126,7 @@ void container_write(const Snapshot& s, char* out);  // exactly container_size b
 void container_write_file(const Snapshot& s, const char* path);
 Snapshot* container_read(Ctx* c, const char* buf, size_t n, const uint64_t* expected_hash);
 Snapshot* container_read_file(Ctx* c, const char* path, const uint64_t* expected_hash);
+void restore_timeline(Ctx& c);  // reads the last restore's per-layer events
 void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
              krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
              double* ttft_ms);

@@ -4,7 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "kb.hpp"
+#include "host.hpp"
 
 namespace kb {
 
@@ -159,6 +159,13 @@ uint64_t config_hash(const Cfg& c) {
 }
 
 void Ctx::drop_graph() {
+  if (tl_pending) {  // the timeline's events die with the graph: read them now
+    try {
+      restore_timeline(*this);
+    } catch (...) {
+      tl_pending = false;
+    }
+  }
   if (rg.exec) cudaGraphExecDestroy(rg.exec);
   for (auto& m : rg.ev) {
     if (m.dep) cudaEventDestroy(m.dep);

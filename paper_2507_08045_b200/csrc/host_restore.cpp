@@ -415,22 +415,11 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   KB_CUDA(cudaEventElapsedTime(&te, E[0], E[3]));
   KB_CUDA(cudaEventElapsedTime(&th, E[0], E[4]));
   if (ttft_ms) *ttft_ms = te;
-  // measured per-layer timeline (ms from restore launch), the device
-  // counterpart of PipelineTrace (scheduler.hpp:71-97)
+  // the per-layer timeline is read lazily (restore_timeline): ~100 event
+  // queries would otherwise sit inside every call's host time
+  c.tl_pending = true;
+  c.tl_has_new = new_tok != nullptr;
   c.tl_compute.assign(size_t(g.N), 0.0);
-  c.tl_load.assign(size_t(g.N), 0.0);
-  c.tl_new.assign(size_t(g.N), 0.0);
-  for (int l = 0; l < g.N && G.timeline; ++l) {
-    float a = 0, b = 0, e = 0;
-    KB_CUDA(cudaEventElapsedTime(&a, E[0], E[5 + l]));
-    KB_CUDA(cudaEventElapsedTime(&b, E[0], E[5 + g.N + l]));
-    c.tl_compute[size_t(l)] = a;
-    c.tl_load[size_t(l)] = b;
-    if (new_tok) {
-      KB_CUDA(cudaEventElapsedTime(&e, E[0], E[5 + 2 * g.N + l]));
-      c.tl_new[size_t(l)] = e;
-    }
-  }
   c.tl_h2d_ms = th;
   if (st) {
     Cost cm;
@@ -452,6 +441,29 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     st->recompute_flops = fl;
     st->h2d_ms = th;
   }
+}
+
+// measured per-layer timeline (ms from restore launch) of the last restore,
+// the device counterpart of PipelineTrace (scheduler.hpp:71-97)
+void restore_timeline(Ctx& c) {
+  if (!c.tl_pending) return;
+  const Cfg& g = c.cfg;
+  const auto& E = c.rg.ev;
+  c.tl_compute.assign(size_t(g.N), 0.0);
+  c.tl_load.assign(size_t(g.N), 0.0);
+  c.tl_new.assign(size_t(g.N), 0.0);
+  for (int l = 0; l < g.N && c.rg.timeline; ++l) {
+    float a = 0, b = 0, e = 0;
+    KB_CUDA(cudaEventElapsedTime(&a, E[0].tim, E[size_t(5 + l)].tim));
+    KB_CUDA(cudaEventElapsedTime(&b, E[0].tim, E[size_t(5 + g.N + l)].tim));
+    c.tl_compute[size_t(l)] = a;
+    c.tl_load[size_t(l)] = b;
+    if (c.tl_has_new) {
+      KB_CUDA(cudaEventElapsedTime(&e, E[0].tim, E[size_t(5 + 2 * g.N + l)].tim));
+      c.tl_new[size_t(l)] = e;
+    }
+  }
+  c.tl_pending = false;
 }
 
 }  // namespace kb

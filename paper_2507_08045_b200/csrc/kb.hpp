@@ -210,6 +210,7 @@ struct Ctx {
   bool dec_valid = false;
 
   // restore staging + last measured timeline (ms from launch)
+  bool tl_pending = false, tl_has_new = false;  // per-layer timeline not yet read back
   DevBuf staging;
   DevBuf cstaging;       // coded blob images (H2D target; decoded into `staging`)
   bool kv_coding = true; // exponent-code bf16 snapshots at compress (KRUL_KV_CODING=0: off)
