@@ -446,7 +446,8 @@ def run_b200(args, rank, local, world, dist):
                 "unit": "TFLOP/s",
                 "note": "algorithmic pyramid flops / recompute-stream makespan (shares SMs with the "
                         "new-input prefill and expand streams)"},
-            **({"estimator_decode_fold": est["fold"], "selector": est["select"]} if est else {}),
+            **({"estimator_decode_fold": est["fold"], "selector": est["select"],
+                "decode_tpot": est["tpot"]} if est else {}),
             **({"container": ctr} if ctr else {}),
         },
         "e2e": {"value": round(e2e_conv_s, 4), "unit": "conversations/s",
@@ -505,8 +506,21 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
     so the fold reads every layer's row; decode fold HBM GB/s from CUDA
     events around each fold launch (algorithmic bytes: N*H*W*4 + P*H*16)."""
     est = K.StreamingEstimator(ctx, list(range(cfg.n_layers)))
-    ctx.ktime_enable(True)
     rng = np.random.default_rng(7)
+    # TPOT with and without the streaming estimator in the decode loop
+    # (SURVEY f1; the paper reports the overhead as negligible, PAPER.md:710):
+    # wall clock per synchronous decode step, the fold on its own stream
+    tpot = {}
+    for with_est in (False, True, False, True):
+        t0 = time.perf_counter()
+        for _ in range(6):
+            ctx.decode_step(conv, int(rng.integers(0, cfg.vocab_size)))
+            if with_est:
+                est.fold_decode()
+        ctx.sync()
+        dt = (time.perf_counter() - t0) / 6 * 1e3
+        tpot[with_est] = min(tpot.get(with_est, 1e9), dt)
+    ctx.ktime_enable(True)
     for _ in range(steps):
         ctx.decode_step(conv, int(rng.integers(0, cfg.vocab_size)))
         est.fold_decode()
@@ -538,6 +552,11 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
                      "us_per_fold": round(1e3 * ms, 2),
                      "us_per_fold_incl_launch_gap": round(1e3 * ms_ev / max(n, 1), 2),
                      "width": int(len(conv)), "tracked_layers": cfg.n_layers},
+            "tpot": {"decode_step_ms": round(tpot[False], 3),
+                     "decode_step_with_estimator_ms": round(tpot[True], 3),
+                     "estimator_overhead": round(tpot[True] / tpot[False] - 1.0, 4),
+                     "note": "wall clock per synchronous decode step (eager launches) at the restored "
+                             "context length, all layers tracked; fold on the estimator stream"},
             "select": {"bound": "latency", "kernel": "k_select (K3) incl. D upload + result read",
                        "us_per_call": round(sel_us, 1), "pairs_selected": len(strat.pairs),
                        "candidates": cfg.n_layers * (cfg.n_layers - 1) // 2}}
