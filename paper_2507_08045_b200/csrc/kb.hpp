@@ -206,6 +206,7 @@ struct Ctx {
   double cap_ifrac = 0.1, cap_rfrac = 0.1;
   int64_t cap_il = 0, cap_rs = 0;
   DevBuf dec_rows;        // [N][H][W] f32 last decode step
+  DevBuf dec_part;        // split-key partials of the decode attention
   int64_t dec_width = 0;
   bool dec_valid = false;
 

@@ -2,6 +2,8 @@
 // kernels of the B200 Krul hot path. Templated on the compute dtype T
 // (float = parity mode, __nv_bfloat16 = perf mode). GEMMs live in
 // gemm_simt.cu / gemm_sm100.cu.
+#include <cstdlib>
+#include <cstring>
 #include <cfloat>
 #include <cmath>
 
@@ -263,6 +265,218 @@ __global__ void k_attn_simt(const T* q, int64_t pos0, PageView pv, int H, float 
   }
 }
 
+// ---------------------------------------------------------------- decode attention
+// One query row per head (decode_step, engine.cpp:406-446) over W keys, bf16
+// cache, hd = 128, GQA group G = H / Hkv <= 8: the keys are split over
+// CTAs (chunks of 256 keys x KV head) so the whole GPU streams the cache
+// (the per-(row, head) SIMT kernel ran 32 CTAs for 1.2 ms per layer at 8K).
+// Pass 1: each lane scores one key for the group's G heads (K row read once),
+// chunk max / sum / partial P.V per head; raw scores go to the capture row.
+// Pass 2 (one CTA per head): merges the chunk partials, writes the context
+// row and normalises the captured probabilities (+ region mass) in place.
+constexpr int kDecChunk = 256, kDecMaxG = 8;
+__global__ void __launch_bounds__(256) k_attn_decode1(const bf16* __restrict__ q, int64_t W, PageView pv,
+                                                      int H, float scale, float* __restrict__ probs,
+                                                      int64_t ld_probs, float* __restrict__ part) {
+  constexpr int HD = 128;
+  const int g = blockIdx.y, G = H / pv.Hkv, h0 = g * G;
+  const int64_t k0 = int64_t(blockIdx.x) * kDecChunk;
+  const int nk = int(W - k0 < kDecChunk ? W - k0 : kDecChunk);
+  __shared__ float qs[kDecMaxG][HD];
+  __shared__ float ps[kDecMaxG][kDecChunk];
+  __shared__ float red[kDecMaxG][8];
+  __shared__ float o2[kDecMaxG][HD];
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) qs[i / HD][i % HD] = __bfloat162float(q[(h0 + i / HD) * HD + i % HD]) * scale;
+  __syncthreads();
+  // scores: thread j -> key k0 + j
+  float sc[kDecMaxG];
+  const int j = threadIdx.x;
+  if (j < nk) {
+    const int64_t k = k0 + j;
+    const uint4* kr = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(pv.page(k)) + pv.k_off(g, k, 0));
+#pragma unroll
+    for (int hh = 0; hh < kDecMaxG; ++hh) sc[hh] = 0.f;
+#pragma unroll 4
+    for (int v = 0; v < HD / 8; ++v) {
+      const uint4 x = __ldg(kr + v);
+      const uint32_t u[4] = {x.x, x.y, x.z, x.w};
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[e]));
+        f[2 * e] = t.x;
+        f[2 * e + 1] = t.y;
+      }
+#pragma unroll
+      for (int hh = 0; hh < kDecMaxG; ++hh) {
+        if (hh < G) {
+          float a = sc[hh];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) a += qs[hh][8 * v + e] * f[e];
+          sc[hh] = a;
+        }
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < kDecMaxG; ++hh) {
+      if (hh < G) {
+        ps[hh][j] = sc[hh];
+        if (probs) probs[int64_t(h0 + hh) * ld_probs + k] = sc[hh];  // raw score, normalised in pass 2
+      }
+    }
+  }
+  __syncthreads();
+  // chunk max and sum per head (warp w reduces head w's row)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < G) {
+    float m = -FLT_MAX;
+    for (int i = lane; i < nk; i += 32) m = fmaxf(m, ps[warp][i]);
+    m = warp_max(m);
+    float l = 0.f;
+    for (int i = lane; i < nk; i += 32) {
+      const float e = expf(ps[warp][i] - m);
+      ps[warp][i] = e;
+      l += e;
+    }
+    l = warp_sum(l);
+    if (lane == 0) {
+      red[warp][0] = m;
+      red[warp][1] = l;
+    }
+  }
+  __syncthreads();
+  // partial P.V: thread -> dimension d, key half
+  const int d = threadIdx.x & (HD - 1), half = threadIdx.x >> 7;
+  float acc[kDecMaxG];
+#pragma unroll
+  for (int hh = 0; hh < kDecMaxG; ++hh) acc[hh] = 0.f;
+  const int i0 = half * (kDecChunk / 2), i1 = min(nk, i0 + kDecChunk / 2);
+  // V^T rows are token-contiguous inside a page: 8 tokens per 16-byte load
+  int i = i0;
+  for (; i + 8 <= i1; i += 8) {
+    const int64_t k = k0 + i;
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(pv.page(k)) +
+                                                         pv.v_off(g, k, d)));
+    const uint32_t u[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[e]));
+#pragma unroll
+      for (int hh = 0; hh < kDecMaxG; ++hh)
+        if (hh < G) acc[hh] += ps[hh][i + 2 * e] * t.x + ps[hh][i + 2 * e + 1] * t.y;
+    }
+  }
+  for (; i < i1; ++i) {
+    const int64_t k = k0 + i;
+    const float v = __bfloat162float(reinterpret_cast<const bf16*>(pv.page(k))[pv.v_off(g, k, d)]);
+#pragma unroll
+    for (int hh = 0; hh < kDecMaxG; ++hh)
+      if (hh < G) acc[hh] += ps[hh][i] * v;
+  }
+  if (half == 1) {
+#pragma unroll
+    for (int hh = 0; hh < kDecMaxG; ++hh)
+      if (hh < G) o2[hh][d] = acc[hh];
+  }
+  __syncthreads();
+  if (half == 0) {
+    float* pp = part + (int64_t(blockIdx.x) * H + h0) * (HD + 2);
+#pragma unroll
+    for (int hh = 0; hh < kDecMaxG; ++hh) {
+      if (hh < G) {
+        pp[int64_t(hh) * (HD + 2) + d] = acc[hh] + o2[hh][d];
+        if (d == 0) {
+          pp[int64_t(hh) * (HD + 2) + HD] = red[hh][0];
+          pp[int64_t(hh) * (HD + 2) + HD + 1] = red[hh][1];
+        }
+      }
+    }
+  }
+}
+// grid (H, nsub): every CTA merges the chunk statistics (cheap) and
+// normalises its slice of the captured row; sub-block 0 writes the context.
+__global__ void __launch_bounds__(256) k_attn_decode2(const float* __restrict__ part, int nchunks, int64_t W,
+                                                      int H, bf16* __restrict__ out, float* __restrict__ probs,
+                                                      int64_t ld_probs, double* mass, int64_t il, int64_t rs) {
+  constexpr int HD = 128;
+  const int h = blockIdx.x;
+  __shared__ float sh_ml[2];
+  float m = -FLT_MAX;
+  for (int c = threadIdx.x; c < nchunks; c += blockDim.x) m = fmaxf(m, part[(int64_t(c) * H + h) * (HD + 2) + HD]);
+  m = block_max(m);
+  float l = 0.f;
+  for (int c = threadIdx.x; c < nchunks; c += blockDim.x) {
+    const float* pp = part + (int64_t(c) * H + h) * (HD + 2);
+    l += pp[HD + 1] * expf(pp[HD] - m);
+  }
+  l = block_sum(l);
+  if (threadIdx.x == 0) {
+    sh_ml[0] = m;
+    sh_ml[1] = l;
+  }
+  __syncthreads();
+  m = sh_ml[0];
+  l = sh_ml[1];
+  if (blockIdx.y == 0 && threadIdx.x < HD) {
+    float o = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const float* pp = part + (int64_t(c) * H + h) * (HD + 2);
+      o += pp[threadIdx.x] * expf(pp[HD] - m);
+    }
+    out[int64_t(h) * HD + threadIdx.x] = __float2bfloat16_rn(o / l);
+  }
+  if (probs) {
+    const int64_t per = (W + gridDim.y - 1) / gridDim.y;
+    const int64_t a = int64_t(blockIdx.y) * per, b = a + per < W ? a + per : W;
+    double ms = 0.0;
+    float* pr = probs + int64_t(h) * ld_probs;
+    for (int64_t k0 = a + threadIdx.x; k0 < b; k0 += 8 * int64_t(blockDim.x)) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t k = k0 + int64_t(u) * blockDim.x;
+        x[u] = k < b ? pr[k] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t k = k0 + int64_t(u) * blockDim.x;
+        if (k < b) {
+          const float p = expf(x[u] - m) / l;
+          pr[k] = p;
+          if (mass && (k < il || k >= rs)) ms += double(p);
+        }
+      }
+    }
+    if (mass) {  // mass requests run with one sub-block per head
+      ms = block_sum_d(ms);
+      if (threadIdx.x == 0) mass[h] = ms;
+    }
+  }
+}
+static bool attention_decode_supported(const Ctx& c, const AttnArgs& a) {
+  static const bool simt = [] {  // KRUL_DECODE_ATTN=simt: the per-(row, head) kernel (tests)
+    const char* v = std::getenv("KRUL_DECODE_ATTN");
+    return v && std::strcmp(v, "simt") == 0;
+  }();
+  return !simt && a.rows == 1 && c.cfg.dtype == KRUL_BF16 && c.cfg.hd == 128 && c.cfg.H % c.cfg.Hkv == 0 &&
+         c.cfg.H / c.cfg.Hkv <= kDecMaxG && (!a.probs || a.probs_rows == 1) && a.probs_row0 == 0 &&
+         (!a.mass || a.mass_rows == 1);
+}
+static void launch_attention_decode(const Ctx& c, cudaStream_t s, const Conv& conv, int layer, const AttnArgs& a) {
+  PageView pv = page_view(c, conv, layer);
+  const int64_t W = a.pos0 + 1;
+  const int nch = int((W + kDecChunk - 1) / kDecChunk);
+  float* part = static_cast<float*>(const_cast<Ctx&>(c).dec_part.ensure(size_t(nch) * c.cfg.H * (128 + 2) * 4));
+  const float scale = 1.0f / sqrtf(float(c.cfg.hd));
+  k_attn_decode1<<<dim3(unsigned(nch), unsigned(c.cfg.Hkv)), 256, 0, s>>>(
+      (const bf16*)a.q, W, pv, c.cfg.H, scale, a.probs, a.ld_probs, part);
+  KB_LAUNCH();
+  const unsigned nsub = a.mass ? 1u : unsigned(std::min<int64_t>(16, (W + 2047) / 2048));
+  k_attn_decode2<<<dim3(unsigned(c.cfg.H), nsub), 256, 0, s>>>(part, nch, W, c.cfg.H, (bf16*)a.out, a.probs,
+                                                               a.ld_probs, a.mass, a.il, a.rs);
+  KB_LAUNCH();
+}
+
 void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                       const AttnArgs& a) {
   if (a.rows <= 0) return;
@@ -272,6 +486,12 @@ void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
     cudaEvent_t kt0 = kt_begin(c, s);
     launch_attention_tc(c, s, conv, layer, a, *a.part);
     kt_end(c, s, kt0, KT_ATTN, 4.0 * c.cfg.hd * double(c.cfg.H) * vis, 0.0);
+    return;
+  }
+  if (attention_decode_supported(c, a)) {
+    cudaEvent_t kt0 = kt_begin(c, s);
+    launch_attention_decode(c, s, conv, layer, a);
+    kt_end(c, s, kt0, KT_ATTN, 4.0 * c.cfg.hd * double(c.cfg.H) * double(a.pos0 + 1), 0.0);
     return;
   }
   PageView pv = page_view(c, conv, layer);
