@@ -17,7 +17,10 @@ out = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/gemm_sweep.csv", "w
 out.write("M,N,K,epi,variant,splits,us\n")
 Ms = [int(x) for x in os.environ.get("MS", "64,128,130,200,256,300,400,500,600,700,800,1000,1200,1600").split(",")]
 for M in Ms:
-    for N, Kd, epi in ((6144, 4096, 0), (4096, 4096, 2), (28672, 4096, 4), (4096, 14336, 2)):
+    shapes = ((6144, 4096, 0), (4096, 4096, 2), (28672, 4096, 4), (4096, 14336, 2))
+    if os.environ.get("SHAPES") == "70b":  # Llama-3-70B: QKV, O, FFN1 (gate+up), FFN2
+        shapes = ((10240, 8192, 0), (8192, 8192, 2), (57344, 8192, 4), (8192, 28672, 2))
+    for N, Kd, epi in shapes:
         nk = (Kd + 63) // 64
         for var in (0, 1, 2, 3, 5, 6):
             for sp in ((0,) if var in (0, 5, 6) else (1, 2, 3, 4, 6, 8)):
