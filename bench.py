@@ -687,8 +687,8 @@ def run_reference(args, rank, local, world, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)  # p50 over >= 50 restores
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="llama3-8b-8k", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=20.0)
