@@ -667,8 +667,10 @@ def run_reference(args, rank, local, world, dist):
     plan = K.build_plan(spec["L"], spec["n_layers"], r_c, pairs)
     vals = []
     t_all = time.time()
+    # each step a bounded sample: the whole run stays within ~3 minutes
+    per_step = max(0.5, min(args.cpu_budget, 6.0, 180.0 / max(1, args.warmup + args.steps)))
     for _ in range(args.warmup + args.steps):
-        cb = cpu_baseline(args, spec, plan, pairs, budget_s=min(args.cpu_budget, 6.0))
+        cb = cpu_baseline(args, spec, plan, pairs, budget_s=per_step)
         vals.append(cb)
     vals = vals[args.warmup:]
     v = float(np.median([x["value"] for x in vals]))
