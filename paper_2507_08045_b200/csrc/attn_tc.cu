@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -668,6 +669,26 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   const int64_t sms = c.sm_count > 0 ? c.sm_count : 148;
   p.target = int(std::max<int64_t>(4, (total * units_y + sms - 1) / sms));
   p.target = std::max(p.target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
+  {
+    // wave quantisation: the fair share can leave a few items for a second
+    // wave (70B / 32K new-input prefill: 160 items on 148 SMs = two waves of
+    // 28 blocks); take the key-block count per item in [fair, 2 fair] that
+    // minimises waves x blocks per item (ties: fewer splits to merge)
+    const int t0 = p.target;
+    int best_t = t0;
+    int64_t best_cost = INT64_MAX;
+    for (int t = t0; t <= 2 * t0; ++t) {
+      p.target = t;
+      int64_t items_t = 0;
+      for (int qt = 0; qt < p.n_qtiles; ++qt) items_t += attn_nsplit(p, qt);
+      const int64_t cost = (items_t * units_y + sms - 1) / sms * t;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best_t = t;
+      }
+    }
+    p.target = best_t;
+  }
   if (g_attn_target > 0) p.target = std::max(g_attn_target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
   int items = 0, max_split = 1;
   for (int qt = 0; qt < p.n_qtiles; ++qt) {
