@@ -18,6 +18,10 @@
 #include "kb.hpp"
 
 namespace kb {
+CUresult tmap_encode_cached(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* ptr,
+                            const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                            const cuuint32_t* es, CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                            CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob);
 namespace tca {
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -579,20 +583,6 @@ __global__ void __launch_bounds__(128) k_attn_combine(AttnTc p) {
 
 // ---------------------------------------------------------------- host
 namespace {
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeFn encode() {
-  static EncodeFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    KB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (!p) fail(KRUL_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    return reinterpret_cast<EncodeFn>(p);
-  }();
-  return fn;
-}
 CUtensorMap map2d(const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
                   uint32_t box_rows) {
   CUtensorMap m;
@@ -601,7 +591,7 @@ CUtensorMap map2d(const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_ele
   cuuint64_t strides[1] = {ld_elems * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+  CUresult r = tmap_encode_cached(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(KRUL_E_CUDA, "attention tensor map encode failed");

@@ -1090,16 +1090,18 @@ int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int ep
     KB_CUDA(cudaSetDevice(c.device));
     cudaStream_t s = c.s_comp;
     DevBuf a, b, out, res, out2, bias;
-    void* da = a.ensure(size_t(M * K) * 2);
+    // A padded to a 128-row tile like the layer workspaces (Epi::a_rows)
+    void* da = a.ensure(size_t(std::max<int64_t>(M, 128) * K) * 2);
     // weights rotate over >= 320 MB so every launch streams them from HBM as
     // in the restore DAG (one layer's weights fit the 126 MB L2)
     const size_t wbytes = size_t(N * K) * 2;
     const int nb = int(std::max<size_t>(1, ((size_t(320) << 20) + wbytes - 1) / wbytes));
     char* db0 = static_cast<char*>(b.ensure(wbytes * nb));
-    launch_init_uniform(c, s, da, M * K, 1, 1, 1.0f);
+    launch_init_uniform(c, s, da, std::max<int64_t>(M, 128) * K, 1, 1, 1.0f);
     launch_init_uniform(c, s, db0, N * K * nb, 1, 2, 0.02f);
     Epi e;
     e.kind = epi;
+    e.a_rows = std::max<int64_t>(M, 128);
     e.out = out.ensure(size_t(M * N) * 4 + 16);
     e.ldo = epi == Epi::SWIGLU ? N / 2 : N;
     if (epi == Epi::RESID) {

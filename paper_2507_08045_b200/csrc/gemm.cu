@@ -8,6 +8,9 @@
 //  * k_gemm_simt: fp32 CUDA-core tiles for the f32 parity mode (and for
 //    shapes TMA cannot describe, e.g. rows not 16-byte aligned).
 #include <cuda.h>
+#include <unordered_map>
+#include <string>
+#include <mutex>
 
 #include <algorithm>
 #include <cstdlib>
@@ -1081,6 +1084,46 @@ EncodeFn encode_fn() {
   }();
   return fn;
 }
+}  // namespace
+// cuTensorMapEncodeTiled behind a cache keyed by every argument: a map only
+// encodes an address, shape, strides and box (no data), so reuse is exact.
+// Eager paths (decode steps: ~480 maps per token) otherwise spend
+// milliseconds of host time re-encoding identical maps; graph replays
+// carry their maps as kernel parameters and never come here.
+CUresult tmap_encode_cached(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* ptr,
+                            const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                            const cuuint32_t* es, CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                            CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob) {
+  static std::mutex mu;
+  static std::unordered_map<std::string, CUtensorMap> cache;
+  std::string key;
+  key.reserve(160);
+  auto put = [&key](const void* p, size_t n) { key.append(static_cast<const char*>(p), n); };
+  put(&dt, sizeof dt);
+  put(&rank, sizeof rank);
+  put(&ptr, sizeof ptr);
+  put(dims, sizeof(cuuint64_t) * rank);
+  put(strides, sizeof(cuuint64_t) * (rank - 1));
+  put(box, sizeof(cuuint32_t) * rank);
+  put(es, sizeof(cuuint32_t) * rank);
+  put(&il, sizeof il);
+  put(&sw, sizeof sw);
+  put(&l2, sizeof l2);
+  put(&oob, sizeof oob);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *m = it->second;
+    return CUDA_SUCCESS;
+  }
+  const CUresult r = encode_fn()(m, dt, rank, ptr, dims, strides, box, es, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) {
+    if (cache.size() > 8192) cache.clear();
+    cache.emplace(std::move(key), *m);
+  }
+  return r;
+}
+namespace {
 // Row-major bf16 [rows][cols] with leading dimension ld (elements); box
 // [box_rows][64] with 128-byte swizzle.
 CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
@@ -1090,7 +1133,7 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
   cuuint64_t strides[1] = {cuuint64_t(ld * 2)};
   cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+  CUresult r = tmap_encode_cached(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1225,7 +1268,7 @@ bool make_out_map(CUtensorMap* m, const Epi& e, int64_t M, int64_t N, int splits
   cuuint32_t box[3] = {cuuint32_t(128 / esz), 32, 1};
   cuuint32_t es[3] = {1, 1, 1};
   const int rank = k == EK_PARTIAL ? 3 : 2;
-  CUresult r = encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+  CUresult r = tmap_encode_cached(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                            rank, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1287,7 +1330,8 @@ void run_tc2(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CU
 void launch_gemm_tc(const GemmPlan& gp, cudaStream_t s, int64_t M, int64_t N, int64_t K,
                     const void* A, int64_t lda, const void* B, int64_t ldb, const Epi& e,
                     float* partial) {
-  const CUtensorMap ta = make_map(A, M, K, lda, 128);
+  const int64_t a_rows = gp.pair ? M : std::max<int64_t>(M, std::min<int64_t>(e.a_rows, 128));
+  const CUtensorMap ta = make_map(A, a_rows, K, lda, 128);
   const CUtensorMap tb = make_map(B, N, K, ldb, gp.pair ? 128 : gp.bn);
   CUtensorMap tcm;
   int kind = EK_GENERIC;

@@ -224,9 +224,11 @@ Conv* conv_create(Ctx& c, int64_t capacity) {
 }
 
 // ---------------------------------------------------------------- workspaces
+constexpr int64_t kWsMinRows = 128;
 WS ws_get(Ctx& c, int set, int64_t rows) {
   const Cfg& g = c.cfg;
   const size_t r = size_t(std::max<int64_t>(rows, 1));
+  const size_t ra = std::max<size_t>(r, kWsMinRows);  // GEMM A operands: >= one 128-row tile
   WS w;
   DevBuf* h = set == 0 ? &c.ws_h : &c.ws_new_h;
   DevBuf* h2 = set == 0 ? &c.ws_h2 : &c.ws_new_h2;
@@ -239,13 +241,13 @@ WS ws_get(Ctx& c, int set, int64_t rows) {
   DevBuf* act = set == 0 ? &c.ws_act : &c.ws2_act;
   w.h = static_cast<float*>(h->ensure(r * g.d * 4));
   w.h2 = static_cast<float*>(h2->ensure(r * g.d * 4));
-  w.xn = xn->ensure(r * g.d * c.esz);
+  w.xn = xn->ensure(ra * g.d * c.esz);
   w.qkv = static_cast<float*>(qkv->ensure(r * g.nqkv() * 4));
   w.q = q->ensure(r * g.qd() * c.esz);
-  w.attn = at->ensure(r * g.qd() * c.esz);
+  w.attn = at->ensure(ra * g.qd() * c.esz);
   w.hmid = static_cast<float*>(hm->ensure(r * g.d * 4));
-  w.hmidc = hc->ensure(r * g.d * c.esz);
-  w.act = act->ensure(r * g.F * c.esz);
+  w.hmidc = hc->ensure(ra * g.d * c.esz);
+  w.act = act->ensure(ra * g.F * c.esz);
   w.part = set == 0 ? &c.ws_part : &c.ws2_part;
   return w;
 }
@@ -266,6 +268,7 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
     for (int k = 0; k < fs->n_waits; ++k) KB_CUDA(cudaStreamWaitEvent(s, fs->waits[k], 0));
   launch_rmsnorm(c, s, h_in, rows, w.xn);
   Epi e;
+  e.a_rows = kWsMinRows;  // workspace A operands hold >= 128 rows
   if (gemm_uses_tc(c, w.xn, g.d, lw.wqkv, g.d) && g.hd % 32 == 0) {
     // tcgen05 path: RoPE + paged K/V^T scatter + Q fused into the epilogue
     e.kind = Epi::QKV;
@@ -316,6 +319,7 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
   }
   launch_attention(c, s, conv, l, a);
   Epi eo;
+  eo.a_rows = kWsMinRows;  // workspace A operands hold >= 128 rows
   eo.kind = Epi::RESID;
   eo.out = w.hmid;
   eo.ldo = g.d;
@@ -325,6 +329,7 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
   eo.ldo2 = g.d;
   gemm(c, s, out_rows, g.d, g.qd(), w.attn, g.qd(), lw.wo, g.qd(), eo);
   Epi e1;
+  e1.a_rows = kWsMinRows;  // workspace A operands hold >= 128 rows
   e1.out = w.act;
   e1.ldo = g.F;
   if (g.ffn_kind == KRUL_FFN_TANH) {
@@ -339,6 +344,7 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
     gemm(c, s, out_rows, 2 * int64_t(g.F), g.d, w.hmidc, g.d, lw.w1, g.d, e1);
   }
   Epi e2;
+  e2.a_rows = kWsMinRows;  // workspace A operands hold >= 128 rows
   e2.kind = Epi::RESID;
   e2.out = h_out;
   e2.ldo = g.d;

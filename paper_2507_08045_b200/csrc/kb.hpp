@@ -286,6 +286,10 @@ struct Epi {  // GEMM epilogue
   void* out2 = nullptr;          // RESID: optional cdt copy of out
   int64_t ldo2 = 0;
   EpiKV kv;                      // QKV
+  // rows of A the caller has allocated (>= M; 0 = M): with M < 128 the
+  // 1-SM kernel then loads real (ignored) rows instead of TMA out-of-bounds
+  // fill, measured 77 -> 55 us on the M = 1 FFN1 (layer workspaces hold 128)
+  int64_t a_rows = 0;
 };
 
 extern int g_gemm_force, g_gemm_splits;  // debug knobs (krul_debug_gemm_bench)
