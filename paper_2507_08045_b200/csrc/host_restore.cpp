@@ -224,6 +224,22 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   for (size_t bi = 0; bi < snap.blobs.size(); ++bi) {
     const auto& b = snap.blobs[bi];
     KB_CUDA(cudaStreamWaitEvent(c.s_exp, copied[bi], 0));
+    static const bool fuse_env = [] {
+      const char* v = std::getenv("KRUL_DECODE_EXPAND");
+      return !(v && v[0] == '0');
+    }();
+    if (snap.coded && b.cbytes && g.hd == kEcLaneSyms && c.esz == 2 && fuse_env) {
+      // decode straight into the owners' pages (one pass, one launch)
+      const int64_t from[2] = {p[size_t(b.owners[0])], b.owners[1] >= 0 ? p[size_t(b.owners[1])] : L};
+      launch_ec_decode_expand(c, c.s_exp, cstg + b.coff, int64_t(b.ec_chunks), snap.lut_dev.as<uint16_t>(),
+                              b.start, L, conv, b.owners, from);
+      for (int o : b.owners) {
+        if (o < 0) continue;
+        expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;
+        record_mark(loaded[o], c.s_exp);
+      }
+      continue;
+    }
     if (snap.coded && b.cbytes) {
       cudaEvent_t kt0 = kt_begin(c, c.s_exp);
       launch_ec_decode(c.s_exp, cstg + b.coff, int64_t(b.ec_chunks), snap.lut_dev.as<uint16_t>(), stg + b.off);

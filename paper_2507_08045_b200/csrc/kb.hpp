@@ -346,6 +346,10 @@ void launch_kv_scatter_f32(const Ctx& c, cudaStream_t s, const Conv& conv, int l
                            int64_t start, int64_t end, const float* k, const float* v);
 // Blob (cdt [2][Hkv][rows][hd], rows = [blob_start, L)) -> pages of `layer`
 // for positions [from, L).
+// coded blob -> owners' pages in one pass (kvcode format, bf16, hd = 128)
+void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t n_chunks,
+                             const uint16_t* lut, int64_t blob_start, int64_t L, const Conv& conv,
+                             const int* owners, const int64_t* from);
 void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start,
                    int64_t L, const Conv& conv, int layer, int64_t from);
 // Pages -> blob (compress, K8); mean-merge rows [merge_from, L) with `other`.

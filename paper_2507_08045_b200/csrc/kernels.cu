@@ -9,6 +9,7 @@
 
 #include "kb.hpp"
 #include "dev.cuh"
+#include "kvcode.hpp"
 
 namespace kb {
 
@@ -861,6 +862,111 @@ __global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView 
     expand_tile(blob, blob_start, L, pv, from, ti, tile);
     __syncthreads();
   }
+}
+
+// K4b + K5 fused (coded store, hd = 128): one warp decodes a 4096-element
+// chunk of the coded blob; with hd equal to a lane's 128-element stream,
+// lane j holds exactly one row of the blob — token blob_start + r of head g,
+// K or V — and writes it straight into the owners' pages: K rows as 16-byte
+// stores, V^T columns as per-dimension stores that are contiguous across
+// the warp's 32 consecutive tokens. No raw staging round trip, one launch
+// per blob instead of decode + one expand per owner.
+__global__ void __launch_bounds__(128) k_ec_decode_expand(const uint8_t* __restrict__ blob,
+                                                          const uint16_t* __restrict__ lut,
+                                                          int64_t blob_start, int64_t rows, PageView pv0,
+                                                          int64_t from0, PageView pv1, int64_t from1,
+                                                          int n_owners) {
+  constexpr int kWarps = 4;
+  __shared__ uint16_t s_lut[1 << kEcMaxLen];
+  __shared__ uint32_t s_w[kWarps][32 * kEcMaxLaneWords + 2];
+  for (int i = threadIdx.x; i < (1 << kEcMaxLen); i += blockDim.x) s_lut[i] = lut[i];
+  __syncthreads();
+  const EcHeader h = *reinterpret_cast<const EcHeader*>(blob);
+  const uint32_t* base_t = reinterpret_cast<const uint32_t*>(blob + h.base_off);
+  const uint8_t* cnt_t = blob + h.cnt_off;
+  const uint8_t* sm = blob + h.sm_off;
+  const uint32_t* ex = reinterpret_cast<const uint32_t*>(blob + h.exp_off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* sw = s_w[warp];
+  const int64_t n = int64_t(h.n_elems), nrows = n / 128;
+  const int Hkv = pv0.Hkv;
+  for (int64_t ch = blockIdx.x * int64_t(kWarps) + warp; ch < h.n_chunks; ch += int64_t(gridDim.x) * kWarps) {
+    const uint32_t base = __ldg(base_t + ch), total = __ldg(base_t + ch + 1) - base;
+    const uint32_t c = __ldg(cnt_t + ch * 32 + lane);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t my = inc - c;
+    __syncwarp();
+    for (uint32_t i = lane; i < total + 1; i += 32) sw[i] = __ldg(ex + base + i);
+    __syncwarp();
+    const int64_t R = ch * 32 + lane;  // flattened (kv, g, r) row of this lane
+    const bool live = R < nrows;
+    const int64_t r = live ? R % rows : 0;
+    const int64_t hg = live ? R / rows : 0;
+    const int isv = int(hg / Hkv), g = int(hg % Hkv);
+    const int64_t pos = blob_start + r;
+    const bool w0 = live && pos >= from0, w1 = live && n_owners > 1 && pos >= from1;
+    const int64_t e0 = R * 128;
+    uint32_t idx = my, wa = sw[idx], wb = sw[idx + 1], bo = 0;
+#pragma unroll 1
+    for (int gq = 0; gq < 8; ++gq) {  // 16 elements per group
+      uint32_t o[8];
+      if (live) {
+        const uint4 sv = __ldg(reinterpret_cast<const uint4*>(sm + e0) + gq);
+        const uint32_t sb[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const uint32_t win = __funnelshift_l(wb, wa, bo);
+          const uint32_t e = s_lut[win >> (32 - kEcMaxLen)];
+          bo += e >> 8;
+          if (bo >= 32) {
+            bo -= 32;
+            wa = wb;
+            wb = sw[++idx + 1];
+          }
+          const uint32_t sbyte = (sb[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+          const uint32_t v = ((sbyte & 0x80u) << 8) | ((e & 0xFFu) << 7) | (sbyte & 0x7Fu);
+          if (k & 1) o[k >> 1] |= v << 16;
+          else o[k >> 1] = v;
+        }
+      }
+      for (int ow = 0; ow < 2; ++ow) {
+        const bool wr = ow == 0 ? w0 : w1;
+        const PageView& pv = ow == 0 ? pv0 : pv1;
+        if (!wr) continue;
+        bf16* page = reinterpret_cast<bf16*>(pv.page(pos));
+        if (!isv) {
+          uint4* dst = reinterpret_cast<uint4*>(page + pv.k_off(g, pos, 16 * gq));
+          dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {
+          uint16_t* vt = reinterpret_cast<uint16_t*>(page) + pv.v_off(g, pos, 16 * gq);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) vt[int64_t(k) * kPageTokens] = uint16_t(o[k >> 1] >> (16 * (k & 1)));
+        }
+      }
+    }
+  }
+}
+void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t n_chunks,
+                             const uint16_t* lut, int64_t blob_start, int64_t L, const Conv& conv,
+                             const int* owners, const int64_t* from) {
+  if (n_chunks <= 0) return;
+  const int no = owners[1] >= 0 ? 2 : 1;
+  const PageView pv0 = page_view(c, conv, owners[0]);
+  const PageView pv1 = no > 1 ? page_view(c, conv, owners[1]) : pv0;
+  const unsigned blocks = unsigned(std::min<int64_t>((n_chunks + 3) / 4, 148 * 6));
+  cudaEvent_t kt0 = kt_begin(c, s);
+  k_ec_decode_expand<<<blocks, 128, 0, s>>>(static_cast<const uint8_t*>(blob), lut, blob_start, L - blob_start,
+                                            pv0, from[0], pv1, no > 1 ? from[1] : L, no);
+  KB_LAUNCH();
+  double bytes = 0;
+  for (int i = 0; i < no; ++i) bytes += 2.0 * double(L - from[i]) * c.cfg.Hkv * c.cfg.hd * 2.0;
+  kt_end(c, s, kt0, KT_DECODE, 0.0, bytes);
 }
 
 void launch_expand_impl(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,
