@@ -17,6 +17,7 @@
 // doubles with nlohmann's fixed/exponent switch at 10^-5 / 10^15), so a
 // container saved here is bit-identical to the reference's save of the same
 // f32 snapshot (tests/test_container.py pins it against nlohmann 3.11.3).
+#include <locale.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <fcntl.h>
@@ -669,7 +670,9 @@ struct JParser {
       }
     }
     v.t = JV::DBL;
-    v.d = std::strtod(t.c_str(), nullptr);
+    // "C" locale: the process locale must not change the decimal point
+    static const locale_t c_loc = newlocale(LC_ALL_MASK, "C", locale_t(0));
+    v.d = strtod_l(t.c_str(), nullptr, c_loc);
     if (!std::isfinite(v.d)) bad("number overflow");  // nlohmann rejects, no inf
     return v;
   }
