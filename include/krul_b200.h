@@ -191,6 +191,14 @@ int krul_select(krul_ctx* ctx, const double* D, const int* dm_layers, int n,
                 const int* ir_layers, int n_ir, double r_l, int n_layers,
                 krul_pair* out, int* n_out, int* exhausted);
 
+/* validate_strategy (strategy.cpp:76-131): violation bitmask 1 pair
+ * orientation, 2 layer range, 4 non-I-R member, 8 layer reuse, 16 distance
+ * order, 32 shared size, 64 quota shortfall; `details` (optional) receives
+ * the reference's "kind: detail" lines, newline-separated. */
+int krul_validate_strategy(const krul_pair* pairs, int n_pairs, const int* shared, int n_shared,
+                           int exhausted, const int* ir_layers, int n_ir, int n_layers, double r_l,
+                           int* mask, char* details, size_t details_cap);
+
 /* ---- scheduler (scheduler.cpp:15-318), host --------------------------- */
 int krul_build_plan(int64_t L, int n_layers, double r_c, const krul_pair* pairs,
                     int n_pairs, int64_t* recompute_len);
@@ -374,8 +382,9 @@ int krul_set_concurrency(krul_ctx* ctx, int two_stream);
  * krul_launch_count: number of kernels this library has launched (process
  * wide). krul_ktime_*: per-launch CUDA-event timing of instrumented kernel
  * classes (tag: 0 GEMM, 1 attention, 2 expand, 3 decode fold, 4 prefill
- * fold, 5 selector, 6 compress, 7 weight-streaming GEMM with M <= 128) with
- * their algorithmic flops / bytes. */
+ * fold, 5 selector, 6 compress, 7 weight-streaming GEMM with M <= 128, 8 blob
+ * decode, 9 LM-head GEMV, 10 fused decode + expand) with their algorithmic
+ * flops / bytes. */
 int krul_launch_count(uint64_t* n);
 int krul_ktime_enable(krul_ctx* ctx, int on);
 int krul_ktime_read(krul_ctx* ctx, int tag, int64_t* launches, double* ms, double* flops,

@@ -344,6 +344,19 @@ int kro_select(const double* D, const int* dm_layers, int n, const int* ir, int 
   });
 }
 
+// strategy.cpp:76-131 (bitmask of violation kinds, krul_oracle.hpp)
+int kro_validate_strategy(const int* sh, const int* dp, const double* dist, int np, const int* shared,
+                          int n_shared, int exhausted, const int* ir, int n_ir, int n_layers, double r_l,
+                          int* mask) {
+  return guard([&] {
+    Strategy s;
+    for (int i = 0; i < np; ++i) s.pairs.push_back({sh[i], dp[i], dist[i]});
+    s.shared = std::set<int>(shared, shared + n_shared);
+    s.exhausted = exhausted != 0;
+    *mask = validate_strategy(s, std::vector<int>(ir, ir + n_ir), n_layers, r_l);
+  });
+}
+
 // ---- plans / scheduler ----------------------------------------------------
 int kro_build_plan(int64_t L, int N, double r_c, const int* sh, const int* dp, int np, int64_t* out) {
   return guard([&] {

@@ -393,6 +393,20 @@ def select_strategy(D, dm_layers, ir_layers, r_l, n_layers) -> Strategy:
                     bool(exh.value))
 
 
+def validate_strategy(pairs, shared, exhausted, ir_layers, n_layers, r_l) -> int:
+    """strategy.cpp:76-131 -> violation bitmask (krul_oracle.hpp)."""
+    sh = np.ascontiguousarray([p[0] for p in pairs] or [0], np.int32)
+    dp = np.ascontiguousarray([p[1] for p in pairs] or [0], np.int32)
+    ds = np.ascontiguousarray([p[2] for p in pairs] or [0.0], np.float64)
+    sd = np.ascontiguousarray(list(shared) or [0], np.int32)
+    ir = np.ascontiguousarray(list(ir_layers) or [0], np.int32)
+    m = C.c_int()
+    _check(lib().kro_validate_strategy(_p(sh), _p(dp), _p(ds), len(pairs), _p(sd), len(list(shared)),
+                                       int(bool(exhausted)), _p(ir), len(list(ir_layers)), n_layers,
+                                       C.c_double(r_l), C.byref(m)))
+    return m.value
+
+
 # ---- scheduler --------------------------------------------------------------
 
 def build_plan(L, N, r_c, strategy: Strategy | None = None):

@@ -546,6 +546,24 @@ int krul_calibrate_rc(const krul_cost_model* cost, int N, int64_t L, int64_t d,
 int krul_validate_plan(int64_t L, const int64_t* p, int N, const krul_pair* pairs, int np, int* mask) {
   return guard([&] { *mask = validate_plan(L, std::vector<int64_t>(p, p + N), pairs, np); });
 }
+int krul_validate_strategy(const krul_pair* pairs, int n_pairs, const int* shared, int n_shared,
+                           int exhausted, const int* ir_layers, int n_ir, int n_layers, double r_l,
+                           int* mask, char* details, size_t details_cap) {
+  return guard([&] {
+    need(mask, "mask");
+    if (n_pairs > 0) need(pairs, "pairs");
+    if (n_shared > 0) need(shared, "shared");
+    if (n_ir > 0) need(ir_layers, "ir_layers");
+    std::string lines;
+    *mask = validate_strategy(pairs, n_pairs, std::set<int>(shared, shared + std::max(n_shared, 0)),
+                              exhausted != 0, std::set<int>(ir_layers, ir_layers + std::max(n_ir, 0)),
+                              n_layers, r_l, &lines);
+    if (details && details_cap) {
+      std::strncpy(details, lines.c_str(), details_cap - 1);
+      details[details_cap - 1] = 0;
+    }
+  });
+}
 int krul_blob_specs(int64_t L, const int64_t* p, int N, const krul_pair* pairs, int np,
                     krul_blob_spec* out, int* n_out) {
   return guard([&] {

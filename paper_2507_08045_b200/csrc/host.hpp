@@ -1,5 +1,6 @@
 // host.hpp — host-side building blocks shared by the C ABI translation units.
 #pragma once
+#include <set>
 #include <string>
 #include <vector>
 
@@ -69,6 +70,8 @@ double calibrate(const Cost& c, int N, int64_t L, int64_t d, const krul_pair* pa
                  const double* grid, int ng);
 std::vector<double> default_grid(double step);
 int validate_plan(int64_t L, const std::vector<int64_t>& p, const krul_pair* pairs, int np);
+int validate_strategy(const krul_pair* pairs, int np, const std::set<int>& shared, bool exhausted,
+                      const std::set<int>& ir, int n_layers, double r_l, std::string* lines);
 
 // ---- compressed KV store ---------------------------------------------------
 // Container metadata the hot path does not use but the KRUL v1 container

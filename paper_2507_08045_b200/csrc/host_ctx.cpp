@@ -194,6 +194,7 @@ cudaEvent_t Ctx::event() {
 
 Conv::~Conv() {
   if (ctx) {
+    if (ctx->rg.conv_serial == serial) ctx->drop_graph();  // its kernels hold d_pt
     for (int p : pages) ctx->free_pages.push_back(p);
   }
   if (d_pt) cudaFree(d_pt);

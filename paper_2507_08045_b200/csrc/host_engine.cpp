@@ -212,6 +212,7 @@ Conv* conv_create(Ctx& c, int64_t capacity) {
   v->ctx = &c;
   v->capacity = capacity;
   v->max_pages = maxp;
+  v->serial = next_serial();
   v->pages.resize(need);
   for (size_t i = 0; i < need; ++i) {
     v->pages[i] = c.free_pages.back();
@@ -219,6 +220,7 @@ Conv* conv_create(Ctx& c, int64_t capacity) {
   }
   KB_CUDA(cudaSetDevice(c.device));
   KB_CUDA(cudaMalloc(&v->d_pt, need * sizeof(int)));
+  g_buf_gen.fetch_add(1);  // a captured graph never outlives the page tables it baked in
   KB_CUDA(kb_memcpy_sync(v->d_pt, v->pages.data(), need * sizeof(int), cudaMemcpyHostToDevice));
   return v;
 }

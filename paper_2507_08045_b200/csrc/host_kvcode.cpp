@@ -197,6 +197,8 @@ const char* snapshot_raw_blob(const Snapshot& s, int b, std::vector<uint16_t>& t
 // device image -> encode kernel -> one D2H of the whole coded image.
 void snapshot_encode(Ctx& c, Snapshot& s, const char* dev_raw, cudaStream_t st) {
   if (s.esz != 2) fail(KRUL_E_CONFIG, "exponent coding needs a bf16 store");
+  for (const auto& b : s.blobs)
+    if (!ec_fits(b.bytes / 2)) fail(KRUL_E_SNAPSHOT, "blob too large for the coded store (u32 image offsets)");
   DevBuf d_hist, d_code, d_words, d_img;
   auto* hist = static_cast<unsigned long long*>(d_hist.ensure(256 * 8));
   KB_CUDA(cudaMemsetAsync(hist, 0, 256 * 8, st));

@@ -5,6 +5,8 @@
 // (same products, same llround, same nudge order); only the cost model gains
 // optional GQA / bf16 / SwiGLU terms (zero = the reference formula).
 #include <algorithm>
+#include <set>
+#include <string>
 #include <cmath>
 #include <limits>
 #include <map>
@@ -214,6 +216,43 @@ int validate_plan_snapshot(const std::vector<int64_t>& p, int64_t L, const Snaps
     if (bl.end != L || bl.start > p[size_t(l)]) m |= 8;
   }
   return m;
+}
+
+// strategy.cpp:76-131 — every violation in the reference's order, as a
+// bitmask (1 pair orientation, 2 layer range, 4 non-I-R member, 8 layer
+// reuse, 16 distance order, 32 shared size, 64 quota shortfall) plus the
+// reference's "kind: detail" lines.
+int validate_strategy(const krul_pair* pairs, int np, const std::set<int>& shared, bool exhausted,
+                      const std::set<int>& ir, int n_layers, double r_l, std::string* lines) {
+  int mask = 0;
+  auto note = [&](int bit, const char* kind, const std::string& detail) {
+    mask |= bit;
+    if (lines) *lines += std::string(kind) + ": " + detail + "\n";
+  };
+  std::set<int> seen;
+  double last = -1.0;
+  for (int k = 0; k < np; ++k) {
+    const krul_pair& pr = pairs[k];
+    const std::string tag = "(" + std::to_string(pr.shallow) + "," + std::to_string(pr.deep) + ")";
+    if (pr.shallow >= pr.deep) note(1, "pair orientation", "pair " + tag + " is not ordered shallow<deep");
+    for (const int m : {pr.shallow, pr.deep}) {
+      if (m < 0 || m >= n_layers)
+        note(2, "layer range", "layer " + std::to_string(m) + " outside [0, " + std::to_string(n_layers) + ")");
+      if (!ir.count(m)) note(4, "non-I-R member", "layer " + std::to_string(m) + " in pair " + tag);
+      if (!seen.insert(m).second) note(8, "layer reuse", "layer " + std::to_string(m) + " appears in two pairs");
+    }
+    if (pr.distance < last) note(16, "distance order", "pair " + tag + " breaks the non-decreasing selection order");
+    last = pr.distance;
+  }
+  if (shared != seen)
+    note(32, "shared size", "shared set does not equal the union of pair members");
+  else if (shared.size() != 2 * size_t(np))
+    note(32, "shared size", "|shared| != 2 * |pairs|");
+  const int q = quota(n_layers, r_l);
+  if (int(shared.size()) < q && !exhausted)
+    note(64, "quota shortfall", "|shared| = " + std::to_string(shared.size()) + " below quota " +
+                                    std::to_string(q) + " without the exhaustion flag");
+  return mask;
 }
 
 }  // namespace kb

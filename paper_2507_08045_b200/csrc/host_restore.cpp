@@ -89,8 +89,9 @@ Snapshot* snapshot_compress(Ctx& c, Conv& conv, const krul_pair* pairs, int np, 
   if (mode != KRUL_MERGE_MEAN && mode != KRUL_MERGE_KEEP_DEEPER) fail(KRUL_E_CONFIG, "unknown merge mode");
   if (conv.len != L) fail(KRUL_E_SNAPSHOT, "cache span does not cover the plan's history");
   std::unique_ptr<Snapshot> s(new_snapshot(c, pairs, np, p, L, mode));
-  const bool code = coding_on(c);
-  layout_blobs(c, *s, !code);
+  layout_blobs(c, *s, false);
+  bool code = coding_on(c);
+  for (const auto& b : s->blobs) code = code && ec_fits(b.bytes / 2);  // u32 image offsets
   KB_CUDA(cudaSetDevice(c.device));
   cudaStream_t st = c.s_load;
   char* stg = static_cast<char*>(c.staging.ensure(std::max<size_t>(s->total, 256)));
@@ -232,7 +233,7 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
       // decode straight into the owners' pages (one pass, one launch)
       const int64_t from[2] = {p[size_t(b.owners[0])], b.owners[1] >= 0 ? p[size_t(b.owners[1])] : L};
       launch_ec_decode_expand(c, c.s_exp, cstg + b.coff, int64_t(b.ec_chunks), snap.lut_dev.as<uint16_t>(),
-                              b.start, L, conv, b.owners, from);
+                              b.start, L, conv, b.owners, from, double(b.cbytes));
       for (int o : b.owners) {
         if (o < 0) continue;
         expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;
@@ -349,14 +350,14 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   c.ws_logits.ensure(size_t(g.V) * 4);
 
   auto& G = c.rg;
-  const bool same = G.snap_serial == snap.serial && G.conv == &conv && G.L == L && G.n_new == nn &&
+  const bool same = G.snap_serial == snap.serial && G.conv_serial == conv.serial && G.L == L && G.n_new == nn &&
                     G.kt_on == c.kt.on && G.logits == (lp != nullptr) &&
                     G.capture_probs == c.capture_probs && G.buf_gen == g_buf_gen.load() &&
                     G.two_stream == c.two_stream && G.fused == c.fused && G.timeline == c.timeline;
   if (!same) {
     c.drop_graph();
     G.snap_serial = snap.serial;
-    G.conv = &conv;
+    G.conv_serial = conv.serial;
     G.L = L;
     G.n_new = nn;
     G.kt_on = c.kt.on;

@@ -126,6 +126,9 @@ struct Conv {
   int max_pages = 0;
   std::vector<int> pages;  // host copy [N][max_pages]
   int* d_pt = nullptr;     // device page table [N][max_pages]
+  // unique per conversation object: the restore-graph cache key (a freed
+  // Conv's heap address can be reused by the next one)
+  uint64_t serial = 0;
   ~Conv();
 };
 
@@ -137,7 +140,7 @@ struct Est;
 // class from the same timed step.
 enum KTag { KT_GEMM = 0, KT_ATTN = 1, KT_EXPAND = 2, KT_FOLD_DECODE = 3, KT_FOLD_PREFILL = 4,
             KT_SELECT = 5, KT_COMPRESS = 6, KT_GEMM_STREAM = 7, KT_DECODE = 8, KT_LOGITS = 9,
-            KT_NTAGS = 10 };
+            KT_DECODE_EXPAND = 10, KT_NTAGS = 11 };
 struct KTime {
   bool on = false;
   struct Rec {
@@ -220,7 +223,7 @@ struct Ctx {
   // CUDA graph of the last restore DAG (replayed when the key repeats)
   struct RestoreGraph {
     uint64_t snap_serial = 0;
-    const void* conv = nullptr;
+    uint64_t conv_serial = 0;
     int64_t L = -1, n_new = -1;
     bool kt_on = false, logits = false;
     int capture_probs = -1;
@@ -349,7 +352,7 @@ void launch_kv_scatter_f32(const Ctx& c, cudaStream_t s, const Conv& conv, int l
 // coded blob -> owners' pages in one pass (kvcode format, bf16, hd = 128)
 void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t n_chunks,
                              const uint16_t* lut, int64_t blob_start, int64_t L, const Conv& conv,
-                             const int* owners, const int64_t* from);
+                             const int* owners, const int64_t* from, double coded_bytes);
 void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start,
                    int64_t L, const Conv& conv, int layer, int64_t from);
 // Pages -> blob (compress, K8); mean-merge rows [merge_from, L) with `other`.

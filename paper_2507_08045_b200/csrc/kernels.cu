@@ -940,9 +940,12 @@ __global__ void __launch_bounds__(128) k_ec_decode_expand(const uint8_t* __restr
         if (!wr) continue;
         bf16* page = reinterpret_cast<bf16*>(pv.page(pos));
         if (!isv) {
-          uint4* dst = reinterpret_cast<uint4*>(page + pv.k_off(g, pos, 16 * gq));
-          dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-          dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+          // one 32-byte store per lane (STG.256): a whole L2 sector, where two
+          // 16-byte stores wrote every sector in halves (2x SM->L2 traffic)
+          bf16* dst = page + pv.k_off(g, pos, 16 * gq);
+          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(o[0]),
+                       "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                       : "memory");
         } else {
           uint16_t* vt = reinterpret_cast<uint16_t*>(page) + pv.v_off(g, pos, 16 * gq);
 #pragma unroll
@@ -954,7 +957,7 @@ __global__ void __launch_bounds__(128) k_ec_decode_expand(const uint8_t* __restr
 }
 void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t n_chunks,
                              const uint16_t* lut, int64_t blob_start, int64_t L, const Conv& conv,
-                             const int* owners, const int64_t* from) {
+                             const int* owners, const int64_t* from, double coded_bytes) {
   if (n_chunks <= 0) return;
   const int no = owners[1] >= 0 ? 2 : 1;
   const PageView pv0 = page_view(c, conv, owners[0]);
@@ -964,9 +967,10 @@ void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int
   k_ec_decode_expand<<<blocks, 128, 0, s>>>(static_cast<const uint8_t*>(blob), lut, blob_start, L - blob_start,
                                             pv0, from[0], pv1, no > 1 ? from[1] : L, no);
   KB_LAUNCH();
-  double bytes = 0;
+  // algorithmic bytes: the coded image read once + every owner's pages written
+  double bytes = coded_bytes;
   for (int i = 0; i < no; ++i) bytes += 2.0 * double(L - from[i]) * c.cfg.Hkv * c.cfg.hd * 2.0;
-  kt_end(c, s, kt0, KT_DECODE, 0.0, bytes);
+  kt_end(c, s, kt0, KT_DECODE_EXPAND, 0.0, bytes);
 }
 
 void launch_expand_impl(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start, int64_t L,

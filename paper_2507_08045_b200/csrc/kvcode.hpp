@@ -43,6 +43,15 @@ struct EcCode {
 EcCode ec_build_code(const uint64_t* hist);
 
 inline size_t ec_align16(size_t x) { return (x + 15) & ~size_t(15); }
+// The image's section offsets, element count and lane offsets are u32: a
+// blob fits the coded format when its worst-case image (every exponent at
+// the longest code) stays below 4 GiB. Larger blobs stay in the raw store.
+inline bool ec_fits(uint64_t n) {
+  const uint64_t chunks = (n + kEcChunk - 1) / kEcChunk;
+  const uint64_t worst = 64 + 4 * (chunks + 1) + 32 * chunks + n +
+                         4 * (chunks * 32 * uint64_t(kEcMaxLaneWords) + 1) + 64;
+  return worst < (uint64_t(1) << 32);
+}
 // Section offsets of a coded blob of n elements whose streams hold exp_words.
 inline void ec_layout(uint64_t n, uint64_t exp_words, EcHeader* h, size_t* total) {
   const uint64_t chunks = (n + kEcChunk - 1) / kEcChunk;

@@ -515,6 +515,25 @@ def select_strategy(ctx: Context, D, dm_layers, ir_layers, r_l, n_layers) -> Com
                                 for i in range(n.value)], bool(ex.value))
 
 
+VIOLATION_KINDS = {1: "pair orientation", 2: "layer range", 4: "non-I-R member", 8: "layer reuse",
+                   16: "distance order", 32: "shared size", 64: "quota shortfall"}
+
+
+def validate_strategy(strategy: CompressionStrategy, ir_layers, n_layers, r_l, shared=None):
+    """strategy.cpp:76-131 -> (bitmask, ["kind: detail", ...]). `shared`
+    defaults to the union of the pair members (CompressionStrategy::shared)."""
+    arr, n = _pairs(strategy.pairs)
+    sh = list(strategy.shared if shared is None else shared)
+    sd = np.ascontiguousarray(sh or [0], np.int32)
+    ir = np.ascontiguousarray(list(ir_layers) or [0], np.int32)
+    m = C.c_int()
+    buf = C.create_string_buffer(8192)
+    _check(lib().krul_validate_strategy(arr, n, _p(sd), len(sh), int(bool(strategy.exhausted_before_quota)),
+                                        _p(ir), len(list(ir_layers)), n_layers, C.c_double(r_l),
+                                        C.byref(m), buf, C.c_size_t(len(buf))))
+    return m.value, [x for x in buf.value.decode().split("\n") if x]
+
+
 # ---- scheduler (scheduler.hpp:14-112) ----------------------------------------
 
 @dataclass

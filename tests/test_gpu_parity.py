@@ -850,3 +850,40 @@ def test_decode_attention_split_keys_matches_simt(K, oracle):
             assert np.abs(rows[0] - rr[0]).max() < 1e-5  # layer 0: identical inputs
             assert rel_fro(rows, rr) < 2e-2              # deeper: bf16 hidden-state drift
             np.testing.assert_allclose(rows.reshape(-1, rows.shape[-1]).sum(axis=-1), 1.0, atol=1e-4)
+
+
+def test_calibrate_rc_measured_contract(K, oracle):
+    """calibrate_rc_measured (scheduler.cpp:402-443) on the device and its
+    TTFT variant: the result is a grid member and the argmin of the measured
+    objective the call returns (|T_C - T_L| with the reference's strict `<`,
+    ties -> the smaller ratio; median TTFT); the measured stream rates feed a
+    cost model whose analytic calibration is also a grid member."""
+    shape = dict(n_layers=4, n_heads=4, n_kv_heads=2, head_dim=128, d_model=512, vocab_size=512,
+                 ffn_mult=3.5, ffn_kind=1, seed=3)
+    cfg = K.ModelConfig(**shape, dtype=K.KRUL_BF16, max_tokens=1280)
+    ctx = K.Context(cfg, 0)
+    ctx.init_weights(3)
+    L = 1024
+    hist = np.random.default_rng(1).integers(0, cfg.vocab_size, L, dtype=np.int32)
+    new = np.random.default_rng(2).integers(0, cfg.vocab_size, 32, dtype=np.int32)
+    prev, scratch = ctx.conversation(1280), ctx.conversation(1280)
+    ctx.prefill(prev, hist)
+    grid = [0.0, 0.1, 0.25, 0.5, 1.0]
+    pairs = [(1, 2, 0.0)]
+    r, tc, tl = ctx.calibrate_rc_measured(prev, scratch, hist, pairs, grid)
+    assert r in grid
+    d = np.abs(tc - tl)
+    best = 0
+    for i in range(1, len(grid)):
+        if d[i] < d[best]:
+            best = i
+    assert r == sorted(grid)[best]
+    assert tc[0] == 0 or tc[0] < tc[-1]  # more recompute costs more compute time
+    assert tl[-1] <= tl[0]               # and less load
+    r2, tt = ctx.calibrate_rc_ttft(prev, scratch, hist, new, pairs, grid, reps=3)
+    assert r2 in grid and r2 == sorted(grid)[int(np.argmin(tt))]
+    assert np.all(tt > 0)
+    b, f = ctx.measure_rates(scratch)
+    assert b > 1e9 and f > 1e12
+    cm = K.CostModel.for_model(cfg, f, b)
+    assert K.calibrate_rc(cm, cfg.n_layers, L, cfg.d_model, pairs) in list(K.default_rc_grid())

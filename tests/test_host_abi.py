@@ -148,3 +148,43 @@ def test_config_hash_matches_oracle(K, oracle):
                dict(n_layers=32, n_heads=32, head_dim=128, d_model=4096, vocab_size=128256,
                     n_kv_heads=8, ffn_kind=1, rope_theta=500000.0, ffn_mult=3.5)):
         assert K.ModelConfig(**kw).hash() == oracle.ModelConfig(**kw).hash()
+
+
+def test_validate_strategy_reference_kats(K):  # test_strategy.cpp:200-254
+    ir, n, r_l = [0, 1, 2, 3], 8, 0.5
+    S = K.CompressionStrategy
+
+    def kinds(s, shared=None):
+        return {line.split(":")[0] for line in K.validate_strategy(s, ir, n, r_l, shared)[1]}
+
+    good = S([(0, 1, 0.5), (2, 3, 0.7)])
+    assert K.validate_strategy(good, ir, n, r_l) == (0, [])
+    assert "pair orientation" in kinds(S([(1, 0, 0.5), (2, 3, 0.7)]))
+    assert "layer range" in kinds(S([(0, 1, 0.5), (2, 9, 0.7)]))
+    assert "non-I-R member" in kinds(S([(0, 1, 0.5), (2, 4, 0.7)]))
+    assert "layer reuse" in kinds(S([(0, 1, 0.5), (1, 2, 0.7)]), shared=[0, 1, 2])
+    assert "distance order" in kinds(S([(2, 3, 0.7), (0, 1, 0.5)]))
+    assert "shared size" in kinds(good, shared=[0, 1, 2])
+    short = S([(0, 1, 0.5)])
+    assert "quota shortfall" in kinds(short)
+    short.exhausted_before_quota = True
+    assert "quota shortfall" not in kinds(short)
+
+
+def test_validate_strategy_matches_oracle_random(K, oracle):
+    rng = np.random.default_rng(11)
+    for _ in range(500):
+        n = 2 + int(rng.integers(20))
+        ir = sorted(set(int(x) for x in rng.integers(-1, n + 2, int(rng.integers(0, n + 1)))))
+        pairs = []
+        for _ in range(int(rng.integers(0, 5))):
+            a, b = (int(x) for x in rng.integers(-1, n + 1, 2))
+            pairs.append((a, b, float(rng.integers(0, 4)) / 4))
+        shared = sorted({x for p in pairs for x in p[:2]})
+        if rng.random() < 0.3 and shared:
+            shared = shared[:-1]
+        ex = bool(rng.random() < 0.3)
+        r_l = float(rng.integers(0, 5)) / 4
+        m, lines = K.validate_strategy(K.CompressionStrategy(pairs, ex), ir, n, r_l, shared)
+        assert m == oracle.validate_strategy(pairs, shared, ex, ir, n, r_l), (pairs, shared, ex, ir, n, r_l)
+        assert bool(lines) == bool(m)
