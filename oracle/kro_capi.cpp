@@ -6,6 +6,8 @@
 // kro_last_error copies the message of the last failure on this thread.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <omp.h>
 #include <cstring>
 #include <string>
 
@@ -120,6 +122,83 @@ int kro_model_build(const kro_cfg* c, void** out) {
   return guard([&] { *out = new Model(build_model(to_cfg(c))); });
 }
 void kro_model_free(void* m) { delete static_cast<Model*>(m); }
+
+// Timing-only model (bench CPU legs at the Llama shapes): the reference's
+// layout and U[-1/sqrt(d), 1/sqrt(d)) bound, but filled in parallel from a
+// counter-based hash instead of the sequential mt19937_64 draw (which takes
+// minutes for 8 B weights). Not a parity model.
+int kro_model_build_fast(const kro_cfg* c, uint64_t seed, void** out) {
+  return guard([&] {
+    const ModelConfig cfg = to_cfg(c);
+    cfg.validate();
+    auto* m = new Model;
+    m->cfg = cfg;
+    const float bound = 1.0f / std::sqrt(float(cfg.d_model));
+    const int64_t d = cfg.d_model, F = cfg.ffn_hidden();
+    const int64_t qd = int64_t(cfg.n_heads) * cfg.head_dim, kvd = int64_t(cfg.kv_heads()) * cfg.head_dim;
+    uint64_t stream = 0;
+    auto fill = [&](std::vector<float>& v) {
+      const uint64_t sid = ++stream;
+      const int64_t n = int64_t(v.size());
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < n; ++i) {
+        uint64_t z = seed ^ (sid << 40) ^ uint64_t(i) * 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        v[size_t(i)] = -bound + 2.0f * bound * float(uint32_t(z >> 40)) * (1.0f / 16777216.0f);
+      }
+    };
+    auto mat = [&](int64_t r, int64_t cc) {
+      Mat x(r, cc);
+      fill(x.v);
+      return x;
+    };
+    m->embed = mat(cfg.vocab, d);
+    m->layers.resize(size_t(cfg.n_layers));
+    for (auto& w : m->layers) {
+      w.wq = mat(d, qd); w.wk = mat(d, kvd); w.wv = mat(d, kvd); w.wo = mat(qd, d);
+      w.w1 = mat(d, F); w.w2 = mat(F, d);
+      if (cfg.ffn_kind == 0) {
+        w.b1.assign(size_t(F), 0.f); fill(w.b1);
+        w.b2.assign(size_t(d), 0.f); fill(w.b2);
+      } else {
+        w.wu = mat(d, F);
+      }
+    }
+    m->unembed = mat(d, cfg.vocab);
+    *out = m;
+  });
+}
+
+void kro_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+int kro_max_threads(void) { return omp_get_max_threads(); }
+
+// KV set of n_layers x [0, L) filled with U(-1, 1) (timing-only snapshots).
+void* kro_kv_synthetic(int n_layers, int kv_heads, int hd, int64_t L, uint64_t seed) {
+  auto* s = new KVSet;
+  s->kv.resize(size_t(n_layers));
+  for (int l = 0; l < n_layers; ++l) {
+    KVLayer& x = s->kv[size_t(l)];
+    x.span = {0, L};
+    for (int g = 0; g < kv_heads; ++g)
+      for (int kvi = 0; kvi < 2; ++kvi) {
+        Mat m(L, hd);
+        const int64_t n = L * hd;
+        const uint64_t sid = (uint64_t(l) * 64 + uint64_t(g)) * 2 + uint64_t(kvi);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+          uint64_t z = seed ^ (sid << 36) ^ uint64_t(i) * 0x9e3779b97f4a7c15ull;
+          z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+          z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+          z ^= z >> 31;
+          m.v[size_t(i)] = -1.0f + 2.0f * float(uint32_t(z >> 40)) * (1.0f / 16777216.0f);
+        }
+        (kvi ? x.v : x.k).push_back(std::move(m));
+      }
+  }
+  return s;
+}
 
 // Flat weights in reference draw order (engine.cpp:368-393). Returns the
 // float count when out == nullptr.
@@ -466,6 +545,28 @@ int kro_expand(void* s, int layer, float* k, float* v, int64_t* span) {
     copy_kv_layer(l, k, v, sn.head_dim);
   });
 }
+// One restoration turn's TTFT work on the CPU, timed (harness.cpp:125-131):
+// execute_restore(model, history, snapshot) then prefill(history + new,
+// restored) with the attention record (the reference always captures).
+// out[0] = restore seconds, out[1] = new-input prefill seconds; logits
+// (optional) receives the last-row logits.
+int kro_time_turn(void* mh, const int32_t* hist, int64_t L, void* snap, const int32_t* newtok,
+                  int64_t n_new, double* out, float* logits) {
+  return guard([&] {
+    const Model& m = *static_cast<Model*>(mh);
+    std::vector<int32_t> h(hist, hist + L);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<KVLayer> restored = execute_restore(m, h, *static_cast<Snapshot*>(snap));
+    auto t1 = std::chrono::steady_clock::now();
+    h.insert(h.end(), newtok, newtok + n_new);
+    PrefillOut pf = prefill(m, h, &restored, true);
+    auto t2 = std::chrono::steady_clock::now();
+    out[0] = std::chrono::duration<double>(t1 - t0).count();
+    out[1] = std::chrono::duration<double>(t2 - t1).count();
+    if (logits) std::memcpy(logits, pf.logits.data(), pf.logits.size() * sizeof(float));
+  });
+}
+
 int kro_restore(void* mh, const int32_t* hist, int64_t n, void* snap, void** out) {
   return guard([&] {
     std::vector<int32_t> t(hist, hist + n);

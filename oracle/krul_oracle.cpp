@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <array>
+#include <immintrin.h>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -95,19 +96,58 @@ void fill(std::vector<float>& v, Uniform& u, float bound) {
   for (auto& x : v) x = u.next(-bound, bound);
 }
 
-// C[M x N] = A[M x K] * B[K x N], rows in parallel, fixed k order per row.
+// C[M x N] = A[M x K] * B[K x N]. Every element is the left-to-right sum
+// c = (((0 + a0 b0) + a1 b1) + ...) with separately rounded products (no FMA:
+// -ffp-contract=off), exactly the order of the naive i-k-j loop; the blocking
+// below only changes which elements are in flight (6 rows x 16 columns held
+// in AVX2 registers across the whole k loop, a 16-column strip of B reused
+// from cache by every row block), not any element's arithmetic.
 Mat matmul(const Mat& A, const Mat& B) {
   Mat C(A.r, B.c);
-  const int64_t K = A.c, N = B.c;
-#pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < A.r; ++i) {
-    float* c = C.row(i);
-    const float* a = A.row(i);
-    for (int64_t k = 0; k < K; ++k) {
-      const float s = a[k];
-      const float* b = B.row(k);
-      for (int64_t j = 0; j < N; ++j) c[j] += s * b[j];
+  const int64_t M = A.r, K = A.c, N = B.c;
+  constexpr int64_t MR = 6, NR = 16;
+  const int64_t nstrips = (N + NR - 1) / NR;
+#pragma omp parallel
+  {
+  std::vector<float> bp(size_t(K) * NR);  // the strip of B packed contiguously (TLB / prefetch)
+#pragma omp for schedule(dynamic, 1)
+  for (int64_t js = 0; js < nstrips; ++js) {
+    const int64_t j0 = js * NR;
+    const int64_t nj = std::min<int64_t>(NR, N - j0);
+    if (nj == NR)
+      for (int64_t k = 0; k < K; ++k) std::memcpy(bp.data() + k * NR, B.row(k) + j0, sizeof(float) * NR);
+    for (int64_t i0 = 0; i0 < M; i0 += MR) {
+      const int64_t mi = std::min<int64_t>(MR, M - i0);
+      if (nj == NR && mi == MR) {
+        __m256 c[MR][2];
+        for (int r = 0; r < MR; ++r) c[r][0] = c[r][1] = _mm256_setzero_ps();
+        const float* a = A.row(i0);
+        for (int64_t k = 0; k < K; ++k) {
+          const float* b = bp.data() + k * NR;
+          const __m256 b0 = _mm256_loadu_ps(b), b1 = _mm256_loadu_ps(b + 8);
+          for (int r = 0; r < MR; ++r) {
+            const __m256 s = _mm256_set1_ps(a[r * K + k]);
+            c[r][0] = _mm256_add_ps(c[r][0], _mm256_mul_ps(s, b0));
+            c[r][1] = _mm256_add_ps(c[r][1], _mm256_mul_ps(s, b1));
+          }
+        }
+        for (int r = 0; r < MR; ++r) {
+          _mm256_storeu_ps(C.row(i0 + r) + j0, c[r][0]);
+          _mm256_storeu_ps(C.row(i0 + r) + j0 + 8, c[r][1]);
+        }
+      } else {  // ragged edge: the plain loop, same order
+        for (int64_t i = i0; i < i0 + mi; ++i) {
+          float* c = C.row(i) + j0;
+          const float* a = A.row(i);
+          for (int64_t k = 0; k < K; ++k) {
+            const float s = a[k];
+            const float* b = B.row(k) + j0;
+            for (int64_t j = 0; j < nj; ++j) c[j] += s * b[j];
+          }
+        }
+      }
     }
+  }
   }
   return C;
 }
@@ -186,8 +226,15 @@ Mat layer_forward(const ModelConfig& cfg, const LayerW& w, const Mat& h_in,
   rope(q, pos0, hd, H, cfg.rope_theta);
   Mat ctx(out_rows, int64_t(H) * hd);
   const int grp = H / Hkv;
+  std::vector<Mat> kt(static_cast<size_t>(Hkv));  // K^T [hd][total] per kv head: 8 keys per vector below
+  for (int g = 0; g < Hkv; ++g) {
+    const Mat& K = kv.k[size_t(g)];
+    kt[size_t(g)] = Mat(hd, total);
+    for (int64_t c = 0; c < total; ++c)
+      for (int t = 0; t < hd; ++t) kt[size_t(g)].at(t, c) = K.at(c, t);
+  }
   for (int h = 0; h < H; ++h) {
-    const Mat& K = kv.k[size_t(h / grp)];
+    const Mat& KT = kt[size_t(h / grp)];
     const Mat& V = kv.v[size_t(h / grp)];
     Mat probs(out_rows, total);
 #pragma omp parallel for schedule(static)
@@ -196,13 +243,20 @@ Mat layer_forward(const ModelConfig& cfg, const LayerW& w, const Mat& h_in,
       const float* qr = q.row(r) + h * hd;
       float* pr = probs.row(r);
       float mx = -std::numeric_limits<float>::infinity();
-      for (int64_t c = 0; c < width; ++c) {
-        float dot = 0.f;
-        const float* kr = K.row(c);
-        for (int t = 0; t < hd; ++t) dot += qr[t] * kr[t];
-        pr[c] = dot * scale;
-        mx = std::max(mx, pr[c]);
+      // dot(q, k_c) = (((0 + q0 k0) + q1 k1) + ...) per key, 8 keys per lane set
+      int64_t c = 0;
+      for (; c + 8 <= width; c += 8) {
+        __m256 dot = _mm256_setzero_ps();
+        for (int t = 0; t < hd; ++t)
+          dot = _mm256_add_ps(dot, _mm256_mul_ps(_mm256_set1_ps(qr[t]), _mm256_loadu_ps(KT.row(t) + c)));
+        _mm256_storeu_ps(pr + c, _mm256_mul_ps(dot, _mm256_set1_ps(scale)));
       }
+      for (; c < width; ++c) {
+        float dot = 0.f;
+        for (int t = 0; t < hd; ++t) dot += qr[t] * KT.at(t, c);
+        pr[c] = dot * scale;
+      }
+      for (c = 0; c < width; ++c) mx = std::max(mx, pr[c]);
       float sum = 0.f;
       for (int64_t c = 0; c < width; ++c) {
         pr[c] = std::exp(pr[c] - mx);
@@ -268,12 +322,18 @@ std::vector<KVLayer> empty_kv(const ModelConfig& cfg) {  // engine.cpp:209-219
 }
 
 std::vector<float> logits_of(const Model& m, const float* h) {
+  // out[j] = sum_k h[k] u[k][j], k ascending per element; column chunks in parallel
   const int64_t d = m.cfg.d_model, V = m.cfg.vocab;
   std::vector<float> out(size_t(V), 0.f);
-  for (int64_t k = 0; k < d; ++k) {
-    const float s = h[k];
-    const float* u = m.unembed.row(k);
-    for (int64_t j = 0; j < V; ++j) out[size_t(j)] += s * u[j];
+  constexpr int64_t CH = 2048;
+#pragma omp parallel for schedule(static)
+  for (int64_t j0 = 0; j0 < V; j0 += CH) {
+    const int64_t j1 = std::min(V, j0 + CH);
+    for (int64_t k = 0; k < d; ++k) {
+      const float s = h[k];
+      const float* u = m.unembed.row(k);
+      for (int64_t j = j0; j < j1; ++j) out[size_t(j)] += s * u[j];
+    }
   }
   return out;
 }

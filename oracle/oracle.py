@@ -62,6 +62,9 @@ def lib():
         _lib.kro_prefill_flops.restype = C.c_double
         _lib.kro_prefill_flops.argtypes = [C.c_double, C.c_int64, C.c_int64, C.c_int64, C.c_int]
         _lib.kro_time_partial.restype = C.c_double
+        _lib.kro_kv_synthetic.restype = C.c_void_p
+        _lib.kro_kv_synthetic.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_uint64]
+        _lib.kro_set_threads.argtypes = [C.c_int]
         for name in ("kro_prefill_take_kv", "kro_kv_clone", "kro_kv_suffix", "kro_kv_from_host"):
             getattr(_lib, name).restype = C.c_void_p
         _lib.kro_kv_suffix.argtypes = [C.c_void_p, C.c_void_p]
@@ -191,6 +194,11 @@ class KV:
         return KV(lib().kro_kv_suffix(self.h, _p(st)), self.cfg)
 
     @staticmethod
+    def synthetic(cfg: ModelConfig, L: int, seed: int = 1):
+        """Timing-only KV: every layer [0, L) filled with U(-1, 1)."""
+        return KV(lib().kro_kv_synthetic(cfg.n_layers, cfg.kv_heads, cfg.head_dim, L, seed), cfg)
+
+    @staticmethod
     def from_host(cfg: ModelConfig, layers):
         """layers: list of (start, end, K[kvh,rows,hd], V[kvh,rows,hd])."""
         N = len(layers)
@@ -243,13 +251,38 @@ class Prefill:
         return avg, [l for l in range(N) if ir[l]]
 
 
+def set_threads(n: int):
+    """OpenMP threads of the oracle's GEMM / attention loops."""
+    lib().kro_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return lib().kro_max_threads()
+
+
 class Model:
-    def __init__(self, cfg: ModelConfig):
+    def __init__(self, cfg: ModelConfig, fast_seed: int | None = None):
+        """build_model (engine.cpp:361-395); fast_seed: timing-only weights
+        from a parallel counter-based fill instead of the reference draw."""
         self.cfg = cfg
         h = C.c_void_p()
         c = cfg.c()
-        _check(lib().kro_model_build(C.byref(c), C.byref(h)))
+        if fast_seed is None:
+            _check(lib().kro_model_build(C.byref(c), C.byref(h)))
+        else:
+            _check(lib().kro_model_build_fast(C.byref(c), C.c_uint64(fast_seed), C.byref(h)))
         self.h = h
+
+    def time_turn(self, history, snap: "Snapshot", new_tokens):
+        """execute_restore + prefill(history + new, restored), timed in C++
+        -> (restore_s, prefill_s, logits)."""
+        t = np.ascontiguousarray(history, np.int32)
+        nt = np.ascontiguousarray(new_tokens, np.int32)
+        out = np.zeros(2, np.float64)
+        lg = np.empty(self.cfg.vocab_size, np.float32)
+        _check(lib().kro_time_turn(self.h, _p(t), C.c_int64(t.size), snap.h, _p(nt), C.c_int64(nt.size),
+                                   _p(out), _p(lg)))
+        return float(out[0]), float(out[1]), lg
 
     def __del__(self):
         if getattr(self, "h", None) and self.h.value:
