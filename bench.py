@@ -330,7 +330,6 @@ def prepare_snapshot(args, K, T, ctx, cfg, spec, rank):
     tc = T.TurnConfig(gamma=spec["gamma"], r_l=spec["r_l"], merge=K.MERGE_MEAN,
                       calibrate=None if spec.get("f32") else measured_rc)
     st = T.KrulTurns(ctx, tc, cfg.max_tokens)
-    ctx.set_capture(True)  # the estimator's prefill fold reads the captured attention
     if "turn0" in spec:    # cfg1: turn 0 = fresh prefill of the user tokens + forced decode
         n_user, n_dec = spec["turn0"]
         rec = st.turn(0, T.Turn(rng.integers(0, cfg.vocab_size, n_user, dtype=np.int32),
@@ -340,7 +339,6 @@ def prepare_snapshot(args, K, T, ctx, cfg, spec, rank):
         st.start_from(rng.integers(0, cfg.vocab_size, L - n_new - n_dec, dtype=np.int32))
         rec = st.turn(1, T.Turn(rng.integers(0, cfg.vocab_size, n_new, dtype=np.int32),
                                 rng.integers(0, cfg.vocab_size, n_dec, dtype=np.int32)))
-    ctx.set_capture(False)
     assert st.history.size == L, (st.history.size, L)
     return st, new, rec, calib, scratch.get("conv")
 

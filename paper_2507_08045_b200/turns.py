@@ -100,14 +100,19 @@ class KrulTurns:
         user = np.ascontiguousarray(trace.user, np.int32)
         tokens = np.concatenate([self.history, user]).astype(np.int32)
         ttft, stats = None, None
-        if t == 0 or self.snapshot is None:                      # harness.cpp:124-126
-            logits = ctx.prefill(self.conv, tokens)
-        else:                                                   # harness.cpp:127-131
-            logits, stats, ttft = ctx.restore_and_prefill(self.conv, self.history, self.snapshot, user)
-        # the adaptive path analyses the turn it just prefilled (harness.cpp:171-178)
-        avg, ir, non_ir = ctx.classify_layers(cfg.gamma, cfg.initial_frac, cfg.recent_frac)
-        est = K.StreamingEstimator(ctx, ir)
-        est.fold_prefill()
+        # the estimator's prefill fold reads this prefill's attention record
+        ctx.set_capture(True)
+        try:
+            if t == 0 or self.snapshot is None:                      # harness.cpp:124-126
+                logits = ctx.prefill(self.conv, tokens)
+            else:                                                   # harness.cpp:127-131
+                logits, stats, ttft = ctx.restore_and_prefill(self.conv, self.history, self.snapshot, user)
+            # the adaptive path analyses the turn it just prefilled (harness.cpp:171-178)
+            avg, ir, non_ir = ctx.classify_layers(cfg.gamma, cfg.initial_frac, cfg.recent_frac)
+            est = K.StreamingEstimator(ctx, ir)
+            est.fold_prefill()
+        finally:
+            ctx.set_capture(False)
         for tok in np.asarray(trace.forced_decode, np.int32):  # harness.cpp:180-188
             ctx.decode_step(self.conv, int(tok))
             est.fold_decode()

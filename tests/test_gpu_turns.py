@@ -44,7 +44,6 @@ def test_turn_loop_cfg1_bit_exact(merge, oracle):
 
     ctx = K.Context(K.ModelConfig(**CFG1, dtype=K.KRUL_F32, max_tokens=1024), 0)
     ctx.upload_weights(om.weights())
-    ctx.set_capture(True)
     recs, st = T.run_turns(ctx, [T.Turn(u, f) for u, f in traces], T.TurnConfig(**knobs), 1024)
 
     for t, (g, o) in enumerate(zip(recs, orecs)):
