@@ -274,9 +274,11 @@ int krul_capture_decode(krul_ctx* ctx, float* out, int64_t* width) {
     Ctx& c = *ctx->c;
     if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
     if (width) *width = c.dec_width;
-    if (out)
-      KB_CUDA(kb_memcpy_sync(out, c.dec_rows.p, size_t(c.cfg.N) * c.cfg.H * c.dec_width * 4,
-                         cudaMemcpyDeviceToHost));
+    if (out) {
+      KB_CUDA(cudaDeviceSynchronize());
+      KB_CUDA(cudaMemcpy2D(out, size_t(c.dec_width) * 4, c.dec_rows.p, size_t(c.dec_pitch) * 4,
+                           size_t(c.dec_width) * 4, size_t(c.cfg.N) * c.cfg.H, cudaMemcpyDeviceToHost));
+    }
   });
 }
 
@@ -359,14 +361,21 @@ static void fold_prefill_dev(Est& e, const float* probs, int64_t rows, int64_t W
   e.prefill_done = true;
   e.prefill_rows = rows;
 }
-static void fold_decode_dev(Est& e, const float* rows, int64_t W, int N) {
+// rows: [N][H][pitch] f32, pitch % 4 == 0 (the decode step's capture layout)
+static void fold_decode_dev(Est& e, const float* rows, int64_t W, int64_t pitch, int N) {
   if (!e.layers.empty() && e.layers.back() >= N)
     fail(KRUL_E_STATE_CORRUPTION, "decode rows do not cover all tracked layers");
   Ctx& c = *e.ctx;
-  ensure_partial(e, (W + kFoldChunk - 1) / kFoldChunk);
+  const int n = int(e.layers.size());
+  const int sms = c.sm_count > 0 ? c.sm_count : 148;
+  const int64_t need_p = fold_direct_partial_elems(std::max(n, 2), W, e.H, sms);
+  if (need_p > e.partial_cap) {
+    e.partial.ensure(size_t(need_p) * 8);
+    e.partial_cap = need_p;
+  }
   cudaEvent_t kt0 = kt_begin(c, c.s_est);
-  launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()),
-                     e.sums.as<double>(), e.partial.as<double>(), e.partial_cap);
+  launch_fold_direct(c.s_est, rows, int64_t(e.H) * pitch, pitch, W, e.H, e.d_layers.as<int>(), n,
+                     e.sums.as<double>(), e.partial.as<double>(), e.partial_cap, sms);
   // algorithmic bytes: tracked rows read once + f64 accumulator RMW
   kt_end(c, c.s_est, kt0, KT_FOLD_DECODE, 0.0,
          double(e.layers.size()) * e.H * double(W) * 4.0 + double(e.P()) * e.H * 16.0);
@@ -393,7 +402,7 @@ int krul_est_fold_decode(krul_est* est) {
     if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
     KB_CUDA(cudaSetDevice(c.device));
     KB_CUDA(cudaStreamSynchronize(c.s_comp));
-    fold_decode_dev(e, c.dec_rows.as<float>(), c.dec_width, c.cfg.N);
+    fold_decode_dev(e, c.dec_rows.as<float>(), c.dec_width, c.dec_pitch, c.cfg.N);
   });
 }
 int krul_est_fold_prefill_host(krul_est* est, const float* probs, int N, int64_t rows, int64_t W) {
@@ -415,10 +424,14 @@ int krul_est_fold_decode_host(krul_est* est, const float* rows, int N, int64_t W
     need(rows, "rows");
     Est& e = *est->e;
     KB_CUDA(cudaSetDevice(e.ctx->device));
-    const size_t n = size_t(N) * e.H * size_t(W);
+    const int64_t pitch = (W + 3) / 4 * 4;
+    const size_t n = size_t(N) * e.H * size_t(pitch);
     float* d = static_cast<float*>(e.tmp.ensure(std::max<size_t>(n, 1) * 4));
-    KB_CUDA(kb_memcpy_sync(d, rows, n * 4, cudaMemcpyHostToDevice));
-    fold_decode_dev(e, d, W, N);
+    KB_CUDA(cudaDeviceSynchronize());
+    if (W > 0)
+      KB_CUDA(cudaMemcpy2D(d, size_t(pitch) * 4, rows, size_t(W) * 4, size_t(W) * 4, size_t(N) * e.H,
+                           cudaMemcpyHostToDevice));
+    fold_decode_dev(e, d, W, pitch, N);
   });
 }
 int krul_est_sums(krul_est* est, double* sums) {
@@ -1266,20 +1279,27 @@ int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* by
     if (!c.dec_valid) fail(KRUL_E_STATE_CORRUPTION, "no captured decode step");
     KB_CUDA(cudaSetDevice(c.device));
     KB_CUDA(cudaDeviceSynchronize());
-    const int64_t W = c.dec_width;
-    ensure_partial(e, (W + kFoldChunk - 1) / kFoldChunk);
+    const int64_t W = c.dec_width, pitch = c.dec_pitch;
+    const int n = int(e.layers.size());
+    const int sms = c.sm_count > 0 ? c.sm_count : 148;
+    const int64_t need_p = fold_direct_partial_elems(std::max(n, 2), W, e.H, sms);
+    if (need_p > e.partial_cap) {
+      e.partial.ensure(size_t(need_p) * 8);
+      e.partial_cap = need_p;
+    }
     DevBuf scratch;
     double* sums = static_cast<double*>(scratch.ensure(size_t(std::max(e.P(), 1)) * e.H * 8));
     const float* rows = c.dec_rows.as<float>();
-    launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()), sums,
-                       e.partial.as<double>(), e.partial_cap);  // warm
+    auto fold = [&] {
+      launch_fold_direct(c.s_est, rows, int64_t(e.H) * pitch, pitch, W, e.H, e.d_layers.as<int>(), n, sums,
+                         e.partial.as<double>(), e.partial_cap, sms);
+    };
+    fold();  // warm
     cudaEvent_t a, b;
     KB_CUDA(cudaEventCreate(&a));
     KB_CUDA(cudaEventCreate(&b));
     KB_CUDA(cudaEventRecord(a, c.s_est));
-    for (int i = 0; i < iters; ++i)
-      launch_fold_decode(c.s_est, rows, W, e.H, e.d_layers.as<int>(), int(e.layers.size()), sums,
-                         e.partial.as<double>(), e.partial_cap);
+    for (int i = 0; i < iters; ++i) fold();
     KB_CUDA(cudaEventRecord(b, c.s_est));
     KB_CUDA(cudaEventSynchronize(b));
     float ms = 0;

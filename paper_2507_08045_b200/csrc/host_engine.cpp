@@ -504,15 +504,16 @@ void decode_step(Ctx& c, Conv& conv, int32_t tok, float* logits) {
   const int64_t pos = conv.len, W = pos + 1;
   int32_t* d_tok = upload_tokens(c, s, &tok, 1, c.ws_tok);
   float* d_logits = static_cast<float*>(c.ws_logits.ensure(size_t(g.V) * 4));
-  float* rows = static_cast<float*>(c.dec_rows.ensure(size_t(g.N) * g.H * W * 4));
+  const int64_t pitch = (W + 3) / 4 * 4;  // 16-byte rows for the fold's vector loads
+  float* rows = static_cast<float*>(c.dec_rows.ensure(size_t(g.N) * g.H * pitch * 4));
   WS w = ws_get(c, 0, 1);
   launch_embed(c, s, d_tok, 1, w.h);
   float* hin = w.h;
   float* hout = w.h2;
   for (int l = 0; l < g.N; ++l) {
     AttnArgs a{};
-    a.probs = rows + int64_t(l) * g.H * W;
-    a.ld_probs = W;
+    a.probs = rows + int64_t(l) * g.H * pitch;
+    a.ld_probs = pitch;
     a.probs_rows = 1;
     layer_forward(c, s, w, conv, l, hin, 1, pos, 1, hout, &a);
     std::swap(hin, hout);
@@ -520,6 +521,7 @@ void decode_step(Ctx& c, Conv& conv, int32_t tok, float* logits) {
   launch_logits(c, s, hin, d_logits);
   conv.len = W;
   c.dec_width = W;
+  c.dec_pitch = pitch;
   c.dec_valid = true;
   if (logits) KB_CUDA(cudaMemcpyAsync(logits, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, s));
   KB_CUDA(cudaStreamSynchronize(s));

@@ -208,7 +208,8 @@ struct Ctx {
   DevBuf cap_mass;        // [N][H][rows] f64 region masses (classifier)
   double cap_ifrac = 0.1, cap_rfrac = 0.1;
   int64_t cap_il = 0, cap_rs = 0;
-  DevBuf dec_rows;        // [N][H][W] f32 last decode step
+  DevBuf dec_rows;        // [N][H][dec_pitch] f32 last decode step (pitch: 16-byte rows)
+  int64_t dec_pitch = 0;
   DevBuf dec_part;        // split-key partials of the decode attention
   int64_t dec_width = 0;
   bool dec_valid = false;
@@ -368,6 +369,11 @@ void launch_fold_prefill(cudaStream_t s, const float* probs, int64_t rows, int64
                          const int* d_layers, int n, double* sums, double* partial,
                          int64_t partial_cap);
 void launch_finalize(cudaStream_t s, const double* sums, int n, int H, double* D);
+// K1 decode fold (fold.cu): rows [layer][head][.] f32 with 16-byte aligned
+// strides; part = per-(chunk, pair, head) f64 scratch
+int64_t fold_direct_partial_elems(int n, int64_t W, int H, int sms);
+void launch_fold_direct(cudaStream_t s, const float* rows, int64_t layer_stride, int64_t head_stride, int64_t W,
+                        int H, const int* d_layers, int n, double* sums, double* part, int64_t part_cap, int sms);
 // selector: candidates sorted on device then greedily matched
 void launch_select(cudaStream_t s, const double* cand_d, const int* cand_i, const int* cand_j,
                    int n_cand, int quota, int* out_i, int* out_j, double* out_d, int* out_n);

@@ -864,94 +864,138 @@ __global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView 
   }
 }
 
-// K4b + K5 fused (coded store, hd = 128): one warp decodes a 4096-element
-// chunk of the coded blob; with hd equal to a lane's 128-element stream,
-// lane j holds exactly one row of the blob — token blob_start + r of head g,
-// K or V — and writes it straight into the owners' pages: K rows as 16-byte
-// stores, V^T columns as per-dimension stores that are contiguous across
-// the warp's 32 consecutive tokens. No raw staging round trip, one launch
-// per blob instead of decode + one expand per owner.
-__global__ void __launch_bounds__(128) k_ec_decode_expand(const uint8_t* __restrict__ blob,
-                                                          const uint16_t* __restrict__ lut,
-                                                          int64_t blob_start, int64_t rows, PageView pv0,
-                                                          int64_t from0, PageView pv1, int64_t from1,
-                                                          int n_owners) {
-  constexpr int kWarps = 4;
-  __shared__ uint16_t s_lut[1 << kEcMaxLen];
-  __shared__ uint32_t s_w[kWarps][32 * kEcMaxLaneWords + 2];
-  for (int i = threadIdx.x; i < (1 << kEcMaxLen); i += blockDim.x) s_lut[i] = lut[i];
-  __syncthreads();
-  const EcHeader h = *reinterpret_cast<const EcHeader*>(blob);
+// K4b + K5 fused (coded store, hd = 128): with hd equal to a lane's
+// 128-element stream, lane j of a 4096-element chunk holds exactly one blob
+// row -- token blob_start + r of head g, K or V -- and writes it straight
+// into the owners' pages: K rows as one 32-byte store per 16 elements (full
+// L2 sectors), V^T columns as per-dimension stores contiguous across the
+// warp's 32 consecutive tokens. No raw staging round trip, one launch per
+// blob.
+//
+// Sized to share SMs with the restore's other kernels (the GEMM / attention
+// CTAs hold ~225 KB of shared memory each): no shared memory at all -- the
+// 8 KB decode LUT and the exponent words are read through L1 (__ldg) --
+// and a small CTA (128 threads), so the decode CTAs co-reside with them
+// instead of queueing behind them. A persistent grid walks the chunks; every warp
+// decodes two chunks at once (two independent bit-stream chains per lane:
+// the LUT lookup latency of one chain hides behind the other).
+struct EcLane {  // one lane's position in its chunk's exponent stream + its row's destinations
+  uint32_t wa, wb, wc, bo;
+  const uint32_t* wp;  // the word after wc
+  const uint4* smv;    // the row's sign+mantissa bytes
+  uint16_t *d0, *d1;   // the row in each owner's page (K row / V^T column), null = not written
+  bool isv;
+};
+__device__ __forceinline__ void ec_lane_init(EcLane& st, const uint8_t* blob, const EcHeader& h, int64_t ch,
+                                             int lane, int64_t rows, const PageView& pv0, const PageView& pv1,
+                                             int64_t blob_start, int64_t from0, int64_t from1, int n_owners) {
   const uint32_t* base_t = reinterpret_cast<const uint32_t*>(blob + h.base_off);
   const uint8_t* cnt_t = blob + h.cnt_off;
-  const uint8_t* sm = blob + h.sm_off;
   const uint32_t* ex = reinterpret_cast<const uint32_t*>(blob + h.exp_off);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* sw = s_w[warp];
-  const int64_t n = int64_t(h.n_elems), nrows = n / 128;
+  const uint32_t base = __ldg(base_t + ch);
+  const uint32_t c = __ldg(cnt_t + ch * 32 + lane);
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const uint32_t* w = ex + base + (inc - c);
+  st.wa = __ldg(w);
+  st.wb = __ldg(w + 1);
+  st.wc = __ldg(w + 2);  // the image ends with a pad word past the last stream; a third read stays inside
+  st.wp = w + 3;
+  st.bo = 0;
+  const int64_t nrows = int64_t(h.n_elems) / 128;
+  const int64_t R = ch * 32 + lane;  // flattened (kv, g, r) row of this lane
+  const bool live = R < nrows;
+  const int64_t r = live ? R % rows : 0;
+  const int64_t hg = live ? R / rows : 0;
   const int Hkv = pv0.Hkv;
-  for (int64_t ch = blockIdx.x * int64_t(kWarps) + warp; ch < h.n_chunks; ch += int64_t(gridDim.x) * kWarps) {
-    const uint32_t base = __ldg(base_t + ch), total = __ldg(base_t + ch + 1) - base;
-    const uint32_t c = __ldg(cnt_t + ch * 32 + lane);
-    uint32_t inc = c;
+  st.isv = hg >= Hkv;
+  const int g = int(hg % Hkv);
+  const int64_t pos = blob_start + r;
+  st.smv = reinterpret_cast<const uint4*>(blob + h.sm_off + R * 128);
+  auto dst = [&](const PageView& pv) {
+    uint16_t* page = reinterpret_cast<uint16_t*>(pv.page(pos));
+    return page + (st.isv ? pv.v_off(g, pos, 0) : pv.k_off(g, pos, 0));
+  };
+  st.d0 = live && pos >= from0 ? dst(pv0) : nullptr;
+  st.d1 = live && n_owners > 1 && pos >= from1 ? dst(pv1) : nullptr;
+  if (!live) st.smv = nullptr;
+}
+__device__ __forceinline__ uint32_t ec_next(EcLane& st, const uint16_t* __restrict__ lut) {
+  const uint32_t win = __funnelshift_l(st.wb, st.wa, st.bo);
+  const uint32_t e = __ldg(lut + (win >> (32 - kEcMaxLen)));
+  st.bo += e >> 8;
+  if (st.bo >= 32) {  // next word; the one after it is already in flight
+    st.bo -= 32;
+    st.wa = st.wb;
+    st.wb = st.wc;
+    st.wc = __ldg(st.wp++);
+  }
+  return e;
+}
+__device__ __forceinline__ void ec_store16(const EcLane& st, const uint32_t (&o)[8], int gq) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
+  for (int ow = 0; ow < 2; ++ow) {
+    uint16_t* d = ow == 0 ? st.d0 : st.d1;
+    if (!d) continue;
+    if (!st.isv) {  // one 32-byte store per lane (STG.256): whole L2 sectors
+      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d + 16 * gq), "r"(o[0]),
+                   "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                   : "memory");
+    } else {
+      uint16_t* vt = d + int64_t(16 * gq) * kPageTokens;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) vt[k * kPageTokens] = uint16_t(o[k >> 1] >> (16 * (k & 1)));
     }
-    const uint32_t my = inc - c;
-    __syncwarp();
-    for (uint32_t i = lane; i < total + 1; i += 32) sw[i] = __ldg(ex + base + i);
-    __syncwarp();
-    const int64_t R = ch * 32 + lane;  // flattened (kv, g, r) row of this lane
-    const bool live = R < nrows;
-    const int64_t r = live ? R % rows : 0;
-    const int64_t hg = live ? R / rows : 0;
-    const int isv = int(hg / Hkv), g = int(hg % Hkv);
-    const int64_t pos = blob_start + r;
-    const bool w0 = live && pos >= from0, w1 = live && n_owners > 1 && pos >= from1;
-    const int64_t e0 = R * 128;
-    uint32_t idx = my, wa = sw[idx], wb = sw[idx + 1], bo = 0;
+  }
+}
+__global__ void __launch_bounds__(128, 4) k_ec_decode_expand(const uint8_t* __restrict__ blob,
+                                                             const uint16_t* __restrict__ lut,
+                                                             int64_t blob_start, int64_t rows, PageView pv0,
+                                                             int64_t from0, PageView pv1, int64_t from1,
+                                                             int n_owners) {
+  const EcHeader h = *reinterpret_cast<const EcHeader*>(blob);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t wid = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int64_t ch = 2 * wid; ch < h.n_chunks; ch += 2 * warps) {
+    EcLane a, b;
+    ec_lane_init(a, blob, h, ch, lane, rows, pv0, pv1, blob_start, from0, from1, n_owners);
+    if (ch + 1 < h.n_chunks) {
+      ec_lane_init(b, blob, h, ch + 1, lane, rows, pv0, pv1, blob_start, from0, from1, n_owners);
+    } else {
+      b = a;
+      b.smv = nullptr;
+      b.d0 = b.d1 = nullptr;
+    }
 #pragma unroll 1
-    for (int gq = 0; gq < 8; ++gq) {  // 16 elements per group
-      uint32_t o[8];
-      if (live) {
-        const uint4 sv = __ldg(reinterpret_cast<const uint4*>(sm + e0) + gq);
-        const uint32_t sb[4] = {sv.x, sv.y, sv.z, sv.w};
+    for (int gq = 0; gq < 8; ++gq) {  // 16 elements per group and chain
+      const uint4 sa = a.smv ? __ldg(a.smv + gq) : make_uint4(0, 0, 0, 0);
+      const uint4 sb = b.smv ? __ldg(b.smv + gq) : make_uint4(0, 0, 0, 0);
+      uint32_t oa[8], ob[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const uint32_t win = __funnelshift_l(wb, wa, bo);
-          const uint32_t e = s_lut[win >> (32 - kEcMaxLen)];
-          bo += e >> 8;
-          if (bo >= 32) {
-            bo -= 32;
-            wa = wb;
-            wb = sw[++idx + 1];
-          }
-          const uint32_t sbyte = (sb[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-          const uint32_t v = ((sbyte & 0x80u) << 8) | ((e & 0xFFu) << 7) | (sbyte & 0x7Fu);
-          if (k & 1) o[k >> 1] |= v << 16;
-          else o[k >> 1] = v;
-        }
-      }
-      for (int ow = 0; ow < 2; ++ow) {
-        const bool wr = ow == 0 ? w0 : w1;
-        const PageView& pv = ow == 0 ? pv0 : pv1;
-        if (!wr) continue;
-        bf16* page = reinterpret_cast<bf16*>(pv.page(pos));
-        if (!isv) {
-          // one 32-byte store per lane (STG.256): a whole L2 sector, where two
-          // 16-byte stores wrote every sector in halves (2x SM->L2 traffic)
-          bf16* dst = page + pv.k_off(g, pos, 16 * gq);
-          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(o[0]),
-                       "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
-                       : "memory");
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t ea = ec_next(a, lut);
+        const uint32_t eb = ec_next(b, lut);
+        // bf16 = sign | exponent | 7 mantissa bits; the byte plane holds sign + mantissa
+        const uint32_t wa = k < 4 ? sa.x : k < 8 ? sa.y : k < 12 ? sa.z : sa.w;
+        const uint32_t wb = k < 4 ? sb.x : k < 8 ? sb.y : k < 12 ? sb.z : sb.w;
+        const uint32_t ya = (wa >> (8 * (k & 3))) & 0xFFu, yb = (wb >> (8 * (k & 3))) & 0xFFu;
+        const uint32_t va = ((ya & 0x80u) << 8) | ((ea & 0xFFu) << 7) | (ya & 0x7Fu);
+        const uint32_t vb = ((yb & 0x80u) << 8) | ((eb & 0xFFu) << 7) | (yb & 0x7Fu);
+        if (k & 1) {
+          oa[k >> 1] |= va << 16;
+          ob[k >> 1] |= vb << 16;
         } else {
-          uint16_t* vt = reinterpret_cast<uint16_t*>(page) + pv.v_off(g, pos, 16 * gq);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) vt[int64_t(k) * kPageTokens] = uint16_t(o[k >> 1] >> (16 * (k & 1)));
+          oa[k >> 1] = va;
+          ob[k >> 1] = vb;
         }
       }
+      ec_store16(a, oa, gq);
+      ec_store16(b, ob, gq);
     }
   }
 }
@@ -962,7 +1006,9 @@ void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int
   const int no = owners[1] >= 0 ? 2 : 1;
   const PageView pv0 = page_view(c, conv, owners[0]);
   const PageView pv1 = no > 1 ? page_view(c, conv, owners[1]) : pv0;
-  const unsigned blocks = unsigned(std::min<int64_t>((n_chunks + 3) / 4, 148 * 6));
+  // persistent: 4 CTAs (128 registers x 128 threads) per SM, two chunks per warp and pass
+  const int sms = c.sm_count > 0 ? c.sm_count : 148;
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((n_chunks + 7) / 8, int64_t(sms) * 4)));
   cudaEvent_t kt0 = kt_begin(c, s);
   k_ec_decode_expand<<<blocks, 128, 0, s>>>(static_cast<const uint8_t*>(blob), lut, blob_start, L - blob_start,
                                             pv0, from[0], pv1, no > 1 ? from[1] : L, no);

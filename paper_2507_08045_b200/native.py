@@ -16,7 +16,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libkrul_b200.so")
+# KRUL_LIB: an alternate build of the same library (A/B timing experiments)
+LIB_PATH = os.environ.get("KRUL_LIB") or os.path.join(HERE, "_lib", "libkrul_b200.so")
 
 KRUL_F32, KRUL_BF16 = 0, 1
 FFN_TANH, FFN_SWIGLU = 0, 1
