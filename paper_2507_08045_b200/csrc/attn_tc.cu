@@ -274,6 +274,8 @@ __global__ void __launch_bounds__(352, 1)
   __syncthreads();
   tca::fence_after();
   const uint32_t tmem = *tslot;
+  pdl_trigger();
+  pdl_wait();  // Q and this step's K / V rows come from the preceding kernels
   auto page_of = [&](int i, int half) {
     return i < kPgCache ? pg_s[2 * i + half] : p.pt[min(2 * (b0 + i) + half, p.max_pages - 1)];
   };
@@ -533,6 +535,8 @@ constexpr int kMaxSplit = 16;
 template <int HD>
 __global__ void __launch_bounds__(128) k_attn_combine(AttnTc p) {
   __shared__ float tile[32][33];
+  pdl_trigger();
+  pdl_wait();
   const int64_t r0 = int64_t(blockIdx.x) * 32;
   const int h = blockIdx.y, d0 = blockIdx.z * 32;
   const int n_splits = attn_nsplit(p, int(r0 / 128));
@@ -615,7 +619,7 @@ void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap&
     KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  kern<<<grid, 352, smem, s>>>(tq, tk, tv, p);
+  KB_CUDA(launch_pdl(kern, grid, dim3(352), smem, s, tq, tk, tv, p));
   KB_LAUNCH();
 }
 
@@ -700,9 +704,9 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   if (max_split > 1) {
     const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), unsigned(HD / 32)};
     if (HD == 128)
-      k_attn_combine<128><<<g2, 128, 0, s>>>(p);
+      KB_CUDA(launch_pdl(k_attn_combine<128>, g2, dim3(128), 0, s, p));
     else
-      k_attn_combine<64><<<g2, 128, 0, s>>>(p);
+      KB_CUDA(launch_pdl(k_attn_combine<64>, g2, dim3(128), 0, s, p));
     KB_LAUNCH();
   }
 }

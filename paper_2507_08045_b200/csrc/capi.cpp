@@ -278,6 +278,7 @@ int krul_capture_decode(krul_ctx* ctx, float* out, int64_t* width) {
       KB_CUDA(cudaDeviceSynchronize());
       KB_CUDA(cudaMemcpy2D(out, size_t(c.dec_width) * 4, c.dec_rows.p, size_t(c.dec_pitch) * 4,
                            size_t(c.dec_width) * 4, size_t(c.cfg.N) * c.cfg.H, cudaMemcpyDeviceToHost));
+      KB_CUDA(cudaDeviceSynchronize());
     }
   });
 }
@@ -431,6 +432,9 @@ int krul_est_fold_decode_host(krul_est* est, const float* rows, int N, int64_t W
     if (W > 0)
       KB_CUDA(cudaMemcpy2D(d, size_t(pitch) * 4, rows, size_t(W) * 4, size_t(W) * 4, size_t(N) * e.H,
                            cudaMemcpyHostToDevice));
+    // a pageable H2D copy may return before its DMA lands; the fold runs on a
+    // non-blocking stream that does not order against the legacy stream
+    KB_CUDA(cudaDeviceSynchronize());
     fold_decode_dev(e, d, W, pitch, N);
   });
 }

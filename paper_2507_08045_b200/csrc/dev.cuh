@@ -4,10 +4,38 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 
 namespace kb {
 
 using bf16 = __nv_bfloat16;
+
+// Programmatic dependent launch (PDL). Kernels launched with launch_pdl may
+// start while the preceding kernel in the stream is still running: they
+// call pdl_trigger() (lets the next kernel in the stream start its prologue
+// in turn) and do only work independent of the predecessor -- barrier / TMEM
+// setup, weight prefetch -- before pdl_wait(), which returns once the
+// predecessor grid has completed and its writes are visible. Without the
+// launch attribute both are no-ops, so every kernel below keeps them
+// unconditionally.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();  // KRUL_PDL=0 disables the launch attribute (A/B)
+template <typename... P, typename... A>
+inline cudaError_t launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
 
 __device__ __forceinline__ float tof(float x) { return x; }
 __device__ __forceinline__ float tof(bf16 x) { return __bfloat162float(x); }

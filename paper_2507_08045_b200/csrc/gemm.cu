@@ -615,26 +615,45 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // the next kernel in the stream may start its prologue
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       int s = 0;
       uint32_t ph = 0;
       Unit un;
+      // weights do not depend on the preceding kernel: the first unit's first
+      // stages of B are in flight before the dependency wait (PDL)
+      int pre = 0;
+      if (unit_at(0, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un)) {
+        pre = min(STAGES, un.k1 - un.k0);
+        for (int q = 0; q < pre; ++q) {
+          tc::mbar_expect_tx(&full[q], A_BYTES + B_BYTES);
+          tc::tma_load_2d(sB + q * B_BYTES, &tmB, &full[q], (un.k0 + q) * BK, un.n * BN);
+        }
+      }
+      pdl_wait();
       for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
         for (int kb = un.k0; kb < un.k1; ++kb) {
-          tc::mbar_wait(&empty[s], ph ^ 1);
-          tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-          tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, un.m * BM);
-          tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, un.n * BN);
+          if (i == 0 && kb - un.k0 < pre) {  // first pass over the ring: B already issued
+            tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, un.m * BM);
+          } else {
+            tc::mbar_wait(&empty[s], ph ^ 1);
+            tc::mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+            tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, un.m * BM);
+            tc::tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, un.n * BN);
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
       }
+    } else {
+      pdl_wait();
     }
   } else if (warp == 1) {
+    pdl_wait();
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
                                  (uint32_t(BM >> 4) << 24);
@@ -669,6 +688,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {  // epilogue warps 2..5
+    pdl_wait();  // outputs / residual inputs belong to the dependency chain
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     float* my = stg + q * 32 * 33;
     unsigned char* stage = reinterpret_cast<unsigned char*>(stg) + q * 8192;
@@ -922,6 +942,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 template <class T>
 __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t M, int64_t N,
                                 Epi e, SkInfo sk) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t MN = M * N;
   if ((N & 3) == 0) {
     const int64_t q = N >> 2, total = M * q;
@@ -993,6 +1015,8 @@ __global__ void __launch_bounds__(256) k_qkv_reduce(const float* __restrict__ P,
   // before the partial sums, off the dependent chain
   constexpr int RB = 32, RJ = RB / 8;
   __shared__ float t[RB][33];
+  pdl_trigger();
+  pdl_wait();
   const int64_t r0 = int64_t(blockIdx.x) * RB;
   const int64_t cc = int64_t(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // column, token group
@@ -1291,8 +1315,8 @@ void run_tc(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUt
     attr = true;
   }
   const int mt = int((M + 127) / 128), nt = int((N + BN - 1) / BN);
-  kern<<<gp.grid, 192, smem, s>>>(ta, tb, tcm, int(M), int(N), int(K), mt, nt, gp.splits, gp.kb_per,
-                                  e, partial, gp.grid, gp.sk_T);
+  KB_CUDA(launch_pdl(kern, dim3(gp.grid), dim3(192), smem, s, ta, tb, tcm, int(M), int(N), int(K), mt, nt,
+                     gp.splits, gp.kb_per, e, partial, gp.grid, gp.sk_T));
   KB_LAUNCH();
 }
 
@@ -1408,12 +1432,13 @@ void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, co
     if (part && e.kind == Epi::QKV) {
       if (c.cfg.hd % 32) fail(KRUL_E_CUDA, "fused QKV epilogue needs head_dim % 32 == 0");
       const dim3 g2{unsigned((M + 31) / 32), unsigned((N + 31) / 32), 1u};
-      k_qkv_reduce<<<g2, 256, 0, s>>>(part, gp.splits, M, N, e.kv, sk);
+      KB_CUDA(launch_pdl(k_qkv_reduce, g2, dim3(256), 0, s, (const float*)part, gp.splits, M, N, e.kv, sk));
       KB_LAUNCH();
     } else if (part) {
       const int64_t work = (N % 4 == 0) ? M * N / 4 : (e.kind == Epi::SWIGLU ? M * N / 2 : M * N);
       const unsigned blocks = unsigned(std::min<int64_t>((work + 255) / 256, 8 * 148));
-      k_splitk_reduce<bf16><<<blocks, 256, 0, s>>>(part, gp.splits, M, N, e, sk);
+      KB_CUDA(launch_pdl(k_splitk_reduce<bf16>, dim3(blocks), dim3(256), 0, s, (const float*)part, gp.splits, M,
+                         N, e, sk));
       KB_LAUNCH();
     }
     return;

@@ -11,6 +11,17 @@ namespace kb {
 void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
 std::atomic<uint64_t> g_launches{0};
+// Off by default: measured on the Llama-3-8B restore, the early-launched
+// dependents' resident CTAs hold SMs the concurrent restore streams need
+// (TTFT 11.23 -> 11.62 ms) although each chain alone runs ~6% faster
+// (KRUL_PDL=1 to enable).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("KRUL_PDL");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
 std::atomic<uint64_t> g_buf_gen{0};
 
 cudaEvent_t KTime::ev() {

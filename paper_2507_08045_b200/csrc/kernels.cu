@@ -48,6 +48,8 @@ __global__ void k_rmsnorm(const float* h, int d, T* out) {
 template <int V>  // float4 vectors per lane: d = 128 * V
 __global__ void __launch_bounds__(256) k_rmsnorm_warp(const float* __restrict__ h, int64_t rows,
                                                       int d, bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (r >= rows) return;
   const int lane = threadIdx.x & 31;
@@ -75,6 +77,8 @@ __global__ void __launch_bounds__(256) k_rmsnorm_warp(const float* __restrict__ 
 template <int V>  // float4 vectors per thread: d = 1024 * V
 __global__ void __launch_bounds__(256) k_rmsnorm_cta(const float* __restrict__ h, int d,
                                                      bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t r = blockIdx.x;
   const float4* x = reinterpret_cast<const float4*>(h + r * d);
   float4 v[V];
@@ -99,18 +103,18 @@ void launch_rmsnorm(const Ctx& c, cudaStream_t s, const float* h, int64_t rows, 
   const int d = c.cfg.d;
   if (c.cfg.dtype == KRUL_BF16 && rows <= 2 * 148 && (d == 4096 || d == 8192)) {
     if (d == 4096)
-      k_rmsnorm_cta<4><<<unsigned(rows), 256, 0, s>>>(h, d, (bf16*)xn);
+      KB_CUDA(launch_pdl(k_rmsnorm_cta<4>, dim3(unsigned(rows)), dim3(256), 0, s, h, d, (bf16*)xn));
     else
-      k_rmsnorm_cta<8><<<unsigned(rows), 256, 0, s>>>(h, d, (bf16*)xn);
+      KB_CUDA(launch_pdl(k_rmsnorm_cta<8>, dim3(unsigned(rows)), dim3(256), 0, s, h, d, (bf16*)xn));
     KB_LAUNCH();
     return;
   }
   if (c.cfg.dtype == KRUL_BF16 && d % 128 == 0 && d <= 128 * 32) {
     const unsigned blocks = unsigned((rows + 7) / 8);
     switch (d / 128) {
-      case 32: k_rmsnorm_warp<32><<<blocks, 256, 0, s>>>(h, rows, d, (bf16*)xn); KB_LAUNCH(); return;
-      case 2: k_rmsnorm_warp<2><<<blocks, 256, 0, s>>>(h, rows, d, (bf16*)xn); KB_LAUNCH(); return;
-      case 4: k_rmsnorm_warp<4><<<blocks, 256, 0, s>>>(h, rows, d, (bf16*)xn); KB_LAUNCH(); return;
+      case 32: KB_CUDA(launch_pdl(k_rmsnorm_warp<32>, dim3(blocks), dim3(256), 0, s, h, rows, d, (bf16*)xn)); KB_LAUNCH(); return;
+      case 2: KB_CUDA(launch_pdl(k_rmsnorm_warp<2>, dim3(blocks), dim3(256), 0, s, h, rows, d, (bf16*)xn)); KB_LAUNCH(); return;
+      case 4: KB_CUDA(launch_pdl(k_rmsnorm_warp<4>, dim3(blocks), dim3(256), 0, s, h, rows, d, (bf16*)xn)); KB_LAUNCH(); return;
       default: break;
     }
   }
@@ -590,6 +594,8 @@ __global__ void __launch_bounds__(256) k_logits_vec(const float* __restrict__ h,
                                                     float* __restrict__ out) {
   constexpr int D = 256 * NV;
   __shared__ __align__(16) float hs[D];
+  pdl_trigger();
+  pdl_wait();
   for (int i = threadIdx.x; i < D; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -637,9 +643,9 @@ void launch_logits(const Ctx& c, cudaStream_t s, const float* h_last, float* log
         unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count > 0 ? c.sm_count : 148) * per_sm[vi]));
     cudaEvent_t kt0 = kt_begin(c, s);
     if (c.cfg.d == 4096)
-      k_logits_vec<16><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
+      KB_CUDA(launch_pdl(k_logits_vec<16>, dim3(grid), dim3(256), 0, s, h_last, (const bf16*)c.unembedT, V, logits));
     else
-      k_logits_vec<32><<<grid, 256, 0, s>>>(h_last, (const bf16*)c.unembedT, V, logits);
+      KB_CUDA(launch_pdl(k_logits_vec<32>, dim3(grid), dim3(256), 0, s, h_last, (const bf16*)c.unembedT, V, logits));
     KB_LAUNCH();
     kt_end(c, s, kt0, KT_LOGITS, 2.0 * double(V) * c.cfg.d, double(V) * c.cfg.d * 2.0 + double(V) * 4.0);
     return;
