@@ -152,6 +152,7 @@ struct AttnTc {
   bf16* out;       // [rows][H*HD]
   float* part;     // [slot][h][HD + 3][rows] (o..., m, l, mass) for split q tiles
   double* mass;    // [H][rows] region mass, may be null
+  float* stats;    // [H][rows][2] (m, l) in the log2 domain, may be null
   int64_t il, rs;
   int strict_pv;   // wait for PV(i) before S(i+1) (default; KRUL_ATTN_RELAXED=1 skips it)
   int dbg;         // tuning only: 1 = no softmax math, 3 = no MMAs, 4 = neither, 5 = barriers + TMA only
@@ -496,6 +497,10 @@ __global__ void __launch_bounds__(352, 1)
           }
         }
         if (valid && p.mass) p.mass[int64_t(h) * p.rows + row] = l > 0.f ? double(mn) / double(l) : 0.0;
+        if (valid && p.stats) {
+          p.stats[(int64_t(h) * p.rows + row) * 2] = m;
+          p.stats[(int64_t(h) * p.rows + row) * 2 + 1] = l;
+        }
       } else {
         // [slot][h][HD + 3][rows]: for each column the warp's 32 rows are
         // contiguous, so every store below is one coalesced 128-byte access
@@ -565,6 +570,10 @@ __global__ void __launch_bounds__(128) k_attn_combine(AttnTc p) {
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   if (do_mass && valid) p.mass[int64_t(h) * p.rows + row] = L > 0.f ? double(MN) / double(L) : 0.0;
+  if (p.stats && valid && blockIdx.z == 0 && wp == 0) {
+    p.stats[(int64_t(h) * p.rows + row) * 2] = M;
+    p.stats[(int64_t(h) * p.rows + row) * 2 + 1] = L;
+  }
   float acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
@@ -646,6 +655,7 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   p.v_rows_pp = int(pe / 64);
   p.out = static_cast<bf16*>(a.out);
   p.mass = a.mass;
+  p.stats = a.stats;
   p.il = a.mass ? a.il : 0;
   p.rs = a.mass ? a.rs : INT64_MAX;
   static const int strict = [] {

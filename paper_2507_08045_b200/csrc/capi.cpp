@@ -39,7 +39,7 @@ struct Est {
   Ctx* ctx = nullptr;
   std::vector<int> layers;
   int H = 1;
-  DevBuf d_layers, sums, partial, D, tmp;
+  DevBuf d_layers, sums, partial, D, tmp, ident;
   int64_t partial_cap = 0;
   bool prefill_done = false;
   int64_t prefill_rows = 0, decode_steps = 0;
@@ -257,7 +257,7 @@ int krul_capture_prefill(krul_ctx* ctx, int layer, int head, float* out, int64_t
   return guard([&] {
     need(ctx, "ctx");
     Ctx& c = *ctx->c;
-    if (!c.cap_valid || !c.capture_probs) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention");
+    if (!c.cap_valid || c.capture_probs != 1) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention");
     if (layer < 0 || layer >= c.cfg.N || head < 0 || head >= c.cfg.H) fail(KRUL_E_CONFIG, "index out of range");
     if (rows) *rows = c.cap_rows;
     if (width) *width = c.cap_width;
@@ -383,6 +383,48 @@ static void fold_decode_dev(Est& e, const float* rows, int64_t W, int64_t pitch,
   KB_CUDA(cudaStreamSynchronize(c.s_est));
   ++e.decode_steps;
 }
+// K2: the prefill fold without the probability record. The tracked layers'
+// probabilities are recomputed one key-column chunk at a time (bounded
+// scratch, independent of W) from the Q rows, the paged K and the softmax
+// statistics the prefill saved, and each chunk [n][H][rows x wc] is folded
+// by the decode-fold kernel (the sum over the full rows x width rectangle is
+// a sum over its column chunks, analysis.cpp:97-122).
+static void fold_prefill_recompute(Est& e, Ctx& c) {
+  if (e.prefill_done) fail(KRUL_E_ACCOUNTING, "prefill attention folded twice");
+  const int N = c.cfg.N, H = e.H, n = int(e.layers.size());
+  if (!e.layers.empty() && e.layers.back() >= N) fail(KRUL_E_CONFIG, "record does not cover all tracked layers");
+  const Conv* conv = c.cap_conv;
+  if (!conv || std::find(c.convs.begin(), c.convs.end(), conv) == c.convs.end() ||
+      conv->serial != c.cap_conv_serial)
+    fail(KRUL_E_STATE_CORRUPTION, "the captured prefill's conversation is gone");
+  const int64_t rows = c.cap_rows, W = c.cap_width, first_q = c.cap_first_q;
+  if (n >= 2 && rows > 0) {
+    const int sms = c.sm_count > 0 ? c.sm_count : 148;
+    const double per_col = double(n) * H * double(rows) * 4.0;
+    const int64_t wc = std::max<int64_t>(64, std::min<int64_t>((W + 63) / 64 * 64,
+                                                              int64_t((256.0 * 1024 * 1024) / per_col) / 64 * 64));
+    float* P = static_cast<float*>(e.tmp.ensure(size_t(n) * H * size_t(rows) * size_t(wc) * 4));
+    std::vector<int> ident(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) ident[size_t(i)] = i;
+    int* d_ident = static_cast<int*>(e.ident.ensure(size_t(n) * 4));
+    KB_CUDA(kb_memcpy_sync(d_ident, ident.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
+    const int64_t need_p = fold_direct_partial_elems(n, rows * wc, H, sms);
+    if (need_p > e.partial_cap) {
+      e.partial.ensure(size_t(need_p) * 8);
+      e.partial_cap = need_p;
+    }
+    cudaEvent_t kt0 = kt_begin(c, c.s_est);
+    for (int64_t c0 = 0; c0 < W; c0 += wc) {
+      launch_prefill_probs(c, c.s_est, *conv, e.d_layers.as<int>(), n, rows, first_q, c0, int(wc), P);
+      launch_fold_direct(c.s_est, P, int64_t(H) * rows * wc, rows * wc, rows * wc, H, d_ident, n,
+                         e.sums.as<double>(), e.partial.as<double>(), e.partial_cap, sms);
+    }
+    kt_end(c, c.s_est, kt0, KT_FOLD_PREFILL, 0.0, double(n) * H * double(rows) * double(W) * 4.0);
+    KB_CUDA(cudaStreamSynchronize(c.s_est));
+  }
+  e.prefill_done = true;
+  e.prefill_rows = rows;
+}
 int krul_est_fold_prefill(krul_est* est) {
   return guard([&] {
     need(est, "est");
@@ -392,7 +434,10 @@ int krul_est_fold_prefill(krul_est* est) {
     KB_CUDA(cudaSetDevice(c.device));
     KB_CUDA(cudaStreamSynchronize(c.s_comp));
     KB_CUDA(cudaStreamSynchronize(c.s_new));
-    fold_prefill_dev(e, c.cap_probs.as<float>(), c.cap_rows, c.cap_width, c.cfg.N);
+    if (c.capture_probs == 2)
+      fold_prefill_recompute(e, c);
+    else
+      fold_prefill_dev(e, c.cap_probs.as<float>(), c.cap_rows, c.cap_width, c.cfg.N);
   });
 }
 int krul_est_fold_decode(krul_est* est) {

@@ -206,6 +206,9 @@ cudaEvent_t Ctx::event() {
 Conv::~Conv() {
   if (ctx) {
     if (ctx->rg.conv_serial == serial) ctx->drop_graph();  // its kernels hold d_pt
+    auto& cv = ctx->convs;
+    cv.erase(std::remove(cv.begin(), cv.end(), this), cv.end());
+    if (ctx->cap_conv == this) ctx->cap_conv = nullptr;
     for (int p : pages) ctx->free_pages.push_back(p);
   }
   if (d_pt) cudaFree(d_pt);

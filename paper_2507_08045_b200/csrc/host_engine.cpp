@@ -213,6 +213,7 @@ Conv* conv_create(Ctx& c, int64_t capacity) {
   v->capacity = capacity;
   v->max_pages = maxp;
   v->serial = next_serial();
+  c.convs.push_back(v);
   v->pages.resize(need);
   for (size_t i = 0; i < need; ++i) {
     v->pages[i] = c.free_pages.back();
@@ -299,6 +300,9 @@ void layer_forward(Ctx& c, cudaStream_t s, const WS& w, Conv& conv, int l, const
   }
   if (fs && fs->computed) record_mark(*fs->computed, s);
   if (out_rows <= 0) return;
+  if (cap && cap->q_save)  // K2: the rotated Q of the captured rows
+    KB_CUDA(cudaMemcpyAsync(cap->q_save, w.q, size_t(fs ? fs->n_new : out_rows) * g.qd() * c.esz,
+                            cudaMemcpyDeviceToDevice, s));
   AttnArgs a = cap ? *cap : AttnArgs{};
   a.part = w.part;
   a.q = w.q;
@@ -381,13 +385,17 @@ static void prepare_capture(Ctx& c, cudaStream_t s, int64_t rows, int64_t W, int
   a.mass_rows = rows;
   a.il = c.cap_il;
   a.rs = c.cap_rs;
-  if (c.capture_probs) {
+  if (c.capture_probs == 1) {  // the reference's attention record, materialised
     const size_t n = size_t(g.N) * g.H * rows * W;
     float* p = static_cast<float*>(c.cap_probs.ensure(n * 4));
     KB_CUDA(cudaMemsetAsync(p, 0, n * 4, s));
     a.probs = p;
     a.ld_probs = W;
     a.probs_rows = rows;
+  } else if (c.capture_probs == 2) {  // K2: Q rows + softmax statistics only
+    a.q_save = c.cap_q.ensure(size_t(g.N) * rows * g.qd() * c.esz);
+    a.stats = static_cast<float*>(c.cap_stats.ensure(size_t(g.N) * g.H * rows * 2 * 4));
+    c.cap_stats_log2 = false;  // set per launch below (FA: log2 domain)
   }
   c.cap_valid = true;
 }
@@ -396,6 +404,8 @@ static AttnArgs capture_for_layer(const Ctx& c, const AttnArgs& base, int l) {
   const int64_t per_layer = int64_t(c.cfg.H) * base.probs_rows * base.ld_probs;
   if (a.probs) a.probs += l * per_layer;
   if (a.mass) a.mass += int64_t(l) * c.cfg.H * base.mass_rows;
+  if (a.stats) a.stats += int64_t(l) * c.cfg.H * base.mass_rows * 2;
+  if (a.q_save) a.q_save = static_cast<char*>(a.q_save) + size_t(l) * base.mass_rows * c.cfg.qd() * c.esz;
   return a;
 }
 
@@ -409,6 +419,8 @@ void forward_rows(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d_
   WS w = ws_get(c, set, n);
   AttnArgs cap{};
   prepare_capture(c, s, n, pos0 + n, pos0, cap);
+  c.cap_conv = &conv;
+  c.cap_conv_serial = conv.serial;
   launch_embed(c, s, d_tok, n, w.h);
   float* hin = w.h;
   float* hout = w.h2;
@@ -442,6 +454,8 @@ void forward_fused(Ctx& c, cudaStream_t s, int set, Conv& conv, const int32_t* d
   WS w = ws_get(c, set, n + p0);
   AttnArgs cap{};
   prepare_capture(c, s, n, L + n, L, cap);
+  c.cap_conv = &conv;
+  c.cap_conv_serial = conv.serial;
   launch_embed(c, s, d_new, n, w.h);
   if (p0 > 0) launch_embed(c, s, d_hist, p0, w.h + n * g.d);
   float* hin = w.h;

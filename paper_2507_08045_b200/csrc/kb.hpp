@@ -200,12 +200,19 @@ struct Ctx {
   // second workspace set for the concurrent new-input prefill stream
   DevBuf ws2_xn, ws2_qkv, ws2_q, ws2_attn, ws2_hmid, ws2_hmidc, ws2_act, ws2_y;
 
-  // capture
+  // capture (0 off, 1 the reference's materialised attention record, 2 K2:
+  // Q + softmax statistics, the estimator recomputes the probabilities)
   int capture_probs = 0;
+  const Conv* cap_conv = nullptr;  // the conversation the capture was taken on
+  uint64_t cap_conv_serial = 0;
+  std::vector<const Conv*> convs;  // live conversations (cap_conv validity)
   DevBuf cap_probs;       // [N][H][rows][W] f32 (when capture_probs)
   int64_t cap_rows = 0, cap_width = 0, cap_first_q = 0;
   bool cap_valid = false;
   DevBuf cap_mass;        // [N][H][rows] f64 region masses (classifier)
+  DevBuf cap_q;           // capture mode 2: [N][rows][H*hd] rotated Q of the prefill rows (cdt)
+  DevBuf cap_stats;       // capture mode 2: [N][H][rows][2] softmax (max, sum)
+  bool cap_stats_log2 = false;  // the stats' domain (FA: log2)
   double cap_ifrac = 0.1, cap_rfrac = 0.1;
   int64_t cap_il = 0, cap_rs = 0;
   DevBuf dec_rows;        // [N][H][dec_pitch] f32 last decode step (pitch: 16-byte rows)
@@ -323,6 +330,12 @@ struct AttnArgs {
   int64_t probs_rows = 0;   // rows per head in the capture
   double* mass = nullptr;   // optional [H][mass_rows] region mass
   int64_t mass_rows = 0;
+  // K2 (estimator prefill fold without the probability record): per row the
+  // softmax statistics (max, sum) [H][mass_rows][2] -- natural-log domain
+  // (SIMT: P = exp(s - m) / l) or log2 domain (FA: P = exp2(s log2e - m) / l)
+  // -- and a copy of the rotated Q rows [rows][H * hd]
+  float* stats = nullptr;
+  void* q_save = nullptr;
   int64_t il = 0, rs = 0;   // classifier regions [0,il) U [rs, W)
   DevBuf* part = nullptr;   // split-KV scratch owned by the calling stream
 };
@@ -369,6 +382,12 @@ void launch_fold_prefill(cudaStream_t s, const float* probs, int64_t rows, int64
                          const int* d_layers, int n, double* sums, double* partial,
                          int64_t partial_cap);
 void launch_finalize(cudaStream_t s, const double* sums, int n, int H, double* D);
+// K2 (fold.cu): the prefill probabilities of the tracked layers for key
+// columns [c0, c0 + wc), recomputed from the saved Q, the paged K and the
+// softmax statistics -> out [n][H][rows][wc] f32 (zero past a row's causal
+// width or the key count)
+void launch_prefill_probs(const Ctx& c, cudaStream_t s, const Conv& conv, const int* d_layers, int n,
+                          int64_t rows, int64_t first_q, int64_t c0, int wc, float* out);
 // K1 decode fold (fold.cu): rows [layer][head][.] f32 with 16-byte aligned
 // strides; part = per-(chunk, pair, head) f64 scratch
 int64_t fold_direct_partial_elems(int n, int64_t W, int H, int sms);

@@ -220,7 +220,7 @@ void launch_rope_scatter(const Ctx& c, cudaStream_t s, const float* qkv, int64_t
 template <class T>
 __global__ void k_attn_simt(const T* q, int64_t pos0, PageView pv, int H, float scale, T* out,
                             float* probs, int64_t ld_probs, int64_t probs_row0, int64_t probs_rows,
-                            double* mass, int64_t mass_rows, int64_t il, int64_t rs) {
+                            double* mass, int64_t mass_rows, int64_t il, int64_t rs, float* stats) {
   extern __shared__ float sm[];
   const int64_t r = blockIdx.x;
   const int h = blockIdx.y;
@@ -248,6 +248,10 @@ __global__ void k_attn_simt(const T* q, int64_t pos0, PageView pv, int H, float 
     sum += e;
   }
   sum = block_sum(sum);
+  if (stats && threadIdx.x == 0) {
+    stats[(int64_t(h) * mass_rows + probs_row0 + r) * 2] = mx;
+    stats[(int64_t(h) * mass_rows + probs_row0 + r) * 2 + 1] = sum;
+  }
   double ms = 0.0;
   for (int64_t k = threadIdx.x; k < W; k += blockDim.x) {
     const float p = sc[k] / sum;
@@ -465,7 +469,7 @@ static bool attention_decode_supported(const Ctx& c, const AttnArgs& a) {
   }();
   return !simt && a.rows == 1 && c.cfg.dtype == KRUL_BF16 && c.cfg.hd == 128 && c.cfg.H % c.cfg.Hkv == 0 &&
          c.cfg.H / c.cfg.Hkv <= kDecMaxG && (!a.probs || a.probs_rows == 1) && a.probs_row0 == 0 &&
-         (!a.mass || a.mass_rows == 1);
+         (!a.mass || a.mass_rows == 1) && !a.stats;
 }
 static void launch_attention_decode(const Ctx& c, cudaStream_t s, const Conv& conv, int layer, const AttnArgs& a) {
   PageView pv = page_view(c, conv, layer);
@@ -485,6 +489,7 @@ static void launch_attention_decode(const Ctx& c, cudaStream_t s, const Conv& co
 void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
                       const AttnArgs& a) {
   if (a.rows <= 0) return;
+  if (a.stats) const_cast<Ctx&>(c).cap_stats_log2 = a.part && attention_tc_supported(c, a);
   if (a.part && attention_tc_supported(c, a)) {
     // algorithmic flops: QK^T + PV over the causally visible keys of each row
     const double vis = double(a.rows) * double(a.pos0) + 0.5 * double(a.rows) * double(a.rows + 1);
@@ -508,14 +513,105 @@ void launch_attention(const Ctx& c, cudaStream_t s, const Conv& conv, int layer,
     KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     k<<<grid, 128, smem, s>>>((const bf16*)a.q, a.pos0, pv, c.cfg.H, scale, (bf16*)a.out, a.probs,
                               a.ld_probs, a.probs_row0, a.probs_rows, a.mass, a.mass_rows, a.il,
-                              a.rs);
+                              a.rs, a.stats);
   } else {
     auto k = k_attn_simt<float>;
     KB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     k<<<grid, 128, smem, s>>>((const float*)a.q, a.pos0, pv, c.cfg.H, scale, (float*)a.out,
                               a.probs, a.ld_probs, a.probs_row0, a.probs_rows, a.mass,
-                              a.mass_rows, a.il, a.rs);
+                              a.mass_rows, a.il, a.rs, a.stats);
   }
+  KB_LAUNCH();
+}
+
+// ---------------------------------------------------------------- K2 probabilities
+// The prefill attention probabilities of tracked layer layers[li] for key
+// columns [c0, c0 + 64 * gridDim.x), recomputed (never the whole record):
+// CTA = (li, kv head g, 64-key block) stages the block's K rows (one page)
+// in shared memory as f32 and every thread scores one query row (head of
+// the GQA group, prefill row) of the Q saved by the prefill against the 64
+// keys. The arithmetic is the attention kernel's own: the dot product in
+// the order t = 0..hd-1 and P = exp(s - m) / l (SIMT, f32: bit-identical
+// to its capture) or P = exp2(s log2e - m) / l with the ex2 approximation
+// (FA, bf16), m and l being the softmax statistics the kernel saved.
+template <class T, int HD>
+__global__ void __launch_bounds__(256) k_prefill_probs(const T* __restrict__ qsave, const float* __restrict__ stats,
+                                                       PageView pv, const int* __restrict__ pt_base,
+                                                       int64_t pt_stride, const int* __restrict__ layers, int H,
+                                                       int64_t rows, int64_t first_q, int64_t c0, int wc,
+                                                       float scale, int log2dom, float* __restrict__ out) {
+  __shared__ float ks[64][HD + 1];
+  const int li = blockIdx.z, g = blockIdx.y;
+  const int64_t k0 = c0 + int64_t(blockIdx.x) * 64;
+  const int layer = layers[li];
+  pv.pt = pt_base + int64_t(layer) * pt_stride;
+  const int64_t kv_total = first_q + rows;
+  const int grp = H / pv.Hkv;
+  for (int i = threadIdx.x; i < 64 * HD; i += blockDim.x) {
+    const int kk = i / HD, t = i % HD;
+    const int64_t key = k0 + kk;
+    ks[kk][t] = key < kv_total ? tof(reinterpret_cast<const T*>(pv.page(key))[pv.k_off(g, key, t)]) : 0.f;
+  }
+  __syncthreads();
+  const int64_t qd = int64_t(H) * HD;
+  for (int64_t qi = threadIdx.x; qi < int64_t(grp) * rows; qi += blockDim.x) {
+    const int h = g * grp + int(qi / rows);
+    const int64_t r = qi % rows;
+    float q[HD];
+    const T* qr = qsave + (int64_t(li) * rows + r) * qd + int64_t(h) * HD;
+#pragma unroll
+    for (int t = 0; t < HD; ++t) q[t] = tof(qr[t]);
+    const float m = stats[((int64_t(li) * H + h) * rows + r) * 2];
+    const float l = stats[((int64_t(li) * H + h) * rows + r) * 2 + 1];
+    const int64_t last = first_q + r;  // causal: keys <= the row's position
+    float* o = out + ((int64_t(li) * H + h) * rows + r) * wc + (k0 - c0);
+    for (int kk = 0; kk < 64; kk += 4) {
+      float pr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float dot = 0.f;
+#pragma unroll
+        for (int t = 0; t < HD; ++t) dot += q[t] * ks[kk + u][t];
+        float pv_ = 0.f;
+        if (k0 + kk + u <= last && k0 + kk + u < kv_total) {
+          const float sv = __fmul_rn(dot, scale);  // rounded like the kernels' stored scores
+          if (log2dom) {
+            float e;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(sv - m));
+            pv_ = e / l;
+          } else {
+            pv_ = expf(sv - m) / l;
+          }
+        }
+        pr[u] = pv_;
+      }
+      *reinterpret_cast<float4*>(o + kk) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+    }
+  }
+}
+void launch_prefill_probs(const Ctx& c, cudaStream_t s, const Conv& conv, const int* d_layers, int n,
+                          int64_t rows, int64_t first_q, int64_t c0, int wc, float* out) {
+  if (n <= 0 || rows <= 0 || wc <= 0) return;
+  if (wc % 64 || c0 % 64) fail(KRUL_E_CUDA, "prefill probability chunks must be whole 64-key blocks");
+  PageView pv = page_view(c, conv, 0);
+  const dim3 grid(unsigned(wc / 64), unsigned(c.cfg.Hkv), unsigned(n));
+  const bool lg = c.cap_stats_log2;
+  const float scale = lg ? (1.0f / sqrtf(float(c.cfg.hd))) * 1.4426950408889634f : 1.0f / sqrtf(float(c.cfg.hd));
+  const float* st = c.cap_stats.as<float>();
+#define KB_PP(T, HDV)                                                                                         \
+  k_prefill_probs<T, HDV><<<grid, 256, 0, s>>>(static_cast<const T*>(c.cap_q.p), st, pv, conv.d_pt,          \
+                                               int64_t(conv.max_pages), d_layers, c.cfg.H, rows, first_q, c0, \
+                                               wc, scale, lg ? 1 : 0, out)
+  if (c.cfg.dtype == KRUL_BF16 && c.cfg.hd == 128) KB_PP(bf16, 128);
+  else if (c.cfg.dtype == KRUL_BF16 && c.cfg.hd == 64) KB_PP(bf16, 64);
+  else if (c.cfg.dtype == KRUL_F32 && c.cfg.hd == 64) KB_PP(float, 64);
+  else if (c.cfg.dtype == KRUL_F32 && c.cfg.hd == 128) KB_PP(float, 128);
+  else if (c.cfg.dtype == KRUL_F32 && c.cfg.hd == 4) KB_PP(float, 4);
+  else if (c.cfg.dtype == KRUL_F32 && c.cfg.hd == 8) KB_PP(float, 8);
+  else if (c.cfg.dtype == KRUL_F32 && c.cfg.hd == 16) KB_PP(float, 16);
+  else if (c.cfg.dtype == KRUL_F32 && c.cfg.hd == 32) KB_PP(float, 32);
+  else fail(KRUL_E_CONFIG, "estimator prefill recompute: unsupported head_dim");
+#undef KB_PP
   KB_LAUNCH();
 }
 

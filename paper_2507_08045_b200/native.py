@@ -230,8 +230,12 @@ class Context:
         """Exponent-code bf16 snapshots at compress (lossless; default on)."""
         _check(lib().krul_set_kv_coding(self.h, int(bool(on))))
 
-    def set_capture(self, probs: bool):
-        _check(lib().krul_set_capture(self.h, int(bool(probs))))
+    def set_capture(self, mode):
+        """Attention capture of later prefills: False/0 off, True/1 the
+        reference's materialised probability record, 2 the estimator's
+        recompute mode (Q rows + softmax statistics; fold_prefill recomputes
+        the probabilities chunk by chunk)."""
+        _check(lib().krul_set_capture(self.h, int(mode)))
 
     def set_classifier_regions(self, initial_frac=0.1, recent_frac=0.1):
         _check(lib().krul_set_classifier_regions(self.h, C.c_double(initial_frac),

@@ -45,6 +45,9 @@ class TurnConfig:
     merge: int = K.MERGE_MEAN     # BenchConfig::merge
     cost: K.CostModel = field(default_factory=K.CostModel)  # reference defaults F=312e12, B=139e9
     rc_grid_step: float = 0.05
+    # prefill attention for the estimator: 2 = recompute (K2, no record; the
+    # attention stays on the tcgen05 path), 1 = the materialised record
+    capture: int = 2
     # B200 extension: the split from measured stream rates (calibrate_rc_measured,
     # scheduler.cpp:402-443). Called as calibrate(state, pairs, total_len) -> r_c at
     # the end of the turn, with the turn's full KV in state.conv; None keeps the
@@ -101,7 +104,7 @@ class KrulTurns:
         tokens = np.concatenate([self.history, user]).astype(np.int32)
         ttft, stats = None, None
         # the estimator's prefill fold reads this prefill's attention record
-        ctx.set_capture(True)
+        ctx.set_capture(cfg.capture)
         try:
             if t == 0 or self.snapshot is None:                      # harness.cpp:124-126
                 logits = ctx.prefill(self.conv, tokens)

@@ -887,3 +887,91 @@ def test_calibrate_rc_measured_contract(K, oracle):
     assert b > 1e9 and f > 1e12
     cm = K.CostModel.for_model(cfg, f, b)
     assert K.calibrate_rc(cm, cfg.n_layers, L, cfg.d_model, pairs) in list(K.default_rc_grid())
+
+
+@pytest.mark.parametrize("r_c", [0.0, 0.25])
+def test_llama_width_restore_matches_oracle(K, oracle, r_c):
+    """Production shape against the CPU oracle (not the repo's own SIMT
+    path): 2 layers at full Llama-3-8B width (d=4096, GQA 32/8, hd=128,
+    SwiGLU F=14336, rope theta 5e5), bf16 tcgen05 kernels throughout --
+    history prefill, exponent-coded snapshot, the two-stream restore (the
+    r_c=0.25 plan recomputes a 1024 / 0 prefix on the CTA-pair GEMM + FA
+    attention while the rest loads), the 128-row new-input prefill
+    (weight-streaming GEMMs + FA attention), then a decode step (split-key
+    decode attention). Restored K/V, new-input logits, decode logits and the
+    decode attention rows vs the oracle's f32 prefill / decode on the same
+    weights: relative Frobenius <= 2e-2 (bf16 tolerance)."""
+    shape = dict(n_layers=2, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, vocab_size=512,
+                 ffn_mult=3.5, ffn_kind=1, rope_theta=500000.0, seed=21)
+    om = oracle.Model(oracle.ModelConfig(**shape))
+    cfg = K.ModelConfig(**shape, dtype=K.KRUL_BF16, max_tokens=2304)
+    ctx = K.Context(cfg, 0)
+    ctx.upload_weights(om.weights())
+    L, n = 2048, 128
+    hist = oracle.tokens(L, 31, cfg.vocab_size)
+    new = oracle.tokens(n, 32, cfg.vocab_size)
+    prev = ctx.conversation(2304)
+    ctx.prefill(prev, hist)
+    plan = K.build_plan(L, 2, r_c)
+    snap = K.KVSnapshot.compress(ctx, prev, [], plan, L, K.MERGE_KEEP_DEEPER)
+    assert snap.coding()["coded"]
+    conv = ctx.conversation(2304)
+    for _ in range(2):  # eager, then the captured graph
+        logits, _, _ = ctx.restore_and_prefill(conv, hist, snap, new)
+    ref = om.prefill(np.concatenate([hist, new]), capture=False)
+    assert rel_fro(logits, ref.logits()) <= 2e-2, rel_fro(logits, ref.logits())
+    okv = ref.take_kv()
+    for l in range(2):
+        gk, gv = conv.kv(l, 0, L + n)
+        ok_, ov = okv.layer(l)
+        ek, ev = rel_fro(gk, ok_), rel_fro(gv, ov)
+        assert ek <= 2e-2 and ev <= 2e-2, (l, ek, ev)
+    tok = 7
+    dl = ctx.decode_step(conv, tok)
+    rows = ctx.captured_decode()
+    ol, orows = om.decode(okv, tok)
+    assert rel_fro(dl, ol) <= 2e-2, rel_fro(dl, ol)
+    assert rel_fro(rows, orows) <= 2e-2, rel_fro(rows, orows)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_prefill_fold_recompute_matches_record(K, oracle, dtype):
+    """K2 without the attention record: fold_prefill over capture mode 2
+    (Q + softmax statistics, probabilities recomputed per key chunk) equals
+    the fold over the materialised record (mode 1) -- f32: the recomputed
+    probabilities are bit-identical, sums rel <= 1e-6 (the two folds sum in
+    different orders); bf16: mode 2 keeps the tcgen05 FA kernel, mode 1 runs
+    the SIMT kernel that writes the record, so the sums agree to the bf16
+    attention tolerance (2e-2). The f32 sums also match the oracle's
+    SimilarityAccumulator::fold_prefill (analysis.cpp:97-122) on the same
+    weights and tokens."""
+    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    if dtype == "bf16":
+        kw.update(n_kv_heads=2, head_dim=128, d_model=512, ffn_kind=1, ffn_mult=3.5)
+    om = oracle.Model(oracle.ModelConfig(**kw))
+    cfg = K.ModelConfig(**kw, dtype=K.KRUL_F32 if dtype == "f32" else K.KRUL_BF16, max_tokens=640)
+    ctx = K.Context(cfg, 0)
+    ctx.upload_weights(om.weights())
+    hist, new = oracle.tokens(320, 41, cfg.vocab_size), oracle.tokens(48, 42, cfg.vocab_size)
+    sums = {}
+    for mode in (1, 2):
+        conv = ctx.conversation(640)
+        ctx.set_capture(0)
+        ctx.prefill(conv, hist)
+        ctx.set_capture(mode)
+        ctx.prefill_new(conv, new)
+        ctx.set_capture(0)
+        est = K.StreamingEstimator(ctx, list(range(cfg.n_layers)))
+        est.fold_prefill()
+        sums[mode] = est.sums()
+        assert est.counts()[0] == 48
+        del conv
+    rel = np.abs(sums[2] - sums[1]) / np.maximum(np.abs(sums[1]), 1e-30)
+    assert rel.max() <= (1e-6 if dtype == "f32" else 2e-2), rel.max()
+    if dtype == "f32":
+        pf = om.prefill(np.concatenate([hist, new]), preload=om.prefill(hist).take_kv().suffix([0] * 4))
+        acc = oracle.Accumulator(list(range(4)), 4)
+        acc.fold_prefill_handle(pf)
+        want = acc.sums()
+        rel = np.abs(sums[2] - want) / np.maximum(np.abs(want), 1e-30)
+        assert rel.max() <= 1e-5, rel.max()
