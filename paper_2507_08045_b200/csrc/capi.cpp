@@ -257,7 +257,7 @@ int krul_capture_prefill(krul_ctx* ctx, int layer, int head, float* out, int64_t
   return guard([&] {
     need(ctx, "ctx");
     Ctx& c = *ctx->c;
-    if (!c.cap_valid || c.capture_probs != 1) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention");
+    if (!c.cap_valid || c.cap_mode != 1) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention");
     if (layer < 0 || layer >= c.cfg.N || head < 0 || head >= c.cfg.H) fail(KRUL_E_CONFIG, "index out of range");
     if (rows) *rows = c.cap_rows;
     if (width) *width = c.cap_width;
@@ -430,11 +430,11 @@ int krul_est_fold_prefill(krul_est* est) {
     need(est, "est");
     Est& e = *est->e;
     Ctx& c = *e.ctx;
-    if (!c.cap_valid || !c.capture_probs) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention (krul_set_capture)");
+    if (!c.cap_valid || !c.cap_mode) fail(KRUL_E_STATE_CORRUPTION, "no captured prefill attention (krul_set_capture)");
     KB_CUDA(cudaSetDevice(c.device));
     KB_CUDA(cudaStreamSynchronize(c.s_comp));
     KB_CUDA(cudaStreamSynchronize(c.s_new));
-    if (c.capture_probs == 2)
+    if (c.cap_mode == 2)
       fold_prefill_recompute(e, c);
     else
       fold_prefill_dev(e, c.cap_probs.as<float>(), c.cap_rows, c.cap_width, c.cfg.N);

@@ -376,6 +376,7 @@ static void prepare_capture(Ctx& c, cudaStream_t s, int64_t rows, int64_t W, int
   const Cfg& g = c.cfg;
   c.cap_rows = rows;
   c.cap_width = W;
+  c.cap_mode = c.capture_probs;
   c.cap_first_q = first_q;
   c.cap_il = int64_t(c.cap_ifrac * double(W));
   const int64_t rl = int64_t(c.cap_rfrac * double(W));

@@ -203,6 +203,7 @@ struct Ctx {
   // capture (0 off, 1 the reference's materialised attention record, 2 K2:
   // Q + softmax statistics, the estimator recomputes the probabilities)
   int capture_probs = 0;
+  int cap_mode = 0;                // capture_probs when the last capture was taken
   const Conv* cap_conv = nullptr;  // the conversation the capture was taken on
   uint64_t cap_conv_serial = 0;
   std::vector<const Conv*> convs;  // live conversations (cap_conv validity)
