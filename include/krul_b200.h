@@ -4,8 +4,9 @@
  * (/root/reference/proj) is a C++ static library consumed through
  * proj/include/krul/ headers; it has no FFI. Each entry point below replaces one
  * reference call on the hot path (cited as `proj/<file>:<line>`); the C++
- * host API in include/krul/ and the Python mirror in
- * paper_2507_08045_b200/ are thin layers over exactly these symbols.
+ * drop-in include/krul_b200.hpp (compiled against the reference's own
+ * krul/common.hpp + krul/plan.hpp, tests/cpp/test_shim.cpp) and the Python
+ * mirror in paper_2507_08045_b200/ are thin layers over exactly these symbols.
  *
  * Conventions
  *  - Every function returns a krul_status (0 = KRUL_OK). Errors are raised
