@@ -208,6 +208,51 @@ __device__ __forceinline__ void epi_elem(const Epi& e, int64_t r, int64_t c, flo
 }
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
 
+// Where the epilogue's accumulator values come from. Default: this CTA's TMEM.
+// Cluster split-K (cs > 1): the cs CTAs of a thread-block cluster computed
+// the same tile over disjoint k ranges and stashed their fp32 accumulators in
+// their own (drained) operand rings, laid out [chunk][warp][column][lane];
+// the CTA of rank r owns the chunks with (chunk / unit) % cs == r and sums
+// them over the cluster's ranks through distributed shared memory, in rank
+// order (deterministic). A reduce-scatter inside the GEMM: no fp32 partials
+// in global memory, no reduce kernel.
+struct AccSrc {
+  int cs = 1, rank = 0, q = 0;
+  uint32_t red = 0;  // shared::cta address of this CTA's stash
+  __device__ __forceinline__ bool owns(int col, int unit) const { return cs <= 1 || (col / unit) % cs == rank; }
+};
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t sa, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sa), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float dsmem_ld(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// stash offset (bytes) of column crel + j, this warp, this lane
+__device__ __forceinline__ uint32_t red_off(int crel, int q, int j, int lane) {
+  return uint32_t((((crel >> 5) * 4 + q) * 32 + j) * 32 + lane) * 4u;
+}
+__device__ __forceinline__ void acc_ld32(const AccSrc& src, uint32_t taddr, int crel, float* v) {
+  if (src.cs <= 1) {
+    tc::tmem_ld32(taddr, v);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = 0.f;
+  for (int r = 0; r < src.cs; ++r) {
+    const uint32_t b = dsmem_map(src.red + red_off(crel, src.q, 0, lane), r);
+    float t[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t[j] = dsmem_ld(b + uint32_t(j) * 128u);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += t[j];
+  }
+}
+
 // One 32x32 accumulator block of an epilogue warp: TMEM lanes row0..row0+31
 // (this warp's quadrant), columns col0..col0+31. tcgen05.ld gives thread =
 // row; the block is transposed through padded smem (`my`, 32x33 floats) so
@@ -215,7 +260,8 @@ __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f +
 // residual operand (RESID) is prefetched before the TMEM load so its latency
 // overlaps it. P != nullptr stores an fp32 split-K partial instead.
 __device__ __forceinline__ void epi_block(const Epi& e, float* my, uint32_t taddr, int64_t row0,
-                                          int64_t col0, int64_t M, int64_t N, float* P) {
+                                          int64_t col0, int64_t M, int64_t N, float* P,
+                                          const AccSrc& src = AccSrc(), int crel = 0) {
   const int lane = threadIdx.x & 31;
   const int64_t col = col0 + lane;
   const bool cok = col < N;
@@ -229,7 +275,7 @@ __device__ __forceinline__ void epi_block(const Epi& e, float* my, uint32_t tadd
     }
   }
   float v[32];
-  tc::tmem_ld32(taddr, v);
+  acc_ld32(src, taddr, crel, v);
   if (!P && e.kind == Epi::NONE) return;
   if (!P && e.kind == Epi::F32_DIRECT) {  // debug: row-per-thread 16-byte stores, no transpose
     const int64_t r = row0 + lane;
@@ -331,7 +377,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // contiguous 64-byte run. hd % 32 == 0 so a chunk never straddles a head.
 template <int BN>
 __device__ __forceinline__ void epi_qkv(const Epi& e, uint32_t tbase, int64_t row0, int64_t col0,
-                                        int64_t M, int64_t N) {
+                                        int64_t M, int64_t N, const AccSrc& src = AccSrc()) {
   const EpiKV& kv = e.kv;
   const int lane = threadIdx.x & 31;
   const int64_t r = row0 + lane;
@@ -345,8 +391,9 @@ __device__ __forceinline__ void epi_qkv(const Epi& e, uint32_t tbase, int64_t ro
   for (int c = 0; c < BN; c += 32) {
     const int64_t cc = col0 + c;
     if (cc >= N) break;
+    if (!src.owns(c, 32)) continue;
     float v[32];
-    tc::tmem_ld32(tbase + uint32_t(c), v);
+    acc_ld32(src, tbase + uint32_t(c), c, v);
     if (!rok) continue;
     const bool isq = cc < nq, isk = !isq && cc < nq + nkv;
     if (isq || isk) {
@@ -400,7 +447,7 @@ __device__ __forceinline__ void epi_qkv(const Epi& e, uint32_t tbase, int64_t ro
 template <int KIND, int BN>
 __device__ __forceinline__ void epi_unit(const Epi& e, const CUtensorMap* tmC, unsigned char* stage,
                                          int& sbuf, uint32_t tbase, int64_t row0, int64_t col0,
-                                         int64_t M, int64_t N, int ks) {
+                                         int64_t M, int64_t N, int ks, const AccSrc& src = AccSrc()) {
   constexpr int ACC = (KIND == EK_SWIGLU) ? 128 : (KIND == EK_CDT || KIND == EK_TANH) ? 64 : 32;
   constexpr int PIECES = 128 / (ACC / 32) / 16;  // 16-byte pieces per 32-column chunk
   const int lane = threadIdx.x & 31;
@@ -409,6 +456,7 @@ __device__ __forceinline__ void epi_unit(const Epi& e, const CUtensorMap* tmC, u
 #pragma unroll 1
   for (int t = 0; t < BN; t += ACC) {
     if (col0 + t >= N) break;
+    if (!src.owns(t, ACC)) continue;
     unsigned char* tile = stage + sbuf * 4096;
     if (lane == 0) tc::bulk_wait_read1();
     __syncwarp();
@@ -433,7 +481,7 @@ __device__ __forceinline__ void epi_unit(const Epi& e, const CUtensorMap* tmC, u
         }
       }
       float v[32];
-      tc::tmem_ld32(tbase + uint32_t(t + c), v);
+      acc_ld32(src, tbase + uint32_t(t + c), t + c, v);
       uint32_t w[32];  // packed output words of this chunk for this row
       if constexpr (KIND == EK_F32 || KIND == EK_PARTIAL || KIND == EK_NONE) {
 #pragma unroll
@@ -531,7 +579,16 @@ struct Unit {
 // the CTAs touching that tile (fixed order -> deterministic reduce).
 // Otherwise units (m, n, split) are dealt round-robin, m fastest.
 __device__ __forceinline__ bool unit_at(int i, int mt, int nt, int splits, int kb_per, int num_k, int sk_G,
-                                        long long sk_T, Unit& u) {
+                                        long long sk_T, Unit& u, int cs = 1) {
+  if (cs > 1) {  // cluster split-K: one unit per CTA, cluster = tile, rank = k slice
+    if (i > 0) return false;
+    u.m = 0;
+    u.n = int(blockIdx.x) / cs;
+    u.ks = int(blockIdx.x) % cs;
+    u.k0 = u.ks * kb_per;
+    u.k1 = min(num_k, u.k0 + kb_per);
+    return true;
+  }
   if (sk_T > 0) {
     const long long c = blockIdx.x;
     const long long beg = c * sk_T / sk_G, end = (c + 1) * sk_T / sk_G;
@@ -574,7 +631,7 @@ template <int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int mt, int nt, int splits, int kb_per, Epi e,
-              float* __restrict__ partial, int sk_G, long long sk_T) {
+              float* __restrict__ partial, int sk_G, long long sk_T, int cs) {
   constexpr int BM = 128, BK = 64;
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   extern __shared__ unsigned char smem_raw[];
@@ -625,7 +682,7 @@ __global__ void __launch_bounds__(192, 1)
       // weights do not depend on the preceding kernel: the first unit's first
       // stages of B are in flight before the dependency wait (PDL)
       int pre = 0;
-      if (unit_at(0, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un)) {
+      if (unit_at(0, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un, cs)) {
         pre = min(STAGES, un.k1 - un.k0);
         for (int q = 0; q < pre; ++q) {
           tc::mbar_expect_tx(&full[q], A_BYTES + B_BYTES);
@@ -633,7 +690,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       pdl_wait();
-      for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
+      for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un, cs); ++i) {
         for (int kb = un.k0; kb < un.k1; ++kb) {
           if (i == 0 && kb - un.k0 < pre) {  // first pass over the ring: B already issued
             tc::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, un.m * BM);
@@ -660,7 +717,7 @@ __global__ void __launch_bounds__(192, 1)
       int s = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       Unit un;
-      for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
+      for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un, cs); ++i) {
         const int k0 = un.k0, k1 = un.k1;
         tc::mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this accumulator
         tc::fence_after();
@@ -696,13 +753,22 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t aph = 0;
     Unit un;
-    for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un); ++i) {
+    for (int i = 0; unit_at(i, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un, cs); ++i) {
       const int m = un.m, n = un.n, ks = un.ks;
       tc::mbar_wait(&tfull[acc], aph);
       tc::fence_after();
       const int64_t row0 = int64_t(m) * BM + 32 * q;
       float* P = partial ? partial + int64_t(ks) * M * N : nullptr;
-      if constexpr (KIND == EK_GENERIC) {
+      if (cs > 1) {  // stash the partial tile in the drained ring; reduced below
+        float* red = reinterpret_cast<float*>(base);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tc::tmem_ld32(tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + c), v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) red[red_off(c, q, j, lane) / 4] = v[j];
+        }
+      } else if constexpr (KIND == EK_GENERIC) {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           if (int64_t(n) * BN + c >= N) break;
@@ -723,6 +789,37 @@ __global__ void __launch_bounds__(192, 1)
         aph ^= 1;
       }
     }
+  }
+  if (cs > 1) {
+    // every stash of the cluster is written -> reduce-scatter over DSMEM
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp >= 2) {
+      Unit un;
+      unit_at(0, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un, cs);
+      AccSrc src;
+      src.cs = cs;
+      src.rank = un.ks;
+      src.q = warp & 3;
+      src.red = tc::smem_u32(base);
+      const int q = warp & 3;
+      float* my = stg + q * 32 * 33;
+      unsigned char* stage = reinterpret_cast<unsigned char*>(stg) + q * 8192;
+      int sbuf = 0;
+      const int64_t row0 = 32 * q;
+      if constexpr (KIND == EK_GENERIC) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (int64_t(un.n) * BN + c >= N) break;
+          if (src.owns(c, 32)) epi_block(e, my, 0u, row0, int64_t(un.n) * BN + c, M, N, nullptr, src, c);
+        }
+      } else if constexpr (KIND == EK_QKV) {
+        epi_qkv<BN>(e, 0u, row0, int64_t(un.n) * BN, M, N, src);
+      } else {
+        epi_unit<KIND, BN>(e, &tmC, stage, sbuf, 0u, row0, int64_t(un.n) * BN, M, N, 0, src);
+      }
+    }
+    // the peers have read this CTA's stash
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
   if (warp >= 2 && lane == 0) tc::bulk_wait_all();
   tc::fence_before();
@@ -1171,7 +1268,13 @@ struct GemmPlan {
   // stream-K (single m-tile, 1-SM kernel): grid CTAs share T = nt * num_k
   // k-block iterations evenly; `splits` = partial slots (max pieces per tile)
   long long sk_T = 0;
+  int cs = 1;  // > 1: cluster split-K, cs CTAs per tile reduce over DSMEM (grid = nt * cs)
 };
+
+// Clusters of `cs` CTAs of the 1-SM kernel (BN-wide tiles, one CTA per SM)
+// that can be resident at once -- the cluster split-K grid must fit in one
+// wave (a cluster waiting for a second wave would serialise the tail).
+int max_clusters(int bn, int cs);
 
 
 // Pick the kernel (1-SM 128xBN or 2-SM 256x256), tile width and split-K
@@ -1179,16 +1282,19 @@ struct GemmPlan {
 // weight bytes streamed from HBM by this SM (shared by the co-resident
 // m-tiles), operand bytes through L2 -> SM at the measured ~75 B/ns/SM);
 // times the k-blocks on the busiest SM, plus the split-K partial round trip.
-GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
+GemmPlan plan_gemm_f(int64_t M, int64_t N, int64_t K, int sms, bool allow_split, bool cs_ok, int force,
+                     bool* found) {
   const int64_t num_k = (K + 63) / 64;
-  const int force = g_gemm_force;
   GemmPlan best;
   double best_t = 1e30;
+  GemmPlan cl;  // the cluster split-K candidate of the automatic plan
+  cl.grid = 0;
+  cl.cs = 99;
   // constants fitted to a measured sweep of every (variant, split) on the
   // pyramid / new-input shapes with weights streamed from HBM
   // (tools/gemm_sweep.py, 8B + 70B shapes; regret of the chosen plan 3.6% -> 2.1%)
   const double l2_bw = 140.0, hbm_bw = 7000.0, clk = 1.85, unit_ns = 2000.0, pair_eff = 0.8,
-               split_ns = 1500.0, split_bw = 3000.0;
+               split_ns = 1500.0, split_bw = 3000.0, cs_ns = 1500.0;
   for (int variant = 0; variant < 3; ++variant) {
     const bool pair = variant == 0;
     const int bn = variant == 2 ? 128 : 256;
@@ -1199,7 +1305,7 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
       continue;
     const int64_t mt = (M + bm - 1) / bm, nt = (N + bn - 1) / bn;
     const int64_t slots = pair ? sms / 2 : sms;
-    for (int s = 1; s <= 16; ++s) {
+    for (int s = 1; s <= 16 && force != 11 && force != 12; ++s) {
       const int64_t kb_per = (num_k + s - 1) / s;
       const int64_t splits = (num_k + kb_per - 1) / kb_per;
       if (splits != s) continue;
@@ -1227,6 +1333,39 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
         best.kb_per = int(kb_per);
         best.grid = int(active) * (pair ? 2 : 1);
         best.sk_T = 0;
+        best.cs = 1;
+      }
+    }
+    // cluster split-K (one m-tile, 1-SM kernel): cs CTAs per tile over
+    // disjoint k ranges, reduced through DSMEM inside the GEMM (debug force
+    // 11 / 12 = only these with 256- / 128-wide tiles, g_gemm_splits = cs;
+    // force 9 = auto without them)
+    const bool cs_forced = (force == 11 && bn == 256) || (force == 12 && bn == 128);
+    if (!pair && mt == 1 && allow_split && cs_ok && (force == 0 || cs_forced)) {
+      for (int cs = 2; cs <= 4; ++cs) {
+        if (cs_forced && g_gemm_splits > 0 && cs != g_gemm_splits) continue;
+        const int64_t kb_per = (num_k + cs - 1) / cs;
+        if ((cs - 1) * kb_per >= num_k) continue;  // every rank gets k blocks
+        const int64_t ctas = nt * cs;
+        if (ctas > sms || nt > max_clusters(bn, cs)) continue;
+        GemmPlan cp;
+        cp.bn = bn;
+        cp.splits = 1;
+        cp.kb_per = int(kb_per);
+        cp.grid = int(ctas);
+        cp.cs = cs;
+        if (cs_forced) {
+          if (best_t > 0.0) {
+            best_t = 0.0;
+            best = cp;
+          }
+        } else if (ctas > cl.grid || (ctas == cl.grid && cs < cl.cs) ||
+                   (ctas == cl.grid && cs == cl.cs && bn == 128)) {
+          // measured (tools/gemm_cs_sweep.py, Llama-3-8B / 70B weight-streaming
+          // shapes): the cluster plan with the most CTAs wins, then the smaller
+          // cluster; the cost model's per-k-block terms do not rank these
+          cl = cp;
+        }
       }
     }
     // stream-K: one m-tile, every SM streams T / sms weight blocks
@@ -1256,11 +1395,23 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split) {
           best.kb_per = 0;
           best.grid = sms;
           best.sk_T = T;
+          best.cs = 1;
         }
       }
     }
   }
+  if (force == 0 && g_gemm_splits <= 0 && cl.grid >= 64) {
+    *found = true;
+    return cl;
+  }
+  *found = best_t < 1e30;
   return best;
+}
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t K, int sms, bool allow_split, bool cs_ok = false) {
+  bool found = false;
+  GemmPlan gp = plan_gemm_f(M, N, K, sms, allow_split, cs_ok, g_gemm_force, &found);
+  if (!found) gp = plan_gemm_f(M, N, K, sms, allow_split, cs_ok, 0, &found);  // forced plan not applicable
+  return gp;
 }
 
 // Output map for the TMA-store epilogue: 2-D [rows][cols] (or 3-D
@@ -1315,9 +1466,64 @@ void run_tc(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUt
     attr = true;
   }
   const int mt = int((M + 127) / 128), nt = int((N + BN - 1) / BN);
-  KB_CUDA(launch_pdl(kern, dim3(gp.grid), dim3(192), smem, s, ta, tb, tcm, int(M), int(N), int(K), mt, nt,
-                     gp.splits, gp.kb_per, e, partial, gp.grid, gp.sk_T));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gp.grid);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (gp.cs > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = unsigned(gp.cs);
+    at[na].val.clusterDim.y = 1;
+    at[na++].val.clusterDim.z = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = unsigned(na);
+  KB_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, int(M), int(N), int(K), mt, nt, gp.splits, gp.kb_per, e,
+                             partial, gp.grid, gp.sk_T, gp.cs));
   KB_LAUNCH();
+}
+
+template <int BN, int STAGES>
+int max_clusters_of(int cs) {
+  const size_t smem = 1024 + size_t(STAGES) * (128 * 64 * 2 + BN * 64 * 2) + kEpiSmem +
+                      8 * (2 * STAGES + 4) + 16;
+  auto kern = k_gemm_tc<BN, STAGES, EK_F32>;
+  KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(cs));
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(cs);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+int max_clusters(int bn, int cs) {
+  static std::mutex mu;
+  static std::unordered_map<int, int> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  const int key = bn * 16 + cs;
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  const int n = bn == 256 ? max_clusters_of<256, 4>(cs) : max_clusters_of<128, 6>(cs);
+  memo[key] = n;
+  return n;
 }
 
 template <int STAGES, int KSUB, int KIND>
@@ -1415,7 +1621,9 @@ void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, co
     }();
     int sms = c.sm_count > 0 ? c.sm_count : 148;
     if (new_sms > 0 && new_sms < sms) sms = (s == c.s_new) ? new_sms : sms - new_sms;
-    const GemmPlan gp = plan_gemm(M, N, K, sms, true);
+    // the SwiGLU epilogue packs 128 accumulator columns per store: not split
+    // over a cluster's ranks
+    const GemmPlan gp = plan_gemm(M, N, K, sms, true, e.kind != Epi::SWIGLU && new_sms == 0);
     float* part = nullptr;
     if (gp.splits > 1 || gp.sk_T > 0) {
       DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;

@@ -764,13 +764,15 @@ def test_fused_recompute_matches_separate_stream(K, oracle, dtype, monkeypatch):
         assert rel_fro(lf, want) < 3e-2 and rel_fro(lf, ls) < 2e-2
 
 
-@pytest.mark.parametrize("force", [0, 5, 6])
+@pytest.mark.parametrize("force,sp", [(0, 0), (5, 0), (6, 0), (11, 2), (11, 4), (12, 2), (12, 3), (12, 4)])
 @pytest.mark.parametrize("M,N,Kd", [(128, 4096, 4096), (77, 1536, 14336), (1, 6144, 4096), (128, 28672 // 8, 4096)])
-def test_gemm_stream_k_epilogues(K, force, M, N, Kd):
+def test_gemm_stream_k_epilogues(K, force, sp, M, N, Kd):
     """Weight-streaming shapes (M <= 128) through the stream-K schedule
     (every CTA streams T / G weight blocks, tiles split into pieces reduced in
-    fixed order) vs the auto plan, for the F32 / tanh / SwiGLU / residual
-    epilogues; deterministic across calls."""
+    fixed order; force 5 / 6) and the cluster split-K (cs CTAs per tile, fp32
+    partials reduced over DSMEM inside the GEMM; force 11, cs = sp) vs the
+    auto plan, for the F32 / tanh / SwiGLU / residual epilogues;
+    deterministic across calls."""
     from paper_2507_08045_b200.native import _p, lib
     import ctypes as C
     cfg = K.ModelConfig(n_layers=2, n_heads=1, head_dim=8, d_model=8, vocab_size=4,
@@ -782,7 +784,7 @@ def test_gemm_stream_k_epilogues(K, force, M, N, Kd):
     bias = rng.uniform(-.5, .5, N).astype(np.float32)
     acc = A.astype(np.float64) @ B.astype(np.float64).T
     tol = 5e-2
-    assert lib().krul_debug_set_gemm_plan(force, 0) == 0
+    assert lib().krul_debug_set_gemm_plan(force, sp) == 0
     try:
         outs = []
         for _ in range(2):
@@ -889,8 +891,8 @@ def test_calibrate_rc_measured_contract(K, oracle):
     assert K.calibrate_rc(cm, cfg.n_layers, L, cfg.d_model, pairs) in list(K.default_rc_grid())
 
 
-@pytest.mark.parametrize("r_c", [0.0, 0.25])
-def test_llama_width_restore_matches_oracle(K, oracle, r_c):
+@pytest.mark.parametrize("r_c,gemm_force", [(0.0, 0), (0.25, 0), (0.0, 11), (0.0, 12)])
+def test_llama_width_restore_matches_oracle(K, oracle, r_c, gemm_force):
     """Production shape against the CPU oracle (not the repo's own SIMT
     path): 2 layers at full Llama-3-8B width (d=4096, GQA 32/8, hd=128,
     SwiGLU F=14336, rope theta 5e5), bf16 tcgen05 kernels throughout --
@@ -900,7 +902,19 @@ def test_llama_width_restore_matches_oracle(K, oracle, r_c):
     (weight-streaming GEMMs + FA attention), then a decode step (split-key
     decode attention). Restored K/V, new-input logits, decode logits and the
     decode attention rows vs the oracle's f32 prefill / decode on the same
-    weights: relative Frobenius <= 2e-2 (bf16 tolerance)."""
+    weights: relative Frobenius <= 2e-2 (bf16 tolerance).
+    gemm_force 11: every weight-streaming GEMM with a non-SwiGLU epilogue
+    (the fused RoPE / page-scatter QKV, O and FFN2 residual epilogues) runs
+    as cluster split-K with the DSMEM reduce."""
+    from paper_2507_08045_b200.native import lib
+    assert lib().krul_debug_set_gemm_plan(gemm_force, 0) == 0
+    try:
+        _llama_width_restore(K, oracle, r_c)
+    finally:
+        lib().krul_debug_set_gemm_plan(0, 0)
+
+
+def _llama_width_restore(K, oracle, r_c):
     shape = dict(n_layers=2, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, vocab_size=512,
                  ffn_mult=3.5, ffn_kind=1, rope_theta=500000.0, seed=21)
     om = oracle.Model(oracle.ModelConfig(**shape))
