@@ -405,6 +405,8 @@ int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t row
 /* Pin the GEMM plan of later calls (tests): force 0 auto, 1/2 1-SM 256/128
  * wide, 3 CTA pair, 5/6 stream-K 256/128 wide; splits 0 = auto. */
 int krul_debug_set_gemm_plan(int force, int splits);
+int krul_debug_gemm_timeline(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force, int splits,
+                             unsigned long long* ts_out);
 int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
                           int splits, int iters, float* ms_per_iter);
 int krul_debug_gemm(krul_ctx* ctx, int64_t M, int64_t N, int64_t K,

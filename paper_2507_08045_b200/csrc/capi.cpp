@@ -1161,6 +1161,62 @@ int krul_debug_set_gemm_plan(int force, int splits) {
     g_gemm_splits = splits;
   });
 }
+// Phase timeline of one weight-streaming GEMM launch (globaltimer ns, see
+// g_gemm_ts in gemm.cu): ts[0..9] CTA 0 phases, ts[32 + b] / ts[288 + b]
+// entry / exit of CTA b (b < 256). The weights are streamed from HBM.
+int krul_debug_gemm_timeline(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force, int splits,
+                             unsigned long long* ts_out /* [544] */) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t s = c.s_comp;
+    DevBuf a, b, out, res, out2, ts, flush;
+    void* da = a.ensure(size_t(std::max<int64_t>(M, 128) * K) * 2);
+    void* db = b.ensure(size_t(N * K) * 2);
+    launch_init_uniform(c, s, da, std::max<int64_t>(M, 128) * K, 1, 1, 1.0f);
+    launch_init_uniform(c, s, db, N * K, 1, 2, 0.02f);
+    Epi e;
+    e.kind = epi;
+    e.a_rows = std::max<int64_t>(M, 128);
+    e.out = out.ensure(size_t(M * N) * 4 + 16);
+    e.ldo = epi == Epi::SWIGLU ? N / 2 : N;
+    if (epi == Epi::RESID) {
+      e.resid = static_cast<float*>(res.ensure(size_t(M * N) * 4));
+      KB_CUDA(cudaMemsetAsync(const_cast<float*>(e.resid), 0, size_t(M * N) * 4, s));
+      e.ldr = N;
+      e.out2 = out2.ensure(size_t(M * N) * 2);
+      e.ldo2 = N;
+    }
+    unsigned long long* dts = static_cast<unsigned long long*>(ts.ensure(544 * 8));
+    KB_CUDA(cudaMemsetAsync(dts, 0, 544 * 8, s));
+    g_gemm_force = force;
+    g_gemm_splits = splits;
+    try {
+      gemm(c, s, M, N, K, da, K, db, K, e);  // warm (plan, maps)
+      void* fl = flush.ensure(size_t(256) << 20);  // evict the weights from L2
+      KB_CUDA(cudaMemsetAsync(fl, 1, size_t(256) << 20, s));
+      // the activations / residual were just written by the producing kernel
+      // in the layer chain: L2-resident, as there
+      launch_init_uniform(c, s, da, std::max<int64_t>(M, 128) * K, 1, 1, 1.0f);
+      if (epi == Epi::RESID) KB_CUDA(cudaMemsetAsync(const_cast<float*>(e.resid), 0, size_t(M * N) * 4, s));
+      KB_CUDA(cudaStreamSynchronize(s));
+      gemm_set_timeline(dts);
+      gemm(c, s, M, N, K, da, K, db, K, e);
+      KB_CUDA(cudaStreamSynchronize(s));
+      gemm_set_timeline(nullptr);
+    } catch (...) {
+      g_gemm_force = 0;
+      g_gemm_splits = 0;
+      gemm_set_timeline(nullptr);
+      throw;
+    }
+    g_gemm_force = 0;
+    g_gemm_splits = 0;
+    KB_CUDA(cudaMemcpy(ts_out, dts, 544 * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
 int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int epi, int force,
                           int splits, int iters, float* ms_per_iter) {
   return guard([&] {
@@ -1199,11 +1255,23 @@ int krul_debug_gemm_bench(krul_ctx* ctx, int64_t M, int64_t N, int64_t K, int ep
     g_gemm_splits = splits;
     try {
       for (int i = 0; i < 2; ++i) gemm(c, s, M, N, K, da, K, db0 + wbytes * (i % nb), K, e);
+      KB_CUDA(cudaStreamSynchronize(s));
+      // the launches are captured into a graph and replayed (as in the restore
+      // DAG): device time, not the host's per-launch cost
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t exec = nullptr;
+      KB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+      for (int i = 0; i < iters; ++i) gemm(c, s, M, N, K, da, K, db0 + wbytes * (i % nb), K, e);
+      KB_CUDA(cudaStreamEndCapture(s, &graph));
+      KB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      KB_CUDA(cudaGraphLaunch(exec, s));  // warm
       cudaEvent_t e0 = c.event(), e1 = c.event();
       KB_CUDA(cudaEventRecord(e0, s));
-      for (int i = 0; i < iters; ++i) gemm(c, s, M, N, K, da, K, db0 + wbytes * (i % nb), K, e);
+      KB_CUDA(cudaGraphLaunch(exec, s));
       KB_CUDA(cudaEventRecord(e1, s));
       KB_CUDA(cudaEventSynchronize(e1));
+      cudaGraphExecDestroy(exec);
+      cudaGraphDestroy(graph);
       float ms = 0;
       KB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       *ms_per_iter = ms / float(iters);

@@ -22,6 +22,17 @@
 namespace kb {
 
 int g_gemm_force = 0;   // debug: 0 auto, 1 1-SM BN256, 2 1-SM BN128, 3 pair, 4 pair BK128
+
+// Debug timeline of the 1-SM GEMM (krul_debug_gemm_timeline): when set,
+// %globaltimer stamps of CTA 0's phases plus every CTA's entry / exit.
+__device__ unsigned long long* g_gemm_ts = nullptr;
+__device__ __forceinline__ void gemm_ts(int slot) {
+  if (g_gemm_ts) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_ts[slot] = t;
+  }
+}
 int g_gemm_splits = 0;  // debug: force the split-K count (0 = planner)
 
 // ---------------------------------------------------------------- epilogue
@@ -206,50 +217,51 @@ __device__ __forceinline__ void epi_elem(const Epi& e, int64_t r, int64_t c, flo
       break;
   }
 }
-__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + expf(-g)) * u; }
+// silu(g) * u for the bf16 epilogues: MUFU exp2 + fast reciprocal (relative
+// error ~1e-6, far below the bf16 output rounding). The accurate expf + IEEE
+// division made the SwiGLU epilogue of a 128 x 256 tile ~8 us (measured with
+// krul_debug_gemm_timeline): compute-bound on the 4 epilogue warps.
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 // Where the epilogue's accumulator values come from. Default: this CTA's TMEM.
 // Cluster split-K (cs > 1): the cs CTAs of a thread-block cluster computed
-// the same tile over disjoint k ranges and stashed their fp32 accumulators in
-// their own (drained) operand rings, laid out [chunk][warp][column][lane];
-// the CTA of rank r owns the chunks with (chunk / unit) % cs == r and sums
-// them over the cluster's ranks through distributed shared memory, in rank
-// order (deterministic). A reduce-scatter inside the GEMM: no fp32 partials
-// in global memory, no reduce kernel.
+// the same tile over disjoint k ranges. Each 32-column chunk has an owner
+// rank ((chunk / unit) % cs); every CTA writes the chunks it does not own
+// to a global (L2-resident) exchange buffer, one cluster barrier, then each
+// owner adds the other ranks' partials to its own (still in TMEM) in rank
+// order (deterministic) and runs the epilogue on its chunks: a reduce-scatter
+// inside the GEMM, no reduce kernel. (The same exchange through DSMEM loads
+// measured 2-3x slower: ~10-16 B/ns per SM of remote shared-memory reads.)
+// Exchange layout: [tile][chunk][src rank][warp][column j][lane] floats, so
+// every store / load is a coalesced 128-byte warp access.
 struct AccSrc {
   int cs = 1, rank = 0, q = 0;
-  uint32_t red = 0;  // shared::cta address of this CTA's stash
+  const float* xw = nullptr;  // exchange buffer of this tile
+  int nchunks = 0;            // 32-column chunks per tile
   __device__ __forceinline__ bool owns(int col, int unit) const { return cs <= 1 || (col / unit) % cs == rank; }
 };
-__device__ __forceinline__ uint32_t dsmem_map(uint32_t sa, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sa), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float dsmem_ld(uint32_t a) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
-  return v;
-}
-// stash offset (bytes) of column crel + j, this warp, this lane
-__device__ __forceinline__ uint32_t red_off(int crel, int q, int j, int lane) {
-  return uint32_t((((crel >> 5) * 4 + q) * 32 + j) * 32 + lane) * 4u;
+__device__ __forceinline__ int64_t xw_off(int chunk, int src, int cs, int q) {
+  return ((int64_t(chunk) * cs + src) * 4 + q) * 1024;
 }
 __device__ __forceinline__ void acc_ld32(const AccSrc& src, uint32_t taddr, int crel, float* v) {
-  if (src.cs <= 1) {
-    tc::tmem_ld32(taddr, v);
-    return;
-  }
+  tc::tmem_ld32(taddr, v);
+  if (src.cs <= 1) return;
   const int lane = threadIdx.x & 31;
+  float own[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = 0.f;
-  for (int r = 0; r < src.cs; ++r) {
-    const uint32_t b = dsmem_map(src.red + red_off(crel, src.q, 0, lane), r);
-    float t[32];
+  for (int j = 0; j < 32; ++j) {
+    own[j] = v[j];
+    v[j] = 0.f;
+  }
+  // rank order (deterministic); unrolled over the (<= 4) ranks so the
+  // compiler can issue later ranks' loads ahead of earlier ranks' adds
 #pragma unroll
-    for (int j = 0; j < 32; ++j) t[j] = dsmem_ld(b + uint32_t(j) * 128u);
+  for (int r = 0; r < 4; ++r) {
+    if (r >= src.cs) break;
+    const float* p = src.xw + xw_off(crel >> 5, r, src.cs, src.q) + lane;
+    const bool mine = r == src.rank;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] += t[j];
+    for (int j = 0; j < 32; ++j) v[j] += mine ? own[j] : __ldcg(p + 32 * j);
   }
 }
 
@@ -631,10 +643,14 @@ template <int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int mt, int nt, int splits, int kb_per, Epi e,
-              float* __restrict__ partial, int sk_G, long long sk_T, int cs) {
+              float* __restrict__ partial, int sk_G, long long sk_T, int cs, float* __restrict__ xw) {
   constexpr int BM = 128, BK = 64;
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
   extern __shared__ unsigned char smem_raw[];
+  if (threadIdx.x == 0) {
+    gemm_ts(32 + blockIdx.x);
+    if (blockIdx.x == 0) gemm_ts(0);
+  }
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = base;
@@ -672,6 +688,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0 && blockIdx.x == 0) gemm_ts(1);
   pdl_trigger();  // the next kernel in the stream may start its prologue
 
   if (warp == 0) {
@@ -725,6 +742,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = k0; kb < k1; ++kb) {
           tc::mbar_wait(&full[s], ph);
           tc::fence_after();
+          if (blockIdx.x == 0 && i == 0 && kb == k0) gemm_ts(2);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t da = tc::sw128_desc(sA + s * A_BYTES + k * 32);
@@ -738,6 +756,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
         tc::mma_commit(&tfull[acc]);
+        if (blockIdx.x == 0 && i == 0) gemm_ts(3);
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
@@ -757,16 +776,20 @@ __global__ void __launch_bounds__(192, 1)
       const int m = un.m, n = un.n, ks = un.ks;
       tc::mbar_wait(&tfull[acc], aph);
       tc::fence_after();
+      if (blockIdx.x == 0 && warp == 2 && lane == 0 && i == 0) gemm_ts(4);
       const int64_t row0 = int64_t(m) * BM + 32 * q;
       float* P = partial ? partial + int64_t(ks) * M * N : nullptr;
-      if (cs > 1) {  // stash the partial tile in the drained ring; reduced below
-        float* red = reinterpret_cast<float*>(base);
+      if (cs > 1) {  // hand the chunks other ranks own to the exchange buffer; reduced below
+        const int unit = (KIND == EK_CDT || KIND == EK_TANH) ? 64 : 32;
+        float* tile = xw + int64_t(n) * (BN / 32) * cs * 4096;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
+          if ((c / unit) % cs == ks) continue;
           float v[32];
           tc::tmem_ld32(tmem + (uint32_t(32 * q) << 16) + uint32_t(acc * BN + c), v);
+          float* dst = tile + xw_off(c >> 5, ks, cs, q) + lane;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) red[red_off(c, q, j, lane) / 4] = v[j];
+          for (int j = 0; j < 32; ++j) __stcg(dst + 32 * j, v[j]);
         }
       } else if constexpr (KIND == EK_GENERIC) {
 #pragma unroll 1
@@ -791,8 +814,10 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   if (cs > 1) {
-    // every stash of the cluster is written -> reduce-scatter over DSMEM
+    if (blockIdx.x == 0 && warp == 2 && lane == 0) gemm_ts(5);
+    // every rank's exchange writes are done (cluster-scope release/acquire)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (blockIdx.x == 0 && warp == 2 && lane == 0) gemm_ts(6);
     if (warp >= 2) {
       Unit un;
       unit_at(0, mt, nt, splits, kb_per, num_k, sk_G, sk_T, un, cs);
@@ -800,28 +825,30 @@ __global__ void __launch_bounds__(192, 1)
       src.cs = cs;
       src.rank = un.ks;
       src.q = warp & 3;
-      src.red = tc::smem_u32(base);
+      src.xw = xw + int64_t(un.n) * (BN / 32) * cs * 4096;
       const int q = warp & 3;
       float* my = stg + q * 32 * 33;
       unsigned char* stage = reinterpret_cast<unsigned char*>(stg) + q * 8192;
       int sbuf = 0;
       const int64_t row0 = 32 * q;
+      const uint32_t tacc = tmem + (uint32_t(32 * q) << 16);  // single unit: accumulator 0
       if constexpr (KIND == EK_GENERIC) {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           if (int64_t(un.n) * BN + c >= N) break;
-          if (src.owns(c, 32)) epi_block(e, my, 0u, row0, int64_t(un.n) * BN + c, M, N, nullptr, src, c);
+          if (src.owns(c, 32)) epi_block(e, my, tacc + uint32_t(c), row0, int64_t(un.n) * BN + c, M, N, nullptr, src, c);
         }
       } else if constexpr (KIND == EK_QKV) {
-        epi_qkv<BN>(e, 0u, row0, int64_t(un.n) * BN, M, N, src);
+        epi_qkv<BN>(e, tacc, row0, int64_t(un.n) * BN, M, N, src);
       } else {
-        epi_unit<KIND, BN>(e, &tmC, stage, sbuf, 0u, row0, int64_t(un.n) * BN, M, N, 0, src);
+        epi_unit<KIND, BN>(e, &tmC, stage, sbuf, tacc, row0, int64_t(un.n) * BN, M, N, 0, src);
       }
     }
-    // the peers have read this CTA's stash
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (blockIdx.x == 0 && warp == 2 && lane == 0) gemm_ts(7);
   }
+  if (blockIdx.x == 0 && warp == 2 && lane == 0) gemm_ts(8);
   if (warp >= 2 && lane == 0) tc::bulk_wait_all();
+  if (blockIdx.x == 0 && warp == 2 && lane == 0) gemm_ts(9);
   tc::fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -829,6 +856,7 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(uint32_t(2 * BN)));
   }
+  if (threadIdx.x == 0) gemm_ts(32 + 256 + blockIdx.x);
 }
 
 // ---------------------------------------------------------------- 2-SM pair
@@ -1456,7 +1484,7 @@ constexpr size_t kEpiSmem = 4 * 2 * 4096;  // staging tiles of the 4 epilogue wa
 
 template <int BN, int STAGES, int KIND>
 void run_tc(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& tb,
-            const CUtensorMap& tcm, int64_t M, int64_t N, int64_t K, const Epi& e, float* partial) {
+            const CUtensorMap& tcm, int64_t M, int64_t N, int64_t K, const Epi& e, float* partial, float* xw) {
   const size_t smem = 1024 + size_t(STAGES) * (128 * 64 * 2 + BN * 64 * 2) + kEpiSmem +
                       8 * (2 * STAGES + 4) + 16;
   auto kern = k_gemm_tc<BN, STAGES, KIND>;
@@ -1486,7 +1514,7 @@ void run_tc(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUt
   cfg.attrs = at;
   cfg.numAttrs = unsigned(na);
   KB_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, int(M), int(N), int(K), mt, nt, gp.splits, gp.kb_per, e,
-                             partial, gp.grid, gp.sk_T, gp.cs));
+                             partial, gp.grid, gp.sk_T, gp.cs, xw));
   KB_LAUNCH();
 }
 
@@ -1528,7 +1556,7 @@ int max_clusters(int bn, int cs) {
 
 template <int STAGES, int KSUB, int KIND>
 void run_tc2(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CUtensorMap& tb,
-             const CUtensorMap& tcm, int64_t M, int64_t N, int64_t K, const Epi& e, float* partial) {
+             const CUtensorMap& tcm, int64_t M, int64_t N, int64_t K, const Epi& e, float* partial, float*) {
   const size_t smem = 1024 + size_t(STAGES) * KSUB * (2 * 128 * 64 * 2) + kEpiSmem +
                       8 * (2 * STAGES + 4) + 16;
   auto kern = k_gemm_tc2<STAGES, KSUB, KIND>;
@@ -1559,14 +1587,14 @@ void run_tc2(const GemmPlan& gp, cudaStream_t s, const CUtensorMap& ta, const CU
 
 void launch_gemm_tc(const GemmPlan& gp, cudaStream_t s, int64_t M, int64_t N, int64_t K,
                     const void* A, int64_t lda, const void* B, int64_t ldb, const Epi& e,
-                    float* partial) {
+                    float* partial, float* xw) {
   const int64_t a_rows = gp.pair ? M : std::max<int64_t>(M, std::min<int64_t>(e.a_rows, 128));
   const CUtensorMap ta = make_map(A, a_rows, K, lda, 128);
   const CUtensorMap tb = make_map(B, N, K, ldb, gp.pair ? 128 : gp.bn);
   CUtensorMap tcm;
   int kind = EK_GENERIC;
   if (!make_out_map(&tcm, e, M, N, gp.splits, partial, &kind)) kind = EK_GENERIC;
-#define ARGS gp, s, ta, tb, tcm, M, N, K, e, partial
+#define ARGS gp, s, ta, tb, tcm, M, N, K, e, partial, xw
   if (gp.pair && g_gemm_force == 4) {
     KB_EPI_DISPATCH(run_tc2, 3, 2)
   } else if (gp.pair) {
@@ -1587,6 +1615,8 @@ int gemm_mode() {  // 0 auto, 1 force SIMT
   return m;
 }
 }  // namespace
+
+void gemm_set_timeline(unsigned long long* d) { KB_CUDA(cudaMemcpyToSymbol(g_gemm_ts, &d, sizeof d)); }
 
 bool gemm_uses_tc(const Ctx& c, const void* A, int64_t lda, const void* B, int64_t ldb) {
   return c.cfg.dtype == KRUL_BF16 && gemm_mode() == 0 && lda % 8 == 0 && ldb % 8 == 0 &&
@@ -1625,11 +1655,16 @@ void gemm_impl(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, co
     // over a cluster's ranks
     const GemmPlan gp = plan_gemm(M, N, K, sms, true, e.kind != Epi::SWIGLU && new_sms == 0);
     float* part = nullptr;
+    float* xw = nullptr;
     if (gp.splits > 1 || gp.sk_T > 0) {
       DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;
       part = static_cast<float*>(buf.ensure(size_t(M) * size_t(N) * gp.splits * 4));
+    } else if (gp.cs > 1) {  // cluster split-K exchange: [tile][chunk][rank][128 rows][32 cols]
+      DevBuf& buf = s == c.s_new ? c.ws2_gpart : c.ws_gpart;
+      const int64_t nt = (N + gp.bn - 1) / gp.bn;
+      xw = static_cast<float*>(buf.ensure(size_t(nt) * (gp.bn / 32) * gp.cs * 4096 * 4));
     }
-    launch_gemm_tc(gp, s, M, N, K, A, lda, B, ldb, e, part);
+    launch_gemm_tc(gp, s, M, N, K, A, lda, B, ldb, e, part, xw);
     SkInfo sk;
     if (gp.sk_T > 0) {
       sk.G = gp.grid;

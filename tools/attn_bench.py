@@ -25,7 +25,7 @@ def main():
     for rows, pos0, name in ((128, 8192, "new-prefill 128x8320"), (1024, 0, "recompute 1024 causal")):
         vis = rows * pos0 + rows * (rows + 1) / 2
         fl = 4 * 128 * 32 * vis
-        for dbg in (0,):
+        for dbg in [int(x) for x in os.environ.get("DBG", "0").split(",")]:
             for target in (0, 8, 16, 32):
                 ms = C.c_float()
                 rc = lib.krul_debug_attn_bench(ctx.h, conv.h, 0, C.c_int64(rows), C.c_int64(pos0),
