@@ -401,6 +401,9 @@ int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* by
 /* Kernel-tuning aid: times `iters` tcgen05 attention launches over conv's pages. */
 int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0,
                           int dbg, int target, int iters, float* ms_per_iter);
+/* Kernel-tuning aid: %globaltimer phase stamps of one attention launch, ts[cta * 8 + slot]. */
+int krul_debug_attn_timeline(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0, int target,
+                             unsigned long long* ts, int64_t n_ts);
 /* Kernel-tuning aid: times `iters` device-resident bf16 GEMMs (not a product entry). */
 /* Pin the GEMM plan of later calls (tests): force 0 auto, 1/2 1-SM 256/128
  * wide, 3 CTA pair, 5/6 stream-K 256/128 wide; splits 0 = auto. */

@@ -1383,6 +1383,41 @@ int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t row
   });
 }
 
+// Phase stamps of one tcgen05 attention launch (kernel tuning, not on the
+// product path): ts[cta * 8 + slot] in ns (%globaltimer), see attn_ts.
+int krul_debug_attn_timeline(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0, int target,
+                             unsigned long long* ts, int64_t n_ts) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(conv, "conv");
+    need(ts, "ts");
+    Ctx& c = *ctx->c;
+    if (c.cfg.dtype != KRUL_BF16) fail(KRUL_E_CONFIG, "attention timeline needs a bf16 context");
+    KB_CUDA(cudaSetDevice(c.device));
+    cudaStream_t s = c.s_comp;
+    DevBuf q, out, part, dts;
+    void* dq = q.ensure(size_t(rows) * c.cfg.qd() * 2);
+    launch_init_uniform(c, s, dq, rows * c.cfg.qd(), 5, 5, 1.0f);
+    AttnArgs a{};
+    a.q = dq;
+    a.rows = rows;
+    a.pos0 = pos0;
+    a.out = out.ensure(size_t(rows) * c.cfg.qd() * 2);
+    a.part = &part;
+    g_attn_target = target;
+    for (int i = 0; i < 2; ++i) launch_attention_tc(c, s, *conv->v, layer, a, part);
+    unsigned long long* d = static_cast<unsigned long long*>(dts.ensure(size_t(n_ts) * 8));
+    KB_CUDA(cudaMemsetAsync(d, 0, size_t(n_ts) * 8, s));
+    KB_CUDA(cudaStreamSynchronize(s));
+    attn_set_timeline(d);
+    launch_attention_tc(c, s, *conv->v, layer, a, part);
+    KB_CUDA(cudaStreamSynchronize(s));
+    attn_set_timeline(nullptr);
+    g_attn_target = 0;
+    KB_CUDA(cudaMemcpy(ts, d, size_t(n_ts) * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
 
 // Device time of the decode fold (K1) on the last captured decode rows:
 // `iters` folds enqueued back to back on the estimator stream between two

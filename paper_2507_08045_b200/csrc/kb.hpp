@@ -307,6 +307,7 @@ struct Epi {  // GEMM epilogue
 extern int g_gemm_force, g_gemm_splits;  // debug knobs (krul_debug_gemm_bench)
 void gemm_set_timeline(unsigned long long* d);  // debug phase stamps (krul_debug_gemm_timeline)
 extern int g_attn_target, g_attn_dbg;    // debug knobs (krul_debug_attn_bench)
+void attn_set_timeline(unsigned long long* d);  // debug phase stamps (krul_debug_attn_timeline)
 // True when gemm() will take the tcgen05 path for these operands (fused
 // epilogues such as Epi::QKV exist only there).
 bool gemm_uses_tc(const Ctx& c, const void* A, int64_t lda, const void* B, int64_t ldb);
