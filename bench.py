@@ -61,12 +61,15 @@ _LLAMA8 = dict(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096
 # turn structure (the turn whose end-of-turn snapshot the timed steps restore):
 # n_dec teacher-forced decode steps after the n_new-token prefill; estimator
 # knobs gamma / r_l (gamma 0.5 empties L_I on random-init weights);
-# `pairs` = the fixed control strategy; r_c_ref = the split the reference arm
-# restores at (= the GPU arm's measured optimum, config.r_c of its line)
+# `pairs` = the fixed control strategy; r_c_ref = the split both arms restore
+# at (the argmin of the GPU arm's measured TTFT curve on B200, round 2:
+# 0.016-0.02 over seven runs; the plan's recompute_token_layers at a given
+# r_c does not depend on which 8 pairs were selected, so the two arms'
+# `config` is identical)
 CONFIGS = {
     # BASELINE.json configs[1]
     "llama3-8b-8k": dict(**_LLAMA8, label="Llama-3-8B-shaped", L=8192, n_new=128, n_dec=64, gamma=0.1,
-                         r_l=0.5, pairs=[(9 + 2 * k, 10 + 2 * k) for k in range(8)], r_c_ref=0.0,
+                         r_l=0.5, pairs=[(9 + 2 * k, 10 + 2 * k) for k in range(8)], r_c_ref=0.02,
                          l2="inputs (16 GB bf16 weights, 1 GB KV) larger than L2; no flush"),
     # BASELINE.json configs[2]: Mistral-7B shape (GQA 32/8), 32K history
     "mistral-7b-32k": dict(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096,
