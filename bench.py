@@ -462,6 +462,8 @@ def run_b200(args, rank, local, world, dist):
                       "achieved_serialised": rate(kti[name], bound),
                       "frac_of_roofline": round(ideal[name] / ms_, 4) if ms_ else None}
     dominant = max(roof, key=lambda k: roof[k]["ms_per_step"])
+    if "gemm_stream" in roof and rank == 0:
+        roof["gemm_stream"]["isolated"] = gemm_stream_isolated(K, ctx, cfg, n_new, peak_b)
     head = dict(roof[dominant])
     tr = NCU_TRAFFIC.get(dominant)
     head.update({"class": dominant,
@@ -541,6 +543,36 @@ def run_b200(args, rank, local, world, dist):
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(args, spec, r_c, budget_s=args.cpu_budget)
     return out
+
+
+def gemm_stream_isolated(K, ctx, cfg, rows, peak_b, iters=20):
+    """The new-input prefill's four weight-streaming GEMM shapes of one layer
+    (QKV, O, FFN up, FFN down at M = rows) timed alone: graph-replayed launches
+    with the planner's choice, weights rotated over >= 320 MB so every launch
+    streams them from HBM (krul_debug_gemm_bench). The QKV shape runs the F32
+    epilogue (the RoPE / page-scatter epilogue needs a conversation). Explains
+    the in-DAG figure: there the launches share the SMs with the blob decode +
+    expand and the recompute."""
+    import ctypes as C
+    d, H, Hkv, hd, F = cfg.d_model, cfg.n_heads, cfg.kv_heads(), cfg.head_dim, cfg.ffn_hidden()
+    swiglu = cfg.ffn_kind == 1
+    shapes = {"qkv": ((H + 2 * Hkv) * hd, d, 0), "o": (d, H * hd, 2),
+              "ffn_up": ((2 if swiglu else 1) * F, d, 4 if swiglu else 3), "ffn_down": (d, F, 2)}
+    out, tot_b, tot_us = {}, 0.0, 0.0
+    for name, (N, Kd, epi) in shapes.items():
+        ms = C.c_float(0)
+        rc = K.lib().krul_debug_gemm_bench(ctx.h, C.c_int64(rows), C.c_int64(N), C.c_int64(Kd), epi, 0, 0, iters,
+                                           C.byref(ms))
+        if rc != 0:
+            return {"error": f"krul_debug_gemm_bench rc={rc}"}
+        by = N * Kd * 2 + rows * Kd * 2 + rows * N * 4
+        us = ms.value * 1e3
+        out[name] = {"N": N, "K": Kd, "us": round(us, 2), "GB/s": round(by / (us * 1e-6) / 1e9, 1)}
+        tot_b += by
+        tot_us += us
+    a = tot_b / (tot_us * 1e-6) / 1e9
+    return {"shapes": out, "achieved": round(a, 1), "frac": round(a / peak_b, 4), "us_per_layer": round(tot_us, 2),
+            "note": "one layer's four GEMMs alone (graph replay, HBM-streamed weights), same bytes formula"}
 
 
 def bubble_leg(K, ctx, prev, conv, cfg, hist, new, L, pairs, calib, reps=7):
