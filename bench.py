@@ -463,7 +463,10 @@ def run_b200(args, rank, local, world, dist):
                       "frac_of_roofline": round(ideal[name] / ms_, 4) if ms_ else None}
     dominant = max(roof, key=lambda k: roof[k]["ms_per_step"])
     if "gemm_stream" in roof and rank == 0:
-        roof["gemm_stream"]["isolated"] = gemm_stream_isolated(K, ctx, cfg, n_new, peak_b)
+        try:  # diagnostic only: never let it cost the bench line
+            roof["gemm_stream"]["isolated"] = gemm_stream_isolated(K, ctx, cfg, n_new, peak_b)
+        except Exception as ex:  # noqa: BLE001
+            roof["gemm_stream"]["isolated"] = {"error": repr(ex)[:200]}
     head = dict(roof[dominant])
     tr = NCU_TRAFFIC.get(dominant)
     head.update({"class": dominant,
@@ -482,8 +485,12 @@ def run_b200(args, rank, local, world, dist):
     pol = policies_leg(K, ctx, prev, conv, cfg, hist, new, L, r_c, pairs, spec) if (
         rank == 0 and not args.no_policies) else None
     est = estimator_leg(K, ctx, conv, cfg, spec) if rank == 0 else None
-    bub = bubble_leg(K, ctx, prev, conv, cfg, hist, new, L, pairs, calib) if (
-        rank == 0 and calib.get("r_c_balanced_restore") is not None) else None
+    bub = None
+    if rank == 0 and calib.get("r_c_balanced_restore") is not None:
+        try:  # diagnostic leg: never let it cost the bench line
+            bub = bubble_leg(K, ctx, prev, conv, cfg, hist, new, L, pairs, calib)
+        except Exception as ex:  # noqa: BLE001
+            bub = {"error": repr(ex)[:200]}
     ctr = container_leg(K, ctx, snap) if rank == 0 and not spec.get("f32") else None
     out = {
         "metric": METRIC,
@@ -554,7 +561,7 @@ def gemm_stream_isolated(K, ctx, cfg, rows, peak_b, iters=20):
     the in-DAG figure: there the launches share the SMs with the blob decode +
     expand and the recompute."""
     import ctypes as C
-    d, H, Hkv, hd, F = cfg.d_model, cfg.n_heads, cfg.kv_heads(), cfg.head_dim, cfg.ffn_hidden()
+    d, H, Hkv, hd, F = cfg.d_model, cfg.n_heads, cfg.kv_heads, cfg.head_dim, cfg.ffn_hidden()
     swiglu = cfg.ffn_kind == 1
     shapes = {"qkv": ((H + 2 * Hkv) * hd, d, 0), "o": (d, H * hd, 2),
               "ffn_up": ((2 if swiglu else 1) * F, d, 4 if swiglu else 3), "ffn_down": (d, F, 2)}
