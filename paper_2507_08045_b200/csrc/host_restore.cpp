@@ -232,8 +232,17 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     if (snap.coded && b.cbytes && g.hd == kEcLaneSyms && c.esz == 2 && fuse_env) {
       // decode straight into the owners' pages (one pass, one launch)
       const int64_t from[2] = {p[size_t(b.owners[0])], b.owners[1] >= 0 ? p[size_t(b.owners[1])] : L};
+      // blobs before the last one decode beside the new-input prefill: a
+      // smaller grid (KRUL_DEXP_CPS CTAs per SM) leaves the prefill's GEMMs
+      // their issue slots; the last blob is on the critical path and gets
+      // the whole GPU
+      static const int cps_env = [] {
+        const char* v = std::getenv("KRUL_DEXP_CPS");
+        return v ? std::atoi(v) : 4;
+      }();
+      const bool last = bi + 1 == snap.blobs.size();
       launch_ec_decode_expand(c, c.s_exp, cstg + b.coff, int64_t(b.ec_chunks), snap.lut_dev.as<uint16_t>(),
-                              b.start, L, conv, b.owners, from, double(b.cbytes));
+                              b.start, L, conv, b.owners, from, double(b.cbytes), last ? 4 : cps_env);
       for (int o : b.owners) {
         if (o < 0) continue;
         expand_bytes += 2.0 * double(L - p[size_t(o)]) * g.Hkv * g.hd * double(c.esz) * 2.0;

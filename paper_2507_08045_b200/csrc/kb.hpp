@@ -369,7 +369,7 @@ void launch_kv_scatter_f32(const Ctx& c, cudaStream_t s, const Conv& conv, int l
 // coded blob -> owners' pages in one pass (kvcode format, bf16, hd = 128)
 void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t n_chunks,
                              const uint16_t* lut, int64_t blob_start, int64_t L, const Conv& conv,
-                             const int* owners, const int64_t* from, double coded_bytes);
+                             const int* owners, const int64_t* from, double coded_bytes, int ctas_per_sm = 4);
 void launch_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t blob_start,
                    int64_t L, const Conv& conv, int layer, int64_t from);
 // Pages -> blob (compress, K8); mean-merge rows [merge_from, L) with `other`.

@@ -1103,14 +1103,15 @@ __global__ void __launch_bounds__(128, 4) k_ec_decode_expand(const uint8_t* __re
 }
 void launch_ec_decode_expand(const Ctx& c, cudaStream_t s, const void* blob, int64_t n_chunks,
                              const uint16_t* lut, int64_t blob_start, int64_t L, const Conv& conv,
-                             const int* owners, const int64_t* from, double coded_bytes) {
+                             const int* owners, const int64_t* from, double coded_bytes, int ctas_per_sm) {
   if (n_chunks <= 0) return;
   const int no = owners[1] >= 0 ? 2 : 1;
   const PageView pv0 = page_view(c, conv, owners[0]);
   const PageView pv1 = no > 1 ? page_view(c, conv, owners[1]) : pv0;
   // persistent: 4 CTAs (128 registers x 128 threads) per SM, two chunks per warp and pass
   const int sms = c.sm_count > 0 ? c.sm_count : 148;
-  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((n_chunks + 7) / 8, int64_t(sms) * 4)));
+  const int cps = std::max(1, std::min(4, ctas_per_sm));
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((n_chunks + 7) / 8, int64_t(sms) * cps)));
   cudaEvent_t kt0 = kt_begin(c, s);
   k_ec_decode_expand<<<blocks, 128, 0, s>>>(static_cast<const uint8_t*>(blob), lut, blob_start, L - blob_start,
                                             pv0, from[0], pv1, no > 1 ? from[1] : L, no);
