@@ -50,26 +50,6 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// blocking form: the thread is suspended in hardware until the phase
-// completes (or a time limit passes), so a long wait does not take issue
-// slots from the softmax warps sharing its SM sub-partition
-__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra D_%=;\n\t"
-      "bra W_%=;\n"
-      "D_%=:\n\t}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bar_wait_mode(uint64_t* b, uint32_t parity, int sleep) {
-  if (sleep)
-    bar_wait_sleep(b, parity);
-  else
-    bar_wait(b, parity);
-}
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* b, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -174,31 +154,10 @@ struct AttnTc {
   double* mass;    // [H][rows] region mass, may be null
   float* stats;    // [H][rows][2] (m, l) in the log2 domain, may be null
   int64_t il, rs;
-  int sleep;       // mbarrier waits: 0 = probe loops, 1 = suspending try_wait in producers / MMA, 2 = everywhere (KRUL_ATTN_SLEEP)
 };
 
-// Debug timeline (krul_debug_attn_timeline): %globaltimer stamps per CTA,
-// [cta][8] = entry, prologue done, Q in (MMA), MMA loop done, softmax done,
-// epilogue done, exit.
-__device__ unsigned long long* g_attn_ts = nullptr;
-__device__ __forceinline__ void attn_ts(int slot) {
-  if (g_attn_ts) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_attn_ts[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + slot] = t;
-  }
-}
-
-// per-block clock64 trace of CTA (0, 0): role (0/1 softmax A/B, 2 MMA,
-// 3 K producer, 4 V producer) x block (< 64) x 4 events, after the per-CTA stamps
-__device__ __forceinline__ void attn_tr(int role, int i, int ev) {
-  if (g_attn_ts && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) {
-    g_attn_ts[32768 + (role * 64 + i) * 4 + ev] = clock64();
-  }
-}
-
-constexpr int kAttnKB = 64;    // keys per block = one 64-token page
-constexpr int kPgCache = 192;  // key blocks whose page ids are cached in smem
+constexpr int kAttnKB = 128;  // keys per block = two 64-token pages
+constexpr int kPgCache = 96;  // key blocks whose page ids are cached in smem
 
 // number of key blocks q tile qt attends to, and its work-item count
 __host__ __device__ __forceinline__ int attn_nblk(const AttnTc& p, int qt) {
@@ -219,12 +178,11 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
-// Warp-converged issue: all 32 lanes of the MMA warp run the issue loop
-// (so descriptors and TMEM addresses stay in uniform registers) and
-// elect.sync picks the one lane that issues -- the single-lane form made the
-// compiler re-broadcast every operand through an elect loop per MMA, and
-// that issue overhead (with the softmax warps taking the sub-partition's
-// issue slots) exceeded the MMA's own execution time at N = 64.
+// Warp-converged issue: all 32 lanes of the MMA warp run the issue loop (so
+// descriptors and TMEM addresses stay in uniform registers) and elect.sync
+// picks the one lane that issues -- the single-lane form compiled to an
+// elect/broadcast loop per MMA whose issue cost (on a sub-partition shared
+// with two busy softmax warps) exceeded the MMA's own execution time.
 __device__ __forceinline__ void mma_ss_e(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -243,63 +201,63 @@ __device__ __forceinline__ void commit_e(uint64_t* b) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(b))
       : "memory");
 }
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// shared::cta address of this CTA -> the same offset in cluster rank `rank`
-__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float4 ld_cl4(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a));
-  return v;
+// suspending wait for the long waits of the producer / MMA warps (a probe
+// loop there takes issue slots from the softmax warps of its sub-partition)
+__device__ __forceinline__ void bar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra D_%=;\n\t"
+      "bra W_%=;\n"
+      "D_%=:\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
 }
 }  // namespace tca
+
+// Debug timeline (krul_debug_attn_timeline): %globaltimer stamps per CTA,
+// [cta][8] = entry, prologue done, Q in (MMA), MMA loop done, softmax done,
+// epilogue done, exit; then a clock64 trace of CTA (0, 0) per key block:
+// role (0/1 softmax A/B, 2 MMA) x block (< 64) x 4 events.
+__device__ unsigned long long* g_attn_ts = nullptr;
+__device__ __forceinline__ void attn_ts(int slot) {
+  if (g_attn_ts) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_attn_ts[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + slot] = t;
+  }
+}
+__device__ __forceinline__ void attn_tr(int role, int i, int ev) {
+  if (g_attn_ts && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) g_attn_ts[32768 + (role * 64 + i) * 4 + ev] = clock64();
+}
 
 // Causal flash attention over the paged KV cache, FA4-style on tcgen05.
 // One CTA = one work item (q tile of 128 rows, key-block range) for up to
 // two query heads; with GQA the two heads read the same KV head, so every
-// K/V page is staged once for both. Key block = one 64-token page (K [64][hd]
-// and V^T [hd][64], TMA SW128) in separate K (5-stage) and V (4-stage) rings.
+// K/V page is staged once for both. Key block = 128 keys = two 64-token
+// pages (K [128][hd], V^T [hd][128], TMA SW128, 2-stage ring).
 //   warps 0-3 / 4-7 : softmax of head A / B; thread = query row = TMEM lane.
-//     S (64 fp32 columns) is read once into registers, the probabilities are
-//     released at once (s_free), the probabilities are written as bf16 into
-//     a double-buffered P area of TMEM (P never touches shared memory), lazy
-//     O rescale (the running max moves only when a row max exceeds it by > 8
-//     in log2), MUFU ex2 with the scale folded into its FFMA.
+//     S (128 fp32 columns) is read once into registers, the probabilities
+//     are written back as bf16 into the first 64 columns of the same TMEM
+//     region (P never touches shared memory), lazy O rescale (the running
+//     max moves only when a row max exceeds it by > 8 in log2), MUFU ex2.
 //   warp 8 : K TMA producer, warp 10 : V TMA producer.
-//   warp 9 : MMA issuer (warp-converged, one elected lane). S(i+1) is issued
-//     as soon as the softmax warps hold S(i) in registers, so QK^T of the
-//     next block runs under the exponentials of this one; PV(i) follows as
-//     soon as P(i) is ready (A = P from TMEM).
-// TMEM (512 columns): S_A [0,64), S_B [64,128), P [head][buffer] at
-// 128 + (2 head + buffer) * 32, O_A at 256, O_B at 384.
-//
-// CL (one q tile, e.g. the new-input prefill): the splits of a head pair are
-// one thread-block cluster; each CTA parks its unnormalised O and (m, l,
-// mass) in its own shared memory, and after a cluster barrier CTA rank r
-// merges rows [r R/ns, (r+1) R/ns) of every split over DSMEM and writes the
-// bf16 output -- no partial round trip through HBM, no combine kernel.
-template <int HD, bool CL>
+//   warp 9 : MMA issuer, ping-pong over the heads: PV_A(i) (TS-MMA, A = P
+//     from TMEM) then S_A(i+1) while head B is exponentiated, then PV_B(i),
+//     S_B(i+1) while head A is -- the tensor pipe and the softmax warps
+//     overlap across the two heads.
+// TMEM (512 columns): S/P_A [0,128), S/P_B [128,256), O_A [256,..), O_B [384,..).
+template <int HD>
 __global__ void __launch_bounds__(352, 1)
     k_attn_fa(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, AttnTc p) {
   constexpr int KB = kAttnKB;
   constexpr int NSUB = HD / 64;                 // 64-wide hd sub-tiles
   constexpr uint32_t Q_BYTES = 128 * HD * 2;    // per head
-  constexpr uint32_t K_BYTES = KB * HD * 2;     // [NSUB][64 keys][128 B]
-  constexpr uint32_t V_BYTES = HD * KB * 2;     // [HD rows][128 B]
-  constexpr int KST = 5, VST = 4;  // separate K and V rings: K frees after S, V after PV
+  constexpr uint32_t K_BYTES = KB * HD * 2;     // [NSUB][128 keys][128 B]
+  constexpr uint32_t V_BYTES = HD * KB * 2;     // [2 key halves][HD rows][128 B]
+  constexpr int KST = 3, VST = 2;  // separate K and V rings: K frees after S, V after PV
   extern __shared__ unsigned char smraw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -312,12 +270,11 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* k_empty = k_full + KST;         // KST
   uint64_t* v_full = k_empty + KST;         // VST
   uint64_t* v_empty = v_full + VST;         // VST
-  uint64_t* s_full = v_empty + VST;         // [head]
-  uint64_t* s_free = s_full + 2;            // [head]: S read into registers
-  uint64_t* p_ready = s_free + 2;           // [head][P buffer]
-  uint64_t* pv_done = p_ready + 4;          // [head][P buffer]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 4);
-  int* pg_s = reinterpret_cast<int*>(tslot + 4);  // [kPgCache] page ids of this item
+  uint64_t* s_full = v_empty + VST;         // [2 heads]
+  uint64_t* p_ready = s_full + 2;           // [2 heads]
+  uint64_t* pv_done = p_ready + 2;          // [2 heads]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  int* pg_s = reinterpret_cast<int*>(tslot + 4);  // [2 * kPgCache] page ids of this item
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) attn_ts(0);
@@ -350,9 +307,6 @@ __global__ void __launch_bounds__(352, 1)
     }
     for (int i = 0; i < 2; ++i) {
       tca::bar_init(&s_full[i], 1);
-      tca::bar_init(&s_free[i], 128);
-    }
-    for (int i = 0; i < 4; ++i) {
       tca::bar_init(&p_ready[i], 128);
       tca::bar_init(&pv_done[i], 1);
     }
@@ -366,7 +320,8 @@ __global__ void __launch_bounds__(352, 1)
   // page ids of the item's key blocks, fetched once by all threads (a
   // dependent global load per block in the producer threads serialised the
   // K/V stream)
-  for (int i = threadIdx.x; i < min(nb, kPgCache); i += blockDim.x) pg_s[i] = p.pt[min(b0 + i, p.max_pages - 1)];
+  for (int i = threadIdx.x; i < 2 * min(nb, kPgCache); i += blockDim.x)
+    pg_s[i] = p.pt[min(2 * b0 + i, p.max_pages - 1)];
   tca::fence_before();
   __syncthreads();
   tca::fence_after();
@@ -374,41 +329,44 @@ __global__ void __launch_bounds__(352, 1)
   pdl_trigger();
   pdl_wait();  // Q and this step's K / V rows come from the preceding kernels
   if (threadIdx.x == 0) attn_ts(1);
-  auto page_of = [&](int i) { return i < kPgCache ? pg_s[i] : p.pt[min(b0 + i, p.max_pages - 1)]; };
+  auto page_of = [&](int i, int half) {
+    return i < kPgCache ? pg_s[2 * i + half] : p.pt[min(2 * (b0 + i) + half, p.max_pages - 1)];
+  };
 
   if (warp == 8) {
-    if (lane == 0 && nb > 0) {  // Q + K TMA producer
+    if (lane == 0 && nb > 0) {  // TMA producer
       tca::bar_expect(q_full, (hasB ? 2 : 1) * Q_BYTES);
       for (int j = 0; j < NSUB; ++j) {
         tca::tma2d(sQ + j * (128 * 128), &tmQ, q_full, hA * HD + 64 * j, int(q0));
         if (hasB) tca::tma2d(sQ + Q_BYTES + j * (128 * 128), &tmQ, q_full, hB * HD + 64 * j, int(q0));
       }
+      const int voff = p.Hkv * HD + g * HD;
       for (int i = 0; i < nb; ++i) {
-        const int pa = page_of(i);
+        const int pa = page_of(i, 0), pb = page_of(i, 1);
         const int ks = i % KST;
-        attn_tr(3, i, 0);
-        tca::bar_wait_mode(&k_empty[ks], ((i / KST) & 1) ^ 1, p.sleep);
-        attn_tr(3, i, 1);
+        tca::bar_wait_sleep(&k_empty[ks], ((i / KST) & 1) ^ 1);
         unsigned char* kd = sK + ks * K_BYTES;
         tca::bar_expect(&k_full[ks], K_BYTES);
-        for (int j = 0; j < NSUB; ++j) tca::tma2d(kd + j * (KB * 128), &tmK, &k_full[ks], 64 * j, pa * p.k_rows_pp + g * 64);
-        attn_tr(3, i, 2);
+        for (int j = 0; j < NSUB; ++j) {
+          tca::tma2d(kd + j * (KB * 128), &tmK, &k_full[ks], 64 * j, pa * p.k_rows_pp + g * 64);
+          tca::tma2d(kd + j * (KB * 128) + 64 * 128, &tmK, &k_full[ks], 64 * j, pb * p.k_rows_pp + g * 64);
+        }
       }
+      (void)voff;
     }
   } else if (warp == 10) {
-    // V producer: its own thread so a V slot still held by PV never holds
-    // back the K prefetch that the next QK^T waits for
+    // V producer: its own thread so a V slot still held by PV(i-2) never
+    // holds back the K prefetch that the next QK^T waits for
     if (lane == 0 && nb > 0) {
       const int voff = p.Hkv * HD + g * HD;
       for (int i = 0; i < nb; ++i) {
-        const int pa = page_of(i);
+        const int pa = page_of(i, 0), pb = page_of(i, 1);
         const int vs = i % VST;
-        attn_tr(4, i, 0);
-        tca::bar_wait_mode(&v_empty[vs], ((i / VST) & 1) ^ 1, p.sleep);
-        attn_tr(4, i, 1);
+        tca::bar_wait_sleep(&v_empty[vs], ((i / VST) & 1) ^ 1);
+        unsigned char* vd = sV + vs * V_BYTES;
         tca::bar_expect(&v_full[vs], V_BYTES);
-        tca::tma2d(sV + vs * V_BYTES, &tmV, &v_full[vs], 0, pa * p.v_rows_pp + voff);
-        attn_tr(4, i, 2);
+        tca::tma2d(vd, &tmV, &v_full[vs], 0, pa * p.v_rows_pp + voff);
+        tca::tma2d(vd + HD * 128, &tmV, &v_full[vs], 0, pb * p.v_rows_pp + voff);
       }
     }
   } else if (warp == 9) {
@@ -418,52 +376,55 @@ __global__ void __launch_bounds__(352, 1)
       constexpr uint32_t idO = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(HD >> 3) << 17) |
                                (uint32_t(128 >> 4) << 24);
       const int nh = hasB ? 2 : 1;
-      tca::bar_wait(q_full, 0);
+      // descriptor of a tile + byte offset = descriptor + offset / 16 (the
+      // 14-bit start-address field cannot carry inside shared memory)
+      auto issue_s = [&](int h, int i) {  // S_h(i) = Q_h K_i^T -> TMEM [h*128, +128)
+        const uint64_t dq = tca::desc(sQ + h * Q_BYTES), dk = tca::desc(sK + (i % KST) * K_BYTES);
+        const uint32_t dS = tmem + uint32_t(h * 128);
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tca::mma_ss_e(dS, dq + uint64_t((j * (128 * 128) + k * 32) >> 4),
+                          dk + uint64_t((j * (KB * 128) + k * 32) >> 4), idS, (j | k) != 0);
+        tca::commit_e(&s_full[h]);
+      };
+      auto issue_pv = [&](int h, int i) {  // O_h += P_h(i) V_i, P from TMEM
+        const uint64_t dv = tca::desc(sV + (i % VST) * V_BYTES);
+        const uint32_t dO = tmem + 256 + uint32_t(h * 128);
+        const uint32_t aP = tmem + uint32_t(h * 128);
+#pragma unroll
+        for (int k = 0; k < KB / 16; ++k)
+          tca::mma_ts_e(dO, aP + uint32_t(k * 8), dv + uint64_t(((k >> 2) * (HD * 128) + (k & 3) * 32) >> 4),
+                        idO, (i | k) != 0);
+        tca::commit_e(&pv_done[h]);
+      };
+      tca::bar_wait_sleep(q_full, 0);
       attn_ts(2);
-      // step t: S(t) for both heads (once K(t) is in and the softmax warps
-      // hold S(t-1) in registers), then PV(t-1) as each head's P(t-1) becomes
-      // ready
-      for (int t = 0; t <= nb; ++t) {
-        if (t < nb) {
-          const int ks = t % KST;
-          tca::bar_wait_mode(&k_full[ks], (t / KST) & 1, p.sleep);
-          attn_tr(2, t, 0);
-          for (int h = 0; h < nh; ++h) {
-            if (t >= 1) tca::bar_wait_mode(&s_free[h], (t - 1) & 1, p.sleep);
+      tca::bar_wait_sleep(&k_full[0], 0);
+      tca::fence_after();
+      for (int h = 0; h < nh; ++h) issue_s(h, 0);
+      tca::commit_e(&k_empty[0]);
+      for (int i = 0; i < nb; ++i) {
+        for (int h = 0; h < nh; ++h) {
+          tca::bar_wait_sleep(&p_ready[h], i & 1);
+          if (h == 0) tca::bar_wait_sleep(&v_full[i % VST], (i / VST) & 1);
+          tca::fence_after();
+          if (h == 0) attn_tr(2, i, 0);
+          issue_pv(h, i);
+          if (i + 1 < nb) {
+            if (h == 0) tca::bar_wait_sleep(&k_full[(i + 1) % KST], ((i + 1) / KST) & 1);
+            // P_h(i) lives in S_h's TMEM columns: S_h(i+1) is issued once
+            // PV_h(i) has consumed them
+            tca::bar_wait_sleep(&pv_done[h], i & 1);
             tca::fence_after();
-            // descriptor of a tile + byte offset = descriptor + offset / 16
-            // (the 14-bit start-address field cannot carry inside smem)
-            const uint64_t dq = tca::desc(sQ + h * Q_BYTES), dk = tca::desc(sK + ks * K_BYTES);
-            const uint32_t dS = tmem + uint32_t(h * KB);
-#pragma unroll
-            for (int j = 0; j < NSUB; ++j)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tca::mma_ss_e(dS, dq + uint64_t((j * (128 * 128) + k * 32) >> 4),
-                              dk + uint64_t((j * (KB * 128) + k * 32) >> 4), idS, (j | k) != 0);
-            tca::commit_e(&s_full[h]);
+            issue_s(h, i + 1);
           }
-          tca::commit_e(&k_empty[ks]);
-          attn_tr(2, t, 1);
+          if (h == 0) attn_tr(2, i, 1);
         }
-        if (t >= 1) {
-          const int i = t - 1, vs = i % VST, sb = i & 1;
-          tca::bar_wait_mode(&v_full[vs], (i / VST) & 1, p.sleep);
-          attn_tr(2, i, 2);
-          for (int h = 0; h < nh; ++h) {
-            tca::bar_wait_mode(&p_ready[2 * h + sb], (i >> 1) & 1, p.sleep);
-            tca::fence_after();
-            const uint64_t dv = tca::desc(sV + vs * V_BYTES);
-            const uint32_t dO = tmem + 256 + uint32_t(h * 128);
-            const uint32_t aP = tmem + 128 + uint32_t((2 * h + sb) * (KB / 2));
-#pragma unroll
-            for (int k = 0; k < KB / 16; ++k)
-              tca::mma_ts_e(dO, aP + uint32_t(k * 8), dv + uint64_t((k * 32) >> 4), idO, (i | k) != 0);
-            tca::commit_e(&pv_done[2 * h + sb]);
-          }
-          tca::commit_e(&v_empty[vs]);
-          attn_tr(2, i, 3);
-        }
+        attn_tr(2, i, 2);
+        tca::commit_e(&v_empty[i % VST]);                      // after PV_A(i), PV_B(i)
+        if (i + 1 < nb) tca::commit_e(&k_empty[(i + 1) % KST]);  // after S_A(i+1), S_B(i+1)
       }
       attn_ts(3);
     }
@@ -473,53 +434,47 @@ __global__ void __launch_bounds__(352, 1)
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
     const int64_t qpos = p.pos0 + q0 + r;
+    const uint32_t tS = tmem + uint32_t(wg * 128) + lane_off;
     const uint32_t tO = tmem + 256 + uint32_t(wg * 128) + lane_off;
     float m = -INFINITY, l = 0.f, mn = 0.f;
     const bool active = wg == 0 || hasB;
     if (active) {
       for (int i = 0; i < nb; ++i) {
-        const int sb = i & 1;
         const int64_t k0 = int64_t(b0 + i) * KB;
-        const uint32_t tS = tmem + uint32_t(wg * KB) + lane_off;
-        const uint32_t tP = tmem + 128 + uint32_t((2 * wg + sb) * (KB / 2)) + lane_off;
         const bool tr = (threadIdx.x & 127) == 0;
         if (tr) attn_tr(wg, i, 0);
-        tca::bar_wait_mode(&s_full[wg], i & 1, p.sleep >= 2);
+        tca::bar_wait(&s_full[wg], i & 1);
         tca::fence_after();
         if (tr) attn_tr(wg, i, 1);
-        uint32_t v[64];
-        tca::ld32_async(tS, v);
-        tca::ld32_async(tS + 32u, v + 32);
-        tca::ld_wait();
-        tca::fence_before();
-        tca::bar_arrive(&s_free[wg]);  // the MMA warp may overwrite S now
-        if (tr) attn_tr(wg, i, 2);
-        // visible keys of this row in the block: [k0, k0 + nv)
-        const int nv = int(imax64(0, imin64(KB, min(qpos + 1, p.kv_total) - k0)));
-        if (__any_sync(0xffffffffu, nv < KB)) {  // causal / sequence edge: mask (raw scores)
+        uint32_t v[128];
 #pragma unroll
-          for (int t = 0; t < 64; ++t) v[t] = t < nv ? v[t] : __float_as_uint(-INFINITY);
+        for (int c = 0; c < 4; ++c) tca::ld32_async(tS + uint32_t(c * 32), v + 32 * c);
+        tca::ld_wait();
+        if (tr) attn_tr(wg, i, 2);
+        // visible keys of this row in the block: [k0, k0 + nv); the raw
+        // scores are masked only on edge blocks (causal diagonal, sequence end)
+        const int nv = int(imax64(0, imin64(KB, min(qpos + 1, p.kv_total) - k0)));
+        if (__any_sync(0xffffffffu, nv < KB)) {
+#pragma unroll
+          for (int t = 0; t < 128; ++t) v[t] = t < nv ? v[t] : __float_as_uint(-INFINITY);
         }
         float mx;
-        {  // tree max of the raw scores; the log2-domain scale is positive, so
-           // it is applied to the max and folded into the exponent's FFMA
-          float t32[32];
+        {  // tree max
+          float t64[64];
 #pragma unroll
-          for (int t = 0; t < 32; ++t) t32[t] = fmaxf(__uint_as_float(v[t]), __uint_as_float(v[t + 32]));
+          for (int t = 0; t < 64; ++t) t64[t] = fmaxf(__uint_as_float(v[t]), __uint_as_float(v[t + 64]));
 #pragma unroll
-          for (int w = 16; w >= 1; w >>= 1)
+          for (int w = 32; w >= 1; w >>= 1)
 #pragma unroll
-            for (int t = 0; t < w; ++t) t32[t] = fmaxf(t32[t], t32[t + w]);
-          mx = t32[0] * p.scale_log2;
+            for (int t = 0; t < w; ++t) t64[t] = fmaxf(t64[t], t64[t + w]);
+          mx = t64[0] * p.scale_log2;  // the log2-domain scale is positive: applied to the max
         }
         // lazy max: move only when the block max exceeds it by > 8 (log2)
         float m_new = m;
         if (mx > m + 8.f || m == -INFINITY) m_new = fmaxf(mx, m);
         const float alpha = (m == -INFINITY || m_new == m) ? 1.f : ex2_approx(m - m_new);
+        // O rescale: PV(i-1) has completed (S(i) was issued after it)
         if (i > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          // O rescale once PV(i-1) has landed (PV(i) waits for this block's P)
-          tca::bar_wait(&pv_done[2 * wg + (sb ^ 1)], ((i - 1) >> 1) & 1);
-          tca::fence_after();
           uint32_t o[32];
 #pragma unroll 1
           for (int c = 0; c < HD / 32; ++c) {
@@ -537,7 +492,7 @@ __global__ void __launch_bounds__(352, 1)
         float sum = 0.f, msum = 0.f;
         // exponentiate and pack in place: v[j] <- bf16x2(p(2j), p(2j+1))
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < 64; ++j) {
           const float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * j]), p.scale_log2, -mb));
           const float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * j + 1]), p.scale_log2, -mb));
           sum += e0 + e1;
@@ -547,22 +502,18 @@ __global__ void __launch_bounds__(352, 1)
           }
           v[j] = pack2(e0, e1);
         }
-        // P buffer sb was last read by PV(i - 2)
-        if (i >= 2) {
-          tca::bar_wait_mode(&pv_done[2 * wg + sb], ((i - 2) >> 1) & 1, p.sleep >= 2);
-          tca::fence_after();
-        }
-        tca::st32_async(tP, v);
+        tca::st32_async(tS, v);
+        tca::st32_async(tS + 32u, v + 32);
         tca::st_wait();
         if (tr) attn_tr(wg, i, 3);
         l = l * alpha + sum;
         mn = mn * alpha + msum;
         m = m_new;
         tca::fence_before();
-        tca::bar_arrive(&p_ready[2 * wg + sb]);
+        tca::bar_arrive(&p_ready[wg]);
       }
       if (nb > 0) {
-        tca::bar_wait_mode(&pv_done[2 * wg + ((nb - 1) & 1)], ((nb - 1) >> 1) & 1, p.sleep >= 2);
+        tca::bar_wait(&pv_done[wg], (nb - 1) & 1);
         tca::fence_after();
       }
       if (threadIdx.x == 0) attn_ts(4);
@@ -591,22 +542,6 @@ __global__ void __launch_bounds__(352, 1)
           p.stats[(int64_t(h) * p.rows + row) * 2] = m;
           p.stats[(int64_t(h) * p.rows + row) * 2 + 1] = l;
         }
-      } else if (CL) {
-        // park the partial: O rows [wg][r][HD + 4] (padded: conflict-free
-        // 16-byte stores across the warp's rows) over the drained K/V rings,
-        // (m, l, mass) over the Q tiles
-        float* sO = reinterpret_cast<float*>(sK) + (wg * 128 + r) * (HD + 4);
-#pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-          tca::ld32(tO + uint32_t(c * 32), o);
-#pragma unroll
-          for (int t = 0; t < 32; t += 4)
-            *reinterpret_cast<float4*>(sO + c * 32 + t) =
-                make_float4(__uint_as_float(o[t]), __uint_as_float(o[t + 1]), __uint_as_float(o[t + 2]),
-                            __uint_as_float(o[t + 3]));
-        }
-        float* sML = reinterpret_cast<float*>(sQ) + (wg * 128 + r) * 4;
-        *reinterpret_cast<float4*>(sML) = make_float4(m, l, mn, 0.f);
       } else {
         // [slot][h][HD + 3][rows]: for each column the warp's 32 rows are
         // contiguous, so every store below is one coalesced 128-byte access
@@ -627,60 +562,6 @@ __global__ void __launch_bounds__(352, 1)
     }
   }
   __syncwarp();
-  if constexpr (CL) {
-    if (nsplit > 1) {
-      tca::cluster_sync();  // every split's partial is parked
-      const int ns = nsplit, rank = int(tca::cluster_rank());
-      const int R = int(imin64(128, p.rows - q0));
-      const int per = (R + ns - 1) / ns;
-      const int r0 = rank * per, r1 = min(R, r0 + per);
-      const int nh = hasB ? 2 : 1;
-      const uint32_t oBase = tca::su32(sK), mlBase = tca::su32(sQ);
-      const int items = nh * max(0, r1 - r0) * (HD / 4);
-      for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int c4 = it % (HD / 4), rr = r0 + (it / (HD / 4)) % max(1, r1 - r0), hh = it / ((HD / 4) * max(1, r1 - r0));
-        const uint32_t mlOff = uint32_t((hh * 128 + rr) * 4 * 4);
-        float M = -INFINITY;
-        float4 ml[16];
-#pragma unroll
-        for (int s2 = 0; s2 < 16; ++s2)
-          if (s2 < ns) {
-            ml[s2] = tca::ld_cl4(tca::mapa(mlBase + mlOff, uint32_t(s2)));
-            M = fmaxf(M, ml[s2].x);
-          }
-        float L = 0.f, MN = 0.f;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        const uint32_t oOff = uint32_t(((hh * 128 + rr) * (HD + 4) + 4 * c4) * 4);
-#pragma unroll
-        for (int s2 = 0; s2 < 16; ++s2)
-          if (s2 < ns) {
-            const float w = ml[s2].x == -INFINITY ? 0.f : ex2_approx(ml[s2].x - M);
-            L += w * ml[s2].y;
-            MN += w * ml[s2].z;
-            const float4 v = tca::ld_cl4(tca::mapa(oBase + oOff, uint32_t(s2)));
-            acc.x += w * v.x;
-            acc.y += w * v.y;
-            acc.z += w * v.z;
-            acc.w += w * v.w;
-          }
-        const float inv = L > 0.f ? 1.f / L : 0.f;
-        const int hq = hh == 0 ? hA : hB;
-        const int64_t row = q0 + rr;
-        uint2 w2;
-        w2.x = pack2(acc.x * inv, acc.y * inv);
-        w2.y = pack2(acc.z * inv, acc.w * inv);
-        *reinterpret_cast<uint2*>(p.out + (row * p.H + hq) * HD + 4 * c4) = w2;
-        if (c4 == 0) {
-          if (p.mass) p.mass[int64_t(hq) * p.rows + row] = L > 0.f ? double(MN) / double(L) : 0.0;
-          if (p.stats) {
-            p.stats[(int64_t(hq) * p.rows + row) * 2] = M;
-            p.stats[(int64_t(hq) * p.rows + row) * 2 + 1] = L;
-          }
-        }
-      }
-      tca::cluster_sync();  // no CTA leaves while its partial is being read
-    }
-  }
   if (threadIdx.x == 0) attn_ts(5);
   tca::fence_before();
   __syncthreads();
@@ -779,70 +660,19 @@ bool attention_tc_supported(const Ctx& c, const AttnArgs& a) {
          a.rows >= 1;
 }
 
-template <int HD, bool CL>
-size_t fa_smem() {
-  return 1024 + 2 * size_t(128) * HD * 2 + (5 + 4) * (size_t(kAttnKB) * HD * 2) + 256 + kPgCache * sizeof(int);
-}
-template <int HD, bool CL>
-void run_fa(cudaStream_t s, dim3 grid, int cluster, const CUtensorMap& tq, const CUtensorMap& tk,
+template <int HD>
+void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk,
             const CUtensorMap& tv, const AttnTc& p) {
-  const size_t smem = fa_smem<HD, CL>();
-  auto kern = k_attn_fa<HD, CL>;
+  const size_t smem = 1024 + 2 * size_t(128) * HD * 2 + (3 + 2) * (size_t(kAttnKB) * HD * 2) + 256 +
+                      2 * kPgCache * sizeof(int);
+  auto kern = k_attn_fa<HD>;
   static bool attr = false;
   if (!attr) {
     KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  if (!CL) {
-    KB_CUDA(launch_pdl(kern, grid, dim3(352), smem, s, tq, tk, tv, p));
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(352);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = unsigned(cluster);
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    KB_CUDA(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
-  }
+  KB_CUDA(launch_pdl(kern, grid, dim3(352), smem, s, tq, tk, tv, p));
   KB_LAUNCH();
-}
-
-// clusters of `cs` CTAs of the merging kernel that fit on the GPU at once
-// (clusters live inside one GPC; 0 = not launchable)
-template <int HD>
-int fa_max_clusters(int cs) {
-  static int cache[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-  if (cs < 1 || cs > 16) return 0;
-  if (cache[cs] >= 0) return cache[cs];
-  const size_t smem = fa_smem<HD, true>();
-  auto kern = k_attn_fa<HD, true>;
-  KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(cs), 1, 1);
-  cfg.blockDim = dim3(352);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = unsigned(cs);
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    n = 0;
-  }
-  cache[cs] = n;
-  return n;
 }
 
 void attn_set_timeline(unsigned long long* d) { KB_CUDA(cudaMemcpyToSymbol(g_attn_ts, &d, sizeof d)); }
@@ -872,19 +702,15 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   p.stats = a.stats;
   p.il = a.mass ? a.il : 0;
   p.rs = a.mass ? a.rs : INT64_MAX;
-  static const int sleep = [] {
-    const char* v = std::getenv("KRUL_ATTN_SLEEP");
-    return v ? std::atoi(v) : 1;
-  }();
-  p.sleep = sleep;
+
   // key blocks per work item: about one SM's fair share of all block-units,
-  // at least 8 (splitting costs a partial round trip + the merge)
+  // at least 4 (splitting costs a partial round trip + the merge)
   const int units_y = (g.H + p.hpc - 1) / p.hpc;
   int64_t total = 0;
   p.target = 1 << 30;
   for (int qt = 0; qt < p.n_qtiles; ++qt) total += attn_nblk(p, qt);
   const int64_t sms = c.sm_count > 0 ? c.sm_count : 148;
-  p.target = int(std::max<int64_t>(8, (total * units_y + sms - 1) / sms));
+  p.target = int(std::max<int64_t>(4, (total * units_y + sms - 1) / sms));
   p.target = std::max(p.target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
   {
     // wave quantisation: the fair share can leave a few items for a second
@@ -907,48 +733,12 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
     p.target = best_t;
   }
   if (g_attn_target > 0) p.target = std::max(g_attn_target, (attn_nblk(p, p.n_qtiles - 1) + kMaxSplit - 1) / kMaxSplit);
-  // one q tile (the new-input prefill): the splits of a head pair merge
-  // inside the kernel over DSMEM (cluster = the pair's splits, <= 8 so the
-  // clusters fit the GPCs in one wave) instead of through HBM partials and
-  // the combine kernel
-  // (measured: 6-CTA clusters, the widest whose 16 clusters fit the GPCs at
-  // once, run 45.8 us vs 38.8 us for 9 splits + combine on the 8B new-input
-  // shape, so the variant is opt-in: KRUL_ATTN_CLUSTER=1)
-  static const bool cl_on = [] {
-    const char* v = std::getenv("KRUL_ATTN_CLUSTER");
-    return v && v[0] == '1';
-  }();
-  int cluster = 0;
-  if (cl_on && p.n_qtiles == 1 && g_attn_target == 0) {
-    const int nblk = attn_nblk(p, 0);
-    // the widest split whose clusters all fit at once (GPCs hold whole
-    // clusters: 8-CTA clusters fit 15 at a time on B200, not the 16 needed)
-    int ns = 1, t = nblk, fit = 0;
-    for (int cs = int(std::min<int64_t>(8, std::max<int64_t>(1, sms / units_y))); cs > 1; --cs) {
-      const int tt = (nblk + cs - 1) / cs;
-      const int nn = (nblk + tt - 1) / tt;
-      const int f = HD == 128 ? fa_max_clusters<128>(nn) : fa_max_clusters<64>(nn);
-      if (nn > 1 && f >= units_y) {
-        ns = nn;
-        t = tt;
-        fit = f;
-        break;
-      }
-    }
-    if (ns > 1) {
-      p.target = t;
-      cluster = ns;
-    }
-    static const bool dbg = std::getenv("KRUL_ATTN_DEBUG") != nullptr;
-    if (dbg) std::fprintf(stderr, "attn: rows %lld nblk %d target %d fit %d units %d -> cluster %d\n",
-                          (long long)a.rows, nblk, t, fit, units_y, cluster);
-  }
   int items = 0, max_split = 1;
   for (int qt = 0; qt < p.n_qtiles; ++qt) {
     items += attn_nsplit(p, qt);
     max_split = std::max(max_split, attn_nsplit(p, qt));
   }
-  if (max_split > 1 && !cluster)
+  if (max_split > 1)
     p.part = static_cast<float*>(
         scratch.ensure(size_t(max_split) * a.rows * g.H * (HD + 3) * sizeof(float)));
   const uint64_t pool_elems = uint64_t(c.pool_pages) * pe;
@@ -956,17 +746,10 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   const CUtensorMap tk = map2d(c.pool.p, pool_elems / HD, HD, HD, 64);
   const CUtensorMap tv = map2d(c.pool.p, pool_elems / 64, 64, 64, uint32_t(HD));
   const dim3 grid{unsigned(items), unsigned(units_y), 1u};
-  if (cluster) {
-    if (HD == 128)
-      run_fa<128, true>(s, grid, cluster, tq, tk, tv, p);
-    else
-      run_fa<64, true>(s, grid, cluster, tq, tk, tv, p);
-    return;
-  }
   if (HD == 128)
-    run_fa<128, false>(s, grid, 0, tq, tk, tv, p);
+    run_fa<128>(s, grid, tq, tk, tv, p);
   else
-    run_fa<64, false>(s, grid, 0, tq, tk, tv, p);
+    run_fa<64>(s, grid, tq, tk, tv, p);
   if (max_split > 1) {
     const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), unsigned(HD / 32)};
     if (HD == 128)

@@ -1,0 +1,3 @@
+timeout 600 python -m pytest tests -m gpu -x -q -k "attn or attention or fa or prefill or restore or turn" 2>&1 | tail -2
+python tools/attn_bench.py 2>&1 | tail -8
+python tools/attn_timeline.py 128 8192 0 | sed -n '/softmaxA/,$p' | head -40
