@@ -328,6 +328,15 @@ int krul_restore_and_prefill(krul_ctx* ctx, krul_conv* conv,
                              int64_t L, const int32_t* new_tokens, int64_t n_new,
                              float* logits, krul_restore_stats* stats,
                              double* ttft_ms);
+/* Restore + new-input prefill of n conversations pipelined back to back
+ * (configs[3]): conversation i+1's blob copies start under conversation i's
+ * new-input prefill tail. convs[i] != convs[i-1]. logits: n x V floats (may be
+ * NULL); ttft_ms[i] = device time from item i's first copy to its logits;
+ * total_ms = first copy to the last logits. No counterpart in the reference
+ * (harness.cpp restores one conversation at a time). */
+int krul_restore_batch(krul_ctx* ctx, int n, krul_conv* const* convs, krul_snapshot* const* snaps,
+                       const int32_t* const* histories, const int64_t* L, const int32_t* const* new_tokens,
+                       const int64_t* n_new, float* logits, double* ttft_ms, double* total_ms);
 
 /* Record the per-layer timeline events in the restore DAG (default on). */
 int krul_set_timeline(krul_ctx* ctx, int on);

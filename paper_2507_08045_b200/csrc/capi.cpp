@@ -945,6 +945,32 @@ int krul_restore_and_prefill(krul_ctx* ctx, krul_conv* conv, krul_snapshot* snap
   });
 }
 
+int krul_restore_batch(krul_ctx* ctx, int n, krul_conv* const* convs, krul_snapshot* const* snaps,
+                       const int32_t* const* histories, const int64_t* L, const int32_t* const* new_tokens,
+                       const int64_t* n_new, float* logits, double* ttft_ms, double* total_ms) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (n <= 0) fail(KRUL_E_CONFIG, "empty restore batch");
+    need(convs, "convs");
+    need(snaps, "snapshots");
+    need(histories, "histories");
+    need(L, "L");
+    need(new_tokens, "new tokens");
+    need(n_new, "n_new");
+    std::vector<Conv*> cv(static_cast<size_t>(n));
+    std::vector<Snapshot*> sv(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      need(convs[i], "conv");
+      need(snaps[i], "snapshot");
+      need(new_tokens[i], "new tokens");
+      if (L[i] > 0) need(histories[i], "history");
+      cv[size_t(i)] = convs[i]->v;
+      sv[size_t(i)] = snaps[i]->s;
+    }
+    restore_batch(*ctx->c, n, cv.data(), sv.data(), histories, L, new_tokens, n_new, logits, ttft_ms, total_ms);
+  });
+}
+
 // Measured stream rates (calibrate_rc_measured, scheduler.cpp:402-443, as
 // device rates rather than a wall-clock grid): pinned H2D bytes/s over a
 // 256 MiB copy and recompute flop/s of one full layer at 2048 rows.

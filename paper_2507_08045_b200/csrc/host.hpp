@@ -133,5 +133,8 @@ void restore_timeline(Ctx& c);  // reads the last restore's per-layer events
 void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
              krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
              double* ttft_ms);
+void restore_batch(Ctx& c, int n, Conv* const* convs, Snapshot* const* snaps, const int32_t* const* hists,
+                   const int64_t* Ls, const int32_t* const* news, const int64_t* n_news, float* logits,
+                   double* ttft_ms, double* total_ms);
 
 }  // namespace kb

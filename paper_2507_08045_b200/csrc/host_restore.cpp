@@ -178,9 +178,22 @@ uint64_t next_serial() {
 // The restore DAG on the ctx streams (all asynchronous, joined back into
 // s_comp). Events: ev[0] launch, ev[1] compute end, ev[2] load end, ev[3]
 // end, ev[4] H2D end, ev[5..5+N) computed[l], then loaded[l], then newp[l].
+// Pipelined batch mode (restore_batch): tokens already on the device
+// (uploaded on the load stream, `tok_ready`), the coded / raw staging of this
+// item's slot, no join into s_comp at the end (the next conversation's copies
+// start under this one's new-input prefill tail), logits read back on the
+// prefill stream.
+struct PipeItem {
+  const int32_t* d_tok = nullptr;
+  const int32_t* d_new = nullptr;
+  cudaEvent_t tok_ready = nullptr;
+  char* stg = nullptr;
+  char* cstg = nullptr;
+  float* logits_host = nullptr;  // pinned, may be null
+};
 static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const int32_t* tp_hist,
                             const int32_t* tp_new, int64_t n_new, float* lp, double* h2d_out,
-                            double* expand_out) {
+                            double* expand_out, const PipeItem* pipe = nullptr) {
   const Cfg& g = c.cfg;
   const std::vector<int64_t>& p = snap.p;
   auto& E = c.rg.ev;
@@ -189,19 +202,31 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   const Mark* loaded = computed + g.N;
   const Mark* newp = loaded + g.N;
   cudaStream_t sc = c.s_comp, sl = c.s_load;
-  char* stg = static_cast<char*>(c.staging.p);
-  char* cstg = static_cast<char*>(c.cstaging.p);
+  char* stg = pipe ? pipe->stg : static_cast<char*>(c.staging.p);
+  char* cstg = pipe ? pipe->cstg : static_cast<char*>(c.cstaging.p);
   float* d_logits = static_cast<float*>(c.ws_logits.p);
 
-  // token uploads first: a small H2D queued behind the blob copies on the
-  // copy engine would hold the recompute back for the whole load (~14 ms)
-  record_mark(ev0, sc);
-  int32_t* d_tok = upload_tokens(c, sc, tp_hist, std::max<int64_t>(p[0], 0), c.ws_tok);
-  int32_t* d_new = tp_new ? upload_tokens(c, sc, tp_new, n_new, c.ws_tok2) : nullptr;
-  cudaEvent_t tok_ready = c.event();
-  KB_CUDA(cudaEventRecord(tok_ready, sc));
-  KB_CUDA(cudaStreamWaitEvent(sl, tok_ready, 0));
-  KB_CUDA(cudaStreamWaitEvent(c.s_exp, ev0.dep, 0));
+  const int32_t* d_tok;
+  const int32_t* d_new;
+  cudaEvent_t tok_ready;
+  if (pipe) {
+    record_mark(ev0, sl);
+    d_tok = pipe->d_tok;
+    d_new = pipe->d_new;
+    tok_ready = pipe->tok_ready;
+    KB_CUDA(cudaStreamWaitEvent(sc, tok_ready, 0));
+    KB_CUDA(cudaStreamWaitEvent(c.s_exp, tok_ready, 0));
+  } else {
+    // token uploads first: a small H2D queued behind the blob copies on the
+    // copy engine would hold the recompute back for the whole load (~14 ms)
+    record_mark(ev0, sc);
+    d_tok = upload_tokens(c, sc, tp_hist, std::max<int64_t>(p[0], 0), c.ws_tok);
+    d_new = tp_new ? upload_tokens(c, sc, tp_new, n_new, c.ws_tok2) : nullptr;
+    tok_ready = c.event();
+    KB_CUDA(cudaEventRecord(tok_ready, sc));
+    KB_CUDA(cudaStreamWaitEvent(sl, tok_ready, 0));
+    KB_CUDA(cudaStreamWaitEvent(c.s_exp, ev0.dep, 0));
+  }
   // ---- load stream: K4 H2D copies back to back on the copy engine; K5
   // expand kernels on their own stream behind each blob's copy, so the PCIe
   // link never idles while a scatter runs.
@@ -267,7 +292,8 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     const char* v = std::getenv("KRUL_FUSED");
     return !(v && v[0] == '0');
   }();
-  const bool fused = tp_new && fused_env && c.fused;
+  const bool has_new = d_new != nullptr;  // host tokens (single restore) or device tokens (pipelined)
+  const bool fused = has_new && fused_env && c.fused;
   if (fused) {
     // ---- K6 + K7 fused: the recompute rows ride in the new-input prefill's
     // layer steps (forward_fused), one weight pass per layer
@@ -299,7 +325,7 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     return !(v && v[0] == '0');
   }();
   const bool two_stream = two_stream_env && c.two_stream;
-  if (tp_new) {
+  if (has_new) {
     cudaStream_t sn = two_stream ? c.s_new : sc;
     if (two_stream) KB_CUDA(cudaStreamWaitEvent(sn, tok_ready, 0));
     std::vector<cudaEvent_t> waits;
@@ -307,7 +333,14 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     for (int l = 0; l < g.N; ++l) waits.push_back(loaded[l].dep);
     conv.len = L;
     forward_rows(c, sn, 1, conv, d_new, n_new, L, d_logits, &waits, newp);
+    if (pipe && pipe->logits_host)
+      KB_CUDA(cudaMemcpyAsync(pipe->logits_host, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sn));
     record_mark(ev_end, sn);
+    if (pipe) {  // no join: the next conversation's restore starts under this tail
+      *h2d_out = h2d;
+      *expand_out = expand_bytes;
+      return;
+    }
     if (two_stream) KB_CUDA(cudaStreamWaitEvent(sc, ev_end.dep, 0));
   } else {
     record_mark(ev_end, sc);
@@ -324,9 +357,8 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
 // (snapshot, conversation, shape) is captured once into a CUDA graph and
 // replayed: one host launch instead of ~600, so the streams start
 // back-to-back on the device.
-void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
-             krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
-             double* ttft_ms) {
+static void check_restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
+                          const int32_t* new_tok, int64_t n_new) {
   const Cfg& g = c.cfg;
   if (snap.config_hash != config_hash(g)) fail(KRUL_E_SNAPSHOT, "snapshot was taken under a different model config");
   if (snap.esz != c.esz || (snap.host.pageable && !snap.host.registered))
@@ -346,6 +378,14 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     check_tokens(c, new_tok, n_new);
   }
   if (L + std::max<int64_t>(n_new, 0) > conv.capacity) fail(KRUL_E_CONFIG, "history exceeds the conversation capacity");
+}
+
+void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
+             krul_restore_stats* st, const int32_t* new_tok, int64_t n_new, float* logits,
+             double* ttft_ms) {
+  const Cfg& g = c.cfg;
+  check_restore(c, conv, snap, hist, L, new_tok, n_new);
+  const std::vector<int64_t>& p = snap.p;
   KB_CUDA(cudaSetDevice(c.device));
   const int64_t nh = std::max<int64_t>(p[0], 0), nn = new_tok ? n_new : 0;
 
@@ -490,6 +530,110 @@ void restore_timeline(Ctx& c) {
     }
   }
   c.tl_pending = false;
+}
+
+// Pipelined restore of a batch of conversations (configs[3]: many
+// conversations per GPU). The DAGs are enqueued back to back without a join:
+// conversation i+1's token upload and blob copies start on the load stream as
+// soon as conversation i's copies are done, under i's new-input prefill tail
+// (the PCIe link is otherwise idle there). Coded / raw staging alternate
+// between two slots (item i+2 reuses i's slot after i's decode + expand);
+// consecutive items must restore into different conversations. Per item the
+// device time from its first copy to its logits; total = first copy to the
+// last logits.
+void restore_batch(Ctx& c, int n, Conv* const* convs, Snapshot* const* snaps, const int32_t* const* hists,
+                   const int64_t* Ls, const int32_t* const* news, const int64_t* n_news, float* logits,
+                   double* ttft_ms, double* total_ms) {
+  const Cfg& g = c.cfg;
+  if (n <= 0) fail(KRUL_E_CONFIG, "empty restore batch");
+  for (int i = 0; i < n; ++i) {
+    check_restore(c, *convs[i], *snaps[i], hists[i], Ls[i], news[i], n_news[i]);
+    if (n_news[i] <= 0) fail(KRUL_E_RESTORATION_GAP, "prefill over preloaded history requires new input tokens");
+    if (i > 0 && convs[i] == convs[i - 1]) fail(KRUL_E_CONFIG, "consecutive batch items need different conversations");
+  }
+  if (c.fused) fail(KRUL_E_CONFIG, "the pipelined batch restore runs the two-stream DAG (fused recompute off)");
+  KB_CUDA(cudaSetDevice(c.device));
+  c.drop_graph();
+  const bool kt_was = c.kt.on;
+  c.kt.on = false;  // per-launch events would serialise the pipelined DAGs
+  // tokens of every item in one pinned block and one device block
+  std::vector<size_t> toff(size_t(n) + 1, 0);
+  for (int i = 0; i < n; ++i) toff[size_t(i) + 1] = toff[size_t(i)] + size_t(std::max<int64_t>(snaps[i]->p[0], 0) + n_news[i]);
+  int32_t* tp = static_cast<int32_t*>(c.tok_pin.ensure((toff[size_t(n)] + 1) * 4));
+  DevBuf dtok;
+  int32_t* dt = static_cast<int32_t*>(dtok.ensure((toff[size_t(n)] + 1) * 4));
+  size_t stg_max = 256, cstg_max = 256;
+  for (int i = 0; i < n; ++i) {
+    const int64_t nh = std::max<int64_t>(snaps[i]->p[0], 0);
+    if (nh) std::memcpy(tp + toff[size_t(i)], hists[i], size_t(nh) * 4);
+    std::memcpy(tp + toff[size_t(i)] + nh, news[i], size_t(n_news[i]) * 4);
+    stg_max = std::max(stg_max, snaps[i]->total);
+    if (snaps[i]->coded) cstg_max = std::max(cstg_max, snaps[i]->ctotal);
+  }
+  DevBuf stg2, cstg2;
+  char* stg_slot[2] = {static_cast<char*>(c.staging.ensure(stg_max)), static_cast<char*>(stg2.ensure(stg_max))};
+  char* cstg_slot[2] = {static_cast<char*>(c.cstaging.ensure(cstg_max)), static_cast<char*>(cstg2.ensure(cstg_max))};
+  c.ws_logits.ensure(size_t(g.V) * 4);
+  float* lp = logits ? static_cast<float*>(c.logits_pin.ensure(size_t(n) * g.V * 4)) : nullptr;
+  auto& G = c.rg;
+  G.ev.resize(size_t(5 + 3 * g.N));
+  for (size_t i = 0; i < G.ev.size(); ++i) {
+    auto& m = G.ev[i];
+    if (!m.dep) KB_CUDA(cudaEventCreateWithFlags(&m.dep, cudaEventDisableTiming));
+  }
+  G.snap_serial = 0;  // the graph key is void after a batch
+  c.reset_events();
+  const size_t nn = static_cast<size_t>(n);
+  std::vector<cudaEvent_t> t0(nn), t1(nn), done(nn);
+  for (int i = 0; i < n; ++i) {
+    KB_CUDA(cudaEventCreate(&t0[size_t(i)]));
+    KB_CUDA(cudaEventCreate(&t1[size_t(i)]));
+    KB_CUDA(cudaEventCreateWithFlags(&done[size_t(i)], cudaEventDisableTiming));
+  }
+  cudaStream_t sl = c.s_load;
+  for (int i = 0; i < n; ++i) {
+    const int slot = i & 1;
+    if (i >= 2) KB_CUDA(cudaStreamWaitEvent(sl, done[size_t(i - 2)], 0));  // the slot's previous item decoded
+    const int64_t nh = std::max<int64_t>(snaps[i]->p[0], 0);
+    int32_t* d = dt + toff[size_t(i)];
+    KB_CUDA(cudaEventRecord(t0[size_t(i)], sl));
+    KB_CUDA(cudaMemcpyAsync(d, tp + toff[size_t(i)], size_t(nh + n_news[i]) * 4, cudaMemcpyHostToDevice, sl));
+    PipeItem it;
+    it.d_tok = d;
+    it.d_new = d + nh;
+    it.tok_ready = c.event();
+    KB_CUDA(cudaEventRecord(it.tok_ready, sl));
+    it.stg = stg_slot[slot];
+    it.cstg = cstg_slot[slot];
+    it.logits_host = lp ? lp + size_t(i) * g.V : nullptr;
+    double h2d = 0, eb = 0;
+    enqueue_restore(c, *convs[i], *snaps[i], Ls[i], nullptr, nullptr, n_news[i], nullptr, &h2d, &eb, &it);
+    KB_CUDA(cudaEventRecord(done[size_t(i)], c.s_exp));
+    KB_CUDA(cudaEventRecord(t1[size_t(i)], c.s_new));
+    convs[i]->len = Ls[i] + n_news[i];
+  }
+  // join everything back into s_comp
+  KB_CUDA(cudaStreamWaitEvent(c.s_comp, t1[size_t(n - 1)], 0));
+  KB_CUDA(cudaStreamWaitEvent(c.s_comp, done[size_t(n - 1)], 0));
+  KB_CUDA(cudaStreamWaitEvent(c.s_comp, G.ev[4].dep, 0));
+  KB_CUDA(cudaStreamSynchronize(c.s_comp));
+  KB_CUDA(cudaDeviceSynchronize());
+  for (int i = 0; i < n; ++i) {
+    float ms = 0;
+    KB_CUDA(cudaEventElapsedTime(&ms, t0[size_t(i)], t1[size_t(i)]));
+    if (ttft_ms) ttft_ms[i] = ms;
+  }
+  float tot = 0;
+  KB_CUDA(cudaEventElapsedTime(&tot, t0[0], t1[size_t(n - 1)]));
+  if (total_ms) *total_ms = tot;
+  if (logits) std::memcpy(logits, lp, size_t(n) * g.V * 4);
+  for (int i = 0; i < n; ++i) {
+    cudaEventDestroy(t0[size_t(i)]);
+    cudaEventDestroy(t1[size_t(i)]);
+    cudaEventDestroy(done[size_t(i)]);
+  }
+  c.tl_pending = false;
+  c.kt.on = kt_was;
 }
 
 }  // namespace kb

@@ -385,6 +385,27 @@ class Context:
         return out, st.as_dict(), ttft.value
 
 
+    def restore_batch(self, convs, histories, snapshots, new_tokens, logits=False):
+        """Pipelined restore + new-input prefill of a batch (conversation i+1's
+        copies under conversation i's prefill tail) -> (ttft_ms[n], total_ms,
+        logits[n][V] or None). Consecutive items need different conversations."""
+        n = len(convs)
+        hs = [np.ascontiguousarray(h, np.int32) for h in histories]
+        ns = [np.ascontiguousarray(t, np.int32) for t in new_tokens]
+        cv = (C.c_void_p * n)(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in convs])
+        sv = (C.c_void_p * n)(*[s.h.value if isinstance(s.h, C.c_void_p) else s.h for s in snapshots])
+        hp = (C.c_void_p * n)(*[h.ctypes.data for h in hs])
+        npp = (C.c_void_p * n)(*[t.ctypes.data for t in ns])
+        Ls = np.array([h.size for h in hs], np.int64)
+        nn = np.array([t.size for t in ns], np.int64)
+        tt = np.zeros(n, np.float64)
+        tot = C.c_double()
+        out = np.empty((n, self.cfg.vocab_size), np.float32) if logits else None
+        _check(lib().krul_restore_batch(self.h, n, cv, sv, hp, _p(Ls), npp, _p(nn),
+                                        _p(out) if out is not None else None, _p(tt), C.byref(tot)))
+        return tt, tot.value, out
+
+
 class Conversation:
     """Paged KV cache of one conversation (krul_conv)."""
 
