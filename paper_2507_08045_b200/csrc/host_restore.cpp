@@ -560,8 +560,7 @@ void restore_batch(Ctx& c, int n, Conv* const* convs, Snapshot* const* snaps, co
   std::vector<size_t> toff(size_t(n) + 1, 0);
   for (int i = 0; i < n; ++i) toff[size_t(i) + 1] = toff[size_t(i)] + size_t(std::max<int64_t>(snaps[i]->p[0], 0) + n_news[i]);
   int32_t* tp = static_cast<int32_t*>(c.tok_pin.ensure((toff[size_t(n)] + 1) * 4));
-  DevBuf dtok;
-  int32_t* dt = static_cast<int32_t*>(dtok.ensure((toff[size_t(n)] + 1) * 4));
+  int32_t* dt = static_cast<int32_t*>(c.batch_tok.ensure((toff[size_t(n)] + 1) * 4));
   size_t stg_max = 256, cstg_max = 256;
   for (int i = 0; i < n; ++i) {
     const int64_t nh = std::max<int64_t>(snaps[i]->p[0], 0);
@@ -570,9 +569,11 @@ void restore_batch(Ctx& c, int n, Conv* const* convs, Snapshot* const* snaps, co
     stg_max = std::max(stg_max, snaps[i]->total);
     if (snaps[i]->coded) cstg_max = std::max(cstg_max, snaps[i]->ctotal);
   }
-  DevBuf stg2, cstg2;
-  char* stg_slot[2] = {static_cast<char*>(c.staging.ensure(stg_max)), static_cast<char*>(stg2.ensure(stg_max))};
-  char* cstg_slot[2] = {static_cast<char*>(c.cstaging.ensure(cstg_max)), static_cast<char*>(cstg2.ensure(cstg_max))};
+  // ctx-owned, grow-only: a per-call cudaMalloc / cudaFree (which
+  // synchronises the device) would cost more than the overlap gains
+  char* stg_slot[2] = {static_cast<char*>(c.staging.ensure(stg_max)), static_cast<char*>(c.staging2.ensure(stg_max))};
+  char* cstg_slot[2] = {static_cast<char*>(c.cstaging.ensure(cstg_max)),
+                        static_cast<char*>(c.cstaging2.ensure(cstg_max))};
   c.ws_logits.ensure(size_t(g.V) * 4);
   float* lp = logits ? static_cast<float*>(c.logits_pin.ensure(size_t(n) * g.V * 4)) : nullptr;
   auto& G = c.rg;

@@ -226,6 +226,7 @@ struct Ctx {
   bool tl_pending = false, tl_has_new = false;  // per-layer timeline not yet read back
   DevBuf staging;
   DevBuf cstaging;       // coded blob images (H2D target; decoded into `staging`)
+  DevBuf staging2, cstaging2, batch_tok;  // restore_batch: the second staging slot, the batch's tokens
   bool kv_coding = true; // exponent-code bf16 snapshots at compress (KRUL_KV_CODING=0: off)
   PinnedBuf tok_pin;     // pinned token staging (history | new input) for async / graph H2D
   PinnedBuf logits_pin;  // pinned logits landing buffer
