@@ -387,6 +387,9 @@ int krul_measure_rates(krul_ctx* ctx, krul_conv* scratch, double* h2d_bps,
  * separate recompute stream. */
 int krul_set_fused_recompute(krul_ctx* ctx, int on);
 int krul_set_concurrency(krul_ctx* ctx, int two_stream);
+/* Capture repeated restore DAGs into CUDA graphs (default on); off = every
+ * restore is enqueued eagerly, as the first restore of a conversation is. */
+int krul_set_graphs(krul_ctx* ctx, int on);
 
 /* ---- measurement support (not on the reference's interface) ----------
  * krul_launch_count: number of kernels this library has launched (process

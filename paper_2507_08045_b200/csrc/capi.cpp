@@ -1499,6 +1499,13 @@ int krul_set_timeline(krul_ctx* ctx, int on) {
     ctx->c->timeline = on != 0;
   });
 }
+int krul_set_graphs(krul_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->drop_graph();
+    ctx->c->use_graphs = on != 0;
+  });
+}
 int krul_set_fused_recompute(krul_ctx* ctx, int on) {
   return guard([&] {
     need(ctx, "ctx");

@@ -335,6 +335,10 @@ class Context:
         """Record per-layer timeline events in the restore DAG (diagnostic)."""
         _check(lib().krul_set_timeline(self.h, int(bool(on))))
 
+    def set_graphs(self, on: bool):
+        """Graph-capture repeated restore DAGs (default) or enqueue every restore eagerly."""
+        _check(lib().krul_set_graphs(self.h, int(bool(on))))
+
     def set_fused_recompute(self, on: bool):
         """Fold the recompute rows into the new-input prefill's layer steps (default off)."""
         _check(lib().krul_set_fused_recompute(self.h, int(bool(on))))
