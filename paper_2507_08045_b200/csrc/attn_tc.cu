@@ -572,6 +572,323 @@ __global__ void __launch_bounds__(352, 1)
   if (threadIdx.x == 0) attn_ts(6);
 }
 
+// One head per CTA (k_attn_fa1): S double-buffered in TMEM (S0, S1, O =
+// 384 columns) so QK^T of block i+1 runs while block i is exponentiated and
+// the per-head PV(i) -> S(i+1) chain no longer serialises the softmax; two
+// softmax warps per TMEM lane quadrant split each 128-key block into column
+// halves (row max / sums exchanged through shared memory), so one block's
+// exponentials spread over 8 warps. Warp 8: TMA producers (lane 0 Q + K,
+// lane 1 V), warp 9: MMA issuer (warp-converged). P goes back over S's own
+// columns [0, 64) of its buffer; PV is a TS-MMA. Each K/V page is staged per
+// head (twice the shared-memory fill of the head-pair kernel).
+template <int HD>
+__global__ void __launch_bounds__(320, 1)
+    k_attn_fa1(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmV, AttnTc p) {
+  constexpr int KB = kAttnKB;
+  constexpr int NSUB = HD / 64;
+  constexpr uint32_t Q_BYTES = 128 * HD * 2;
+  constexpr uint32_t K_BYTES = KB * HD * 2;
+  constexpr uint32_t V_BYTES = HD * KB * 2;
+  constexpr int KST = 3, VST = 2;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sQ = base;
+  unsigned char* sK = sQ + Q_BYTES;
+  unsigned char* sV = sK + KST * K_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VST * V_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;   // [buffer]
+  uint64_t* p_ready = s_full + 2;     // [buffer]
+  uint64_t* pv_done = p_ready + 2;    // [buffer]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  int* pg_s = reinterpret_cast<int*>(tslot + 4);              // [2 * kPgCache]
+  float* xs = reinterpret_cast<float*>(pg_s + 2 * kPgCache);  // [half][128 rows][2]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) attn_ts(0);
+  int qt = p.n_qtiles - 1, split = int(blockIdx.x);
+  for (; qt > 0; --qt) {
+    const int ns = attn_nsplit(p, qt);
+    if (split < ns) break;
+    split -= ns;
+  }
+  const int nsplit = attn_nsplit(p, qt);
+  const int nblk_all = attn_nblk(p, qt);
+  const int b0 = split * p.target;
+  const int b1 = min(nblk_all, b0 + p.target);
+  const int nb = b1 - b0;
+  const int h = int(blockIdx.y);
+  const int g = h / p.grp;
+  const int64_t q0 = int64_t(qt) * 128;
+
+  if (threadIdx.x == 0) {
+    tca::bar_init(q_full, 1);
+    for (int s = 0; s < KST; ++s) {
+      tca::bar_init(&k_full[s], 1);
+      tca::bar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      tca::bar_init(&v_full[s], 1);
+      tca::bar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tca::bar_init(&s_full[i], 1);
+      tca::bar_init(&p_ready[i], 256);
+      tca::bar_init(&pv_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        tca::su32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < 2 * min(nb, kPgCache); i += blockDim.x)
+    pg_s[i] = p.pt[min(2 * b0 + i, p.max_pages - 1)];
+  tca::fence_before();
+  __syncthreads();
+  tca::fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) attn_ts(1);
+  auto page_of = [&](int i, int half) {
+    return i < kPgCache ? pg_s[2 * i + half] : p.pt[min(2 * (b0 + i) + half, p.max_pages - 1)];
+  };
+
+  if (warp == 8 && lane == 0) {
+    if (nb > 0) {  // Q + K producer
+      tca::bar_expect(q_full, Q_BYTES);
+      for (int j = 0; j < NSUB; ++j) tca::tma2d(sQ + j * (128 * 128), &tmQ, q_full, h * HD + 64 * j, int(q0));
+      for (int i = 0; i < nb; ++i) {
+        const int pa = page_of(i, 0), pb = page_of(i, 1);
+        const int ks = i % KST;
+        tca::bar_wait_sleep(&k_empty[ks], ((i / KST) & 1) ^ 1);
+        unsigned char* kd = sK + ks * K_BYTES;
+        tca::bar_expect(&k_full[ks], K_BYTES);
+        for (int j = 0; j < NSUB; ++j) {
+          tca::tma2d(kd + j * (KB * 128), &tmK, &k_full[ks], 64 * j, pa * p.k_rows_pp + g * 64);
+          tca::tma2d(kd + j * (KB * 128) + 64 * 128, &tmK, &k_full[ks], 64 * j, pb * p.k_rows_pp + g * 64);
+        }
+      }
+    }
+  } else if (warp == 8 && lane == 1) {
+    if (nb > 0) {  // V producer
+      const int voff = p.Hkv * HD + g * HD;
+      for (int i = 0; i < nb; ++i) {
+        const int pa = page_of(i, 0), pb = page_of(i, 1);
+        const int vs = i % VST;
+        tca::bar_wait_sleep(&v_empty[vs], ((i / VST) & 1) ^ 1);
+        unsigned char* vd = sV + vs * V_BYTES;
+        tca::bar_expect(&v_full[vs], V_BYTES);
+        tca::tma2d(vd, &tmV, &v_full[vs], 0, pa * p.v_rows_pp + voff);
+        tca::tma2d(vd + HD * 128, &tmV, &v_full[vs], 0, pb * p.v_rows_pp + voff);
+      }
+    }
+  } else if (warp == 9) {
+    if (nb > 0) {  // MMA issuer: the whole warp, one elected lane issues
+      constexpr uint32_t idS = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(KB >> 3) << 17) |
+                               (uint32_t(128 >> 4) << 24);
+      constexpr uint32_t idO = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(HD >> 3) << 17) |
+                               (uint32_t(128 >> 4) << 24);
+      const uint64_t dq = tca::desc(sQ);
+      auto issue_s = [&](int i) {  // S(i) -> TMEM buffer i % 2
+        tca::bar_wait_sleep(&k_full[i % KST], (i / KST) & 1);
+        tca::fence_after();
+        const uint64_t dk = tca::desc(sK + (i % KST) * K_BYTES);
+        const uint32_t dS = tmem + uint32_t((i & 1) * 128);
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tca::mma_ss_e(dS, dq + uint64_t((j * (128 * 128) + k * 32) >> 4),
+                          dk + uint64_t((j * (KB * 128) + k * 32) >> 4), idS, (j | k) != 0);
+        tca::commit_e(&s_full[i & 1]);
+        tca::commit_e(&k_empty[i % KST]);
+      };
+      tca::bar_wait_sleep(q_full, 0);
+      attn_ts(2);
+      issue_s(0);
+      if (nb > 1) issue_s(1);
+      for (int i = 0; i < nb; ++i) {
+        const int b = i & 1;
+        tca::bar_wait_sleep(&p_ready[b], (i >> 1) & 1);
+        tca::bar_wait_sleep(&v_full[i % VST], (i / VST) & 1);
+        tca::fence_after();
+        attn_tr(2, i, 0);
+        const uint64_t dv = tca::desc(sV + (i % VST) * V_BYTES);
+        const uint32_t dO = tmem + 256;
+        const uint32_t aP = tmem + uint32_t(b * 128);
+#pragma unroll
+        for (int k = 0; k < KB / 16; ++k)
+          tca::mma_ts_e(dO, aP + uint32_t(k * 8), dv + uint64_t(((k >> 2) * (HD * 128) + (k & 3) * 32) >> 4),
+                        idO, (i | k) != 0);
+        tca::commit_e(&pv_done[b]);
+        tca::commit_e(&v_empty[i % VST]);
+        if (i + 2 < nb) {  // buffer b holds P(i) until PV(i) has read it
+          tca::bar_wait_sleep(&pv_done[b], (i >> 1) & 1);
+          tca::fence_after();
+          issue_s(i + 2);
+        }
+        attn_tr(2, i, 1);
+      }
+      attn_ts(3);
+    }
+  } else if (warp < 8) {  // softmax: two warps per TMEM lane quadrant, one per 64-column half
+    const int hf = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
+    const int64_t qpos = p.pos0 + q0 + r;
+    const uint32_t tO = tmem + 256 + uint32_t(hf * (HD / 2)) + lane_off;
+    float* xrow = xs + (hf * 128 + r) * 2;
+    const float* xpart = xs + ((hf ^ 1) * 128 + r) * 2;
+    float m = -INFINITY, l = 0.f, mn = 0.f;
+    for (int i = 0; i < nb; ++i) {
+      const int b = i & 1;
+      const uint32_t tS = tmem + uint32_t(b * 128) + lane_off;
+      const int64_t k0 = int64_t(b0 + i) * KB + hf * 64;
+      const bool tr = (warp & 3) == 0 && lane == 0;
+      if (tr) attn_tr(hf, i, 0);
+      tca::bar_wait(&s_full[b], (i >> 1) & 1);
+      tca::fence_after();
+      if (tr) attn_tr(hf, i, 1);
+      uint32_t v[64];
+      tca::ld32_async(tS + uint32_t(hf * 64), v);
+      tca::ld32_async(tS + uint32_t(hf * 64 + 32), v + 32);
+      tca::ld_wait();
+      if (tr) attn_tr(hf, i, 2);
+      const int nv = int(imax64(0, imin64(64, min(qpos + 1, p.kv_total) - k0)));
+      if (__any_sync(0xffffffffu, nv < 64)) {
+#pragma unroll
+        for (int t = 0; t < 64; ++t) v[t] = t < nv ? v[t] : __float_as_uint(-INFINITY);
+      }
+      float mx;
+      {
+        float a8[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a8[t] = __uint_as_float(v[t]);
+#pragma unroll
+        for (int t = 8; t < 64; ++t) a8[t & 7] = fmaxf(a8[t & 7], __uint_as_float(v[t]));
+        mx = fmaxf(fmaxf(fmaxf(a8[0], a8[1]), fmaxf(a8[2], a8[3])), fmaxf(fmaxf(a8[4], a8[5]), fmaxf(a8[6], a8[7])));
+      }
+      // row max over both halves (the slot is rewritten only after this
+      // block's p_ready, which needs the partner's arrival too)
+      xrow[0] = mx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mx = fmaxf(mx, xpart[0]) * p.scale_log2;
+      float m_new = m;
+      if (mx > m + 8.f || m == -INFINITY) m_new = fmaxf(mx, m);
+      const float alpha = (m == -INFINITY || m_new == m) ? 1.f : ex2_approx(m - m_new);
+      if (i > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        // O (this half's columns) once PV(i-1) has landed
+        tca::bar_wait(&pv_done[b ^ 1], ((i - 1) >> 1) & 1);
+        tca::fence_after();
+        uint32_t o[32];
+#pragma unroll 1
+        for (int c = 0; c < HD / 64; ++c) {
+          tca::ld32(tO + uint32_t(c * 32), o);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * alpha);
+          tca::st32_async(tO + uint32_t(c * 32), o);
+        }
+        tca::st_wait();
+      }
+      const float mb = m_new == -INFINITY ? 0.f : m_new;
+      const bool do_mass = p.mass != nullptr;
+      const int ie = do_mass ? int(imax64(0, imin64(64, p.il - k0))) : 0;
+      const int rb = do_mass ? int(imax64(0, imin64(64, p.rs - k0))) : 64;
+      float sum = 0.f, msum = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e0 = ex2_approx(fmaf(__uint_as_float(v[2 * j]), p.scale_log2, -mb));
+        const float e1 = ex2_approx(fmaf(__uint_as_float(v[2 * j + 1]), p.scale_log2, -mb));
+        sum += e0 + e1;
+        if (do_mass) {
+          if (2 * j < ie || 2 * j >= rb) msum += e0;
+          if (2 * j + 1 < ie || 2 * j + 1 >= rb) msum += e1;
+        }
+        v[j] = pack2(e0, e1);
+      }
+      // P of this half's keys into columns [hf * 32, +32) of the buffer: both
+      // halves have read their S columns (the barrier above)
+      tca::st32_async(tS + uint32_t(hf * 32), v);
+      tca::st_wait();
+      if (tr) attn_tr(hf, i, 3);
+      l = l * alpha + sum;
+      mn = mn * alpha + msum;
+      m = m_new;
+      tca::fence_before();
+      tca::bar_arrive(&p_ready[b]);
+    }
+    if (nb > 0) {
+      tca::bar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+      tca::fence_after();
+    }
+    xrow[0] = l;
+    xrow[1] = mn;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    l += xpart[0];
+    mn += xpart[1];
+    if (threadIdx.x == 0) attn_ts(4);
+    const int64_t row = q0 + r;
+    const bool valid = row < p.rows;
+    uint32_t o[32];
+    if (nsplit == 1) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      bf16* dst = p.out + (row * p.H + h) * HD + hf * (HD / 2);
+#pragma unroll 1
+      for (int c = 0; c < HD / 64; ++c) {
+        tca::ld32(tO + uint32_t(c * 32), o);
+        if (!valid) continue;
+#pragma unroll
+        for (int t = 0; t < 32; t += 8) {
+          uint4 w;
+          w.x = pack2(__uint_as_float(o[t]) * inv, __uint_as_float(o[t + 1]) * inv);
+          w.y = pack2(__uint_as_float(o[t + 2]) * inv, __uint_as_float(o[t + 3]) * inv);
+          w.z = pack2(__uint_as_float(o[t + 4]) * inv, __uint_as_float(o[t + 5]) * inv);
+          w.w = pack2(__uint_as_float(o[t + 6]) * inv, __uint_as_float(o[t + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + t) = w;
+        }
+      }
+      if (valid && hf == 0 && p.mass) p.mass[int64_t(h) * p.rows + row] = l > 0.f ? double(mn) / double(l) : 0.0;
+      if (valid && hf == 0 && p.stats) {
+        p.stats[(int64_t(h) * p.rows + row) * 2] = m;
+        p.stats[(int64_t(h) * p.rows + row) * 2 + 1] = l;
+      }
+    } else {
+      float* dst = p.part + (int64_t(split) * p.H + h) * (HD + 3) * p.rows + row;
+#pragma unroll 1
+      for (int c = 0; c < HD / 64; ++c) {
+        if (nb > 0) tca::ld32(tO + uint32_t(c * 32), o);
+        if (!valid) continue;
+        const int d0 = hf * (HD / 2) + c * 32;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) dst[int64_t(d0 + t) * p.rows] = nb > 0 ? __uint_as_float(o[t]) : 0.f;
+      }
+      if (valid && hf == 0) {
+        dst[int64_t(HD) * p.rows] = m;
+        dst[int64_t(HD + 1) * p.rows] = l;
+        dst[int64_t(HD + 2) * p.rows] = mn;
+      }
+    }
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) attn_ts(5);
+  tca::fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tca::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+  if (threadIdx.x == 0) attn_ts(6);
+}
+
 // Split-KV merge for rows of split q tiles: weights 2^(m_s - M) (log2
 // domain); rows whose q tile ran as one item were written by the kernel.
 // Block = (32 rows, head, 32-dim slice), 4 warps, lane = row, warp = 8 dims.
@@ -675,6 +992,21 @@ void run_fa(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap&
   KB_LAUNCH();
 }
 
+template <int HD>
+void run_fa1(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+             const AttnTc& p) {
+  const size_t smem = 1024 + size_t(128) * HD * 2 + (3 + 2) * (size_t(kAttnKB) * HD * 2) + 256 +
+                      2 * kPgCache * sizeof(int) + 2 * 128 * 2 * sizeof(float);
+  auto kern = k_attn_fa1<HD>;
+  static bool attr = false;
+  if (!attr) {
+    KB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  KB_CUDA(launch_pdl(kern, grid, dim3(320), smem, s, tq, tk, tv, p));
+  KB_LAUNCH();
+}
+
 void attn_set_timeline(unsigned long long* d) { KB_CUDA(cudaMemcpyToSymbol(g_attn_ts, &d, sizeof d)); }
 int g_attn_target = 0;  // tuning knob (krul_debug_attn_bench): key blocks per work item
 int g_attn_dbg = 0;     // tuning knob (krul_debug_attn_bench): unused by the pipelined kernel
@@ -686,7 +1018,13 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   p.H = g.H;
   p.Hkv = g.Hkv;
   p.grp = g.H / g.Hkv;
-  p.hpc = (p.grp >= 2 && p.grp % 2 == 0) ? 2 : 1;  // head pairs only when they share a KV head
+  // kernel: one head per CTA with S double-buffered (default), or the
+  // head-pair kernel (KRUL_ATTN_V=2; pairs only when they share a KV head)
+  static const int variant = [] {
+    const char* v = std::getenv("KRUL_ATTN_V");
+    return v && v[0] == '2' ? 2 : 1;
+  }();
+  p.hpc = (variant == 2 && p.grp >= 2 && p.grp % 2 == 0) ? 2 : 1;
   p.rows = a.rows;
   p.pos0 = a.pos0;
   p.kv_total = a.pos0 + a.rows;
@@ -746,10 +1084,16 @@ void launch_attention_tc(const Ctx& c, cudaStream_t s, const Conv& conv, int lay
   const CUtensorMap tk = map2d(c.pool.p, pool_elems / HD, HD, HD, 64);
   const CUtensorMap tv = map2d(c.pool.p, pool_elems / 64, 64, 64, uint32_t(HD));
   const dim3 grid{unsigned(items), unsigned(units_y), 1u};
-  if (HD == 128)
+  if (variant == 1) {
+    if (HD == 128)
+      run_fa1<128>(s, grid, tq, tk, tv, p);
+    else
+      run_fa1<64>(s, grid, tq, tk, tv, p);
+  } else if (HD == 128) {
     run_fa<128>(s, grid, tq, tk, tv, p);
-  else
+  } else {
     run_fa<64>(s, grid, tq, tk, tv, p);
+  }
   if (max_split > 1) {
     const dim3 g2{unsigned((a.rows + 31) / 32), unsigned(g.H), unsigned(HD / 32)};
     if (HD == 128)
