@@ -390,6 +390,11 @@ int krul_set_concurrency(krul_ctx* ctx, int two_stream);
 /* Capture repeated restore DAGs into CUDA graphs (default on); off = every
  * restore is enqueued eagerly, as the first restore of a conversation is. */
 int krul_set_graphs(krul_ctx* ctx, int on);
+/* Diagnostics: device-side spans (first CTA entry -> last CTA exit,
+ * %globaltimer) of the weight-streaming GEMM launches of each restore, with
+ * no timing events in the streams; read after a restore. */
+int krul_span_enable(krul_ctx* ctx, int on);
+int krul_span_read(krul_ctx* ctx, int64_t* launches, double* ms, double* bytes);
 
 /* ---- measurement support (not on the reference's interface) ----------
  * krul_launch_count: number of kernels this library has launched (process

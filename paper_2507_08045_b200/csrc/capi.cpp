@@ -1499,6 +1499,46 @@ int krul_set_timeline(krul_ctx* ctx, int on) {
     ctx->c->timeline = on != 0;
   });
 }
+// Device-side spans of the weight-streaming GEMMs (M <= 128) of the next
+// restores: every launch stamps its first CTA entry and last CTA exit
+// (%globaltimer) into its slot; no events sit between the kernels.
+int krul_span_enable(krul_ctx* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaDeviceSynchronize());
+    c.drop_graph();
+    c.span_on = on != 0;
+    unsigned long long* d = nullptr;
+    if (c.span_on) d = static_cast<unsigned long long*>(c.span_buf.ensure(sizeof(unsigned long long) * 2 * Ctx::kSpanSlots));
+    gemm_set_span(d);
+  });
+}
+// Sum over the last restore's stamped launches: count, span ms, algorithmic bytes.
+int krul_span_read(krul_ctx* ctx, int64_t* launches, double* ms, double* bytes) {
+  return guard([&] {
+    need(ctx, "ctx");
+    Ctx& c = *ctx->c;
+    KB_CUDA(cudaSetDevice(c.device));
+    KB_CUDA(cudaDeviceSynchronize());
+    const int n = std::min<int>(c.span_next, Ctx::kSpanSlots);
+    std::vector<unsigned long long> h(size_t(2) * Ctx::kSpanSlots);
+    if (c.span_on && n > 0) KB_CUDA(cudaMemcpy(h.data(), c.span_buf.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    int64_t k = 0;
+    double t = 0, b = 0;
+    for (int i = 0; i < n; ++i) {
+      const unsigned long long a = h[size_t(i)], e = h[size_t(Ctx::kSpanSlots + i)];
+      if (a == ~0ull || e == 0 || e < a) continue;
+      ++k;
+      t += double(e - a) * 1e-6;
+      b += c.span_bytes[size_t(i)];
+    }
+    if (launches) *launches = k;
+    if (ms) *ms = t;
+    if (bytes) *bytes = b;
+  });
+}
 int krul_set_graphs(krul_ctx* ctx, int on) {
   return guard([&] {
     need(ctx, "ctx");

@@ -34,6 +34,18 @@ __device__ __forceinline__ void gemm_ts(int slot) {
   }
 }
 int g_gemm_splits = 0;  // debug: force the split-K count (0 = planner)
+__device__ unsigned long long* g_gemm_span = nullptr;  // [2][slots]: entry min, exit max
+__device__ __forceinline__ void gemm_span_stamp(int slot, bool exit_stamp) {
+  if (slot >= 0 && g_gemm_span) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (exit_stamp)
+      atomicMax(g_gemm_span + 4096 + slot, t);
+    else
+      atomicMin(g_gemm_span + slot, t);
+  }
+}
+void gemm_set_span(unsigned long long* d) { KB_CUDA(cudaMemcpyToSymbol(g_gemm_span, &d, sizeof d)); }
 
 // ---------------------------------------------------------------- epilogue
 template <class T>
@@ -650,6 +662,7 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 0) {
     gemm_ts(32 + blockIdx.x);
     if (blockIdx.x == 0) gemm_ts(0);
+    gemm_span_stamp(e.span, false);
   }
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -856,7 +869,10 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(uint32_t(2 * BN)));
   }
-  if (threadIdx.x == 0) gemm_ts(32 + 256 + blockIdx.x);
+  if (threadIdx.x == 0) {
+    gemm_ts(32 + 256 + blockIdx.x);
+    gemm_span_stamp(e.span, true);
+  }
 }
 
 // ---------------------------------------------------------------- 2-SM pair
@@ -1102,6 +1118,7 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
         epi_elem<T>(e, r, c + 3, a.w);
       }
     }
+    if (threadIdx.x == 0) gemm_span_stamp(e.span, true);  // the reduce ends the GEMM's span
     return;
   }
   const bool sw = e.kind == Epi::SWIGLU;
@@ -1126,6 +1143,7 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int64_t
       epi_elem<T>(e, r, c, a);
     }
   }
+  if (threadIdx.x == 0) gemm_span_stamp(e.span, true);
 }
 
 // Split-K partner of the fused QKV epilogue (weight-streaming shapes, small
@@ -1630,10 +1648,17 @@ void gemm(const Ctx& c, cudaStream_t s, int64_t M, int64_t N, int64_t K, const v
           int64_t lda, const void* B, int64_t ldb, const Epi& e) {
   if (M <= 0 || N <= 0) return;
   cudaEvent_t kt0 = kt_begin(c, s);
-  gemm_impl(c, s, M, N, K, A, lda, B, ldb, e);
   // M <= 128: a weight-streaming GEMM (HBM-bound: algorithmic bytes = weights
   // + activations in + out); larger M: tensor-bound (2MNK flops)
   const double bytes = double(N) * K * c.esz + double(M) * K * c.esz + double(M) * N * 4.0;
+  if (c.span_on && M <= 128 && c.span_next < Ctx::kSpanSlots) {
+    Epi es = e;
+    es.span = const_cast<Ctx&>(c).span_next++;
+    const_cast<Ctx&>(c).span_bytes.push_back(bytes);
+    gemm_impl(c, s, M, N, K, A, lda, B, ldb, es);
+  } else {
+    gemm_impl(c, s, M, N, K, A, lda, B, ldb, e);
+  }
   kt_end(c, s, kt0, M <= 128 ? KT_GEMM_STREAM : KT_GEMM, 2.0 * double(M) * double(N) * double(K), bytes);
 }
 

@@ -402,7 +402,8 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   const bool same = G.snap_serial == snap.serial && G.conv_serial == conv.serial && G.L == L && G.n_new == nn &&
                     G.kt_on == c.kt.on && G.logits == (lp != nullptr) &&
                     G.capture_probs == c.capture_probs && G.buf_gen == g_buf_gen.load() &&
-                    G.two_stream == c.two_stream && G.fused == c.fused && G.timeline == c.timeline;
+                    G.two_stream == c.two_stream && G.fused == c.fused && G.timeline == c.timeline &&
+                    G.span == c.span_on;
   if (!same) {
     c.drop_graph();
     G.snap_serial = snap.serial;
@@ -415,6 +416,7 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
     G.two_stream = c.two_stream;
     G.fused = c.fused;
     G.timeline = c.timeline;
+    G.span = c.span_on;
     G.ev.resize(size_t(5 + 3 * g.N));
     for (size_t i = 0; i < G.ev.size(); ++i) {
       auto& m = G.ev[i];
@@ -429,6 +431,11 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
   }();
   const bool graphs = c.use_graphs && graphs_env;
   const int32_t* tp_new = new_tok ? tp + nh : nullptr;
+  if (c.span_on) {  // fresh stamps for this restore: entry = max, exit = 0
+    unsigned long long* sp = static_cast<unsigned long long*>(c.span_buf.p);
+    KB_CUDA(cudaMemsetAsync(sp, 0xFF, sizeof(unsigned long long) * Ctx::kSpanSlots, c.s_comp));
+    KB_CUDA(cudaMemsetAsync(sp + Ctx::kSpanSlots, 0, sizeof(unsigned long long) * Ctx::kSpanSlots, c.s_comp));
+  }
   if (graphs && G.exec) {
     KB_CUDA(cudaGraphLaunch(G.exec, c.s_comp));
     g_launches.fetch_add(G.launches);
@@ -439,6 +446,8 @@ void restore(Ctx& c, Conv& conv, Snapshot& snap, const int32_t* hist, int64_t L,
       c.kt.next = 0;
     }
     c.reset_events();
+    c.span_next = 0;  // slots in enqueue order: identical on every replay
+    c.span_bytes.clear();
     if (graphs && G.seen >= 1) {
       const uint64_t l0 = g_launches.load();
       KB_CUDA(cudaStreamBeginCapture(c.s_comp, cudaStreamCaptureModeRelaxed));

@@ -241,6 +241,7 @@ struct Ctx {
     bool two_stream = true;
     bool fused = false;
     bool timeline = false;
+    bool span = false;
     int seen = 0;  // eager runs with this key (capture on the second)
     cudaGraphExec_t exec = nullptr;
     uint64_t launches = 0;
@@ -259,6 +260,13 @@ struct Ctx {
   // per-layer external event-record nodes runs the restore 4-7 ms slower
   // at r_c > 0 (the nodes keep the streams' kernels interleaved).
   bool timeline = true;
+  // device-side spans of the weight-streaming GEMM launches (no events in
+  // the stream: first-CTA entry to last-CTA exit per launch, krul_span_*)
+  bool span_on = false;
+  int span_next = 0;
+  std::vector<double> span_bytes;
+  DevBuf span_buf;
+  static constexpr int kSpanSlots = 4096;
   std::vector<double> tl_compute, tl_load, tl_new;
   double tl_h2d_ms = 0;
   std::vector<cudaEvent_t> ev_pool;
@@ -303,9 +311,13 @@ struct Epi {  // GEMM epilogue
   // 1-SM kernel then loads real (ignored) rows instead of TMA out-of-bounds
   // fill, measured 77 -> 55 us on the M = 1 FFN1 (layer workspaces hold 128)
   int64_t a_rows = 0;
+  // span slot of the weight-streaming GEMM launch (krul_span_enable): the
+  // kernel stamps its first CTA entry / last CTA exit (%globaltimer) there
+  int span = -1;
 };
 
-extern int g_gemm_force, g_gemm_splits;  // debug knobs (krul_debug_gemm_bench)
+extern int g_gemm_force, g_gemm_splits;
+void gemm_set_span(unsigned long long* d);  // [2][slots] entry (min) / exit (max) stamps  // debug knobs (krul_debug_gemm_bench)
 void gemm_set_timeline(unsigned long long* d);  // debug phase stamps (krul_debug_gemm_timeline)
 extern int g_attn_target, g_attn_dbg;    // debug knobs (krul_debug_attn_bench)
 void attn_set_timeline(unsigned long long* d);  // debug phase stamps (krul_debug_attn_timeline)

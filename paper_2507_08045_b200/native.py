@@ -335,6 +335,16 @@ class Context:
         """Record per-layer timeline events in the restore DAG (diagnostic)."""
         _check(lib().krul_set_timeline(self.h, int(bool(on))))
 
+    def span_enable(self, on: bool):
+        """Stamp device-side spans of the weight-streaming GEMMs of each restore."""
+        _check(lib().krul_span_enable(self.h, int(bool(on))))
+
+    def span_read(self):
+        """(launches, span ms, algorithmic bytes) of the last restore's stamped GEMMs."""
+        n, ms, by = C.c_int64(), C.c_double(), C.c_double()
+        _check(lib().krul_span_read(self.h, C.byref(n), C.byref(ms), C.byref(by)))
+        return n.value, ms.value, by.value
+
     def set_graphs(self, on: bool):
         """Graph-capture repeated restore DAGs (default) or enqueue every restore eagerly."""
         _check(lib().krul_set_graphs(self.h, int(bool(on))))

@@ -82,3 +82,32 @@ def test_restore_batch_rejects_same_conversation_twice(monkeypatch):
     c = ctx.conversation(640)
     with pytest.raises(K.ConfigError):
         ctx.restore_batch([c, c], [hist, hist], [snap, snap], [new, new])
+
+
+def test_gemm_spans_do_not_change_results():
+    """krul_span_enable (device-side GEMM spans): stamps every weight-streaming
+    GEMM launch of a restore, sane totals, identical logits with spans on/off."""
+    from paper_2507_08045_b200 import native as K
+
+    cfg = K.ModelConfig(**SHAPE, dtype=K.KRUL_BF16, max_tokens=640)
+    ctx = K.Context(cfg, 0)
+    ctx.init_weights(3)
+    rng = np.random.default_rng(9)
+    hist = rng.integers(0, cfg.vocab_size, 448, dtype=np.int32)
+    new = rng.integers(0, cfg.vocab_size, 64, dtype=np.int32)
+    src = ctx.conversation(640)
+    ctx.prefill(src, hist)
+    snap = K.KVSnapshot.compress(ctx, src, [(1, 3, 0.0)], K.build_plan(448, 4, 0.1, [(1, 3, 0.0)]), 448,
+                                 K.MERGE_MEAN)
+    conv = ctx.conversation(640)
+    want = None
+    for _ in range(3):
+        want, _, _ = ctx.restore_and_prefill(conv, hist, snap, new)
+    ctx.span_enable(True)
+    for _ in range(3):  # eager, capture, replay
+        got, _, _ = ctx.restore_and_prefill(conv, hist, snap, new)
+        assert np.array_equal(got, want)
+        n, ms, by = ctx.span_read()
+        # 4 GEMMs per layer of the new-input prefill (+ the pyramid's small-M layers)
+        assert n >= 4 * cfg.n_layers and ms > 0 and by > 0, (n, ms, by)
+    ctx.span_enable(False)
