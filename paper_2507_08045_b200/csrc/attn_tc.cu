@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* pv_done = p_ready + 2;    // [buffer]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
   int* pg_s = reinterpret_cast<int*>(tslot + 4);              // [2 * kPgCache]
-  float* xs = reinterpret_cast<float*>(pg_s + 2 * kPgCache);  // [half][128 rows][2]
+  float* xs = reinterpret_cast<float*>(pg_s + 2 * kPgCache);  // [block parity][half][128 rows][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) attn_ts(0);
@@ -746,8 +746,12 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
     const int64_t qpos = p.pos0 + q0 + r;
     const uint32_t tO = tmem + 256 + uint32_t(hf * (HD / 2)) + lane_off;
-    float* xrow = xs + (hf * 128 + r) * 2;
-    const float* xpart = xs + ((hf ^ 1) * 128 + r) * 2;
+    // row exchange slots, alternating with the block parity: with S double
+    // buffered a half may reach block i+1 before its partner has read the
+    // block-i slot, but not block i+2 (that needs the partner's arrival at
+    // block i+1's barrier)
+    auto xrow = [&](int i) { return xs + (((i & 1) * 2 + hf) * 128 + r) * 2; };
+    auto xpart = [&](int i) { return xs + (((i & 1) * 2 + (hf ^ 1)) * 128 + r) * 2; };
     float m = -INFINITY, l = 0.f, mn = 0.f;
     for (int i = 0; i < nb; ++i) {
       const int b = i & 1;
@@ -777,11 +781,10 @@ __global__ void __launch_bounds__(320, 1)
         for (int t = 8; t < 64; ++t) a8[t & 7] = fmaxf(a8[t & 7], __uint_as_float(v[t]));
         mx = fmaxf(fmaxf(fmaxf(a8[0], a8[1]), fmaxf(a8[2], a8[3])), fmaxf(fmaxf(a8[4], a8[5]), fmaxf(a8[6], a8[7])));
       }
-      // row max over both halves (the slot is rewritten only after this
-      // block's p_ready, which needs the partner's arrival too)
-      xrow[0] = mx;
+      // row max over both halves
+      xrow(i)[0] = mx;
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      mx = fmaxf(mx, xpart[0]) * p.scale_log2;
+      mx = fmaxf(mx, xpart(i)[0]) * p.scale_log2;
       float m_new = m;
       if (mx > m + 8.f || m == -INFINITY) m_new = fmaxf(mx, m);
       const float alpha = (m == -INFINITY || m_new == m) ? 1.f : ex2_approx(m - m_new);
@@ -830,11 +833,11 @@ __global__ void __launch_bounds__(320, 1)
       tca::bar_wait(&pv_done[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
       tca::fence_after();
     }
-    xrow[0] = l;
-    xrow[1] = mn;
+    xrow(nb)[0] = l;
+    xrow(nb)[1] = mn;
     asm volatile("bar.sync 1, 256;" ::: "memory");
-    l += xpart[0];
-    mn += xpart[1];
+    l += xpart(nb)[0];
+    mn += xpart(nb)[1];
     if (threadIdx.x == 0) attn_ts(4);
     const int64_t row = q0 + r;
     const bool valid = row < p.rows;
@@ -996,7 +999,7 @@ template <int HD>
 void run_fa1(cudaStream_t s, dim3 grid, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
              const AttnTc& p) {
   const size_t smem = 1024 + size_t(128) * HD * 2 + (3 + 2) * (size_t(kAttnKB) * HD * 2) + 256 +
-                      2 * kPgCache * sizeof(int) + 2 * 128 * 2 * sizeof(float);
+                      2 * kPgCache * sizeof(int) + 2 * 2 * 128 * 2 * sizeof(float);
   auto kern = k_attn_fa1<HD>;
   static bool attr = false;
   if (!attr) {
