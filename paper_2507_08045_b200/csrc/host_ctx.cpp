@@ -185,10 +185,24 @@ void Ctx::drop_graph() {
   rg = RestoreGraph{};
 }
 
+Ctx::BatchGraph::~BatchGraph() {
+  if (exec) cudaGraphExecDestroy(exec);
+  if (t0) cudaEventDestroy(t0);
+  if (t1) cudaEventDestroy(t1);
+  for (auto& m : ev)
+    if (m.dep) cudaEventDestroy(m.dep);
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
   drop_graph();
+  for (auto* b : bgraphs) delete b;
+  for (int i = 0; i < 2; ++i) {
+    for (auto e : {b_dec[i], b_comp[i], b_new[i], b_h2d[i]})
+      if (e) cudaEventDestroy(e);
+    if (b_launch[i]) cudaStreamDestroy(b_launch[i]);
+  }
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto s : {s_comp, s_load, s_new, s_est, s_exp})
     if (s) cudaStreamDestroy(s);

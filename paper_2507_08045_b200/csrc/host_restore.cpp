@@ -190,15 +190,22 @@ struct PipeItem {
   char* stg = nullptr;
   char* cstg = nullptr;
   float* logits_host = nullptr;  // pinned, may be null
+  // graph mode (the item's DAG captured once, launched on its own stream):
+  // the item's own dependency marks (no timing events, so the graph never
+  // refers to the ctx's restore-graph events) and the external hand-offs to
+  // the neighbouring items -- the previous item's recompute end (workspace
+  // set 0) and new-input prefill end (set 1)
+  const Mark* ev = nullptr;
+  cudaEvent_t wait_comp = nullptr, rec_comp = nullptr, wait_new = nullptr, rec_new = nullptr;
 };
 static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const int32_t* tp_hist,
                             const int32_t* tp_new, int64_t n_new, float* lp, double* h2d_out,
                             double* expand_out, const PipeItem* pipe = nullptr) {
   const Cfg& g = c.cfg;
   const std::vector<int64_t>& p = snap.p;
-  auto& E = c.rg.ev;
+  const Mark* E = pipe && pipe->ev ? pipe->ev : c.rg.ev.data();
   const Mark &ev0 = E[0], &ev_c_end = E[1], &ev_l_end = E[2], &ev_end = E[3], &ev_h2d_end = E[4];
-  const Mark* computed = E.data() + 5;
+  const Mark* computed = E + 5;
   const Mark* loaded = computed + g.N;
   const Mark* newp = loaded + g.N;
   cudaStream_t sc = c.s_comp, sl = c.s_load;
@@ -311,12 +318,14 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     return;
   }
   // ---- compute stream: K6 pyramid recompute
+  if (pipe && pipe->wait_comp) KB_CUDA(cudaStreamWaitEvent(sc, pipe->wait_comp, cudaEventWaitExternal));
   if (p[0] > 0) {
     enqueue_partial(c, sc, conv, d_tok, p, false, computed);
   } else {
     for (int l = 0; l < g.N; ++l) record_mark(computed[l], sc);
   }
   record_mark(ev_c_end, sc);
+  if (pipe && pipe->rec_comp) KB_CUDA(cudaEventRecordWithFlags(pipe->rec_comp, sc, cudaEventRecordExternal));
   // ---- new-input prefill (K7) on its own stream, layer l behind
   // computed[l] and loaded[l], so it tracks the load events while the
   // recompute runs (KRUL_TWO_STREAM=0: same stream, after the recompute).
@@ -328,6 +337,7 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
   if (has_new) {
     cudaStream_t sn = two_stream ? c.s_new : sc;
     if (two_stream) KB_CUDA(cudaStreamWaitEvent(sn, tok_ready, 0));
+    if (pipe && pipe->wait_new) KB_CUDA(cudaStreamWaitEvent(sn, pipe->wait_new, cudaEventWaitExternal));
     std::vector<cudaEvent_t> waits;
     for (int l = 0; l < g.N; ++l) waits.push_back(computed[l].dep);
     for (int l = 0; l < g.N; ++l) waits.push_back(loaded[l].dep);
@@ -336,6 +346,7 @@ static void enqueue_restore(Ctx& c, Conv& conv, Snapshot& snap, int64_t L, const
     if (pipe && pipe->logits_host)
       KB_CUDA(cudaMemcpyAsync(pipe->logits_host, d_logits, size_t(g.V) * 4, cudaMemcpyDeviceToHost, sn));
     record_mark(ev_end, sn);
+    if (pipe && pipe->rec_new) KB_CUDA(cudaEventRecordWithFlags(pipe->rec_new, sn, cudaEventRecordExternal));
     if (pipe) {  // no join: the next conversation's restore starts under this tail
       *h2d_out = h2d;
       *expand_out = expand_bytes;
@@ -601,6 +612,70 @@ void restore_batch(Ctx& c, int n, Conv* const* convs, Snapshot* const* snaps, co
     KB_CUDA(cudaEventCreateWithFlags(&done[size_t(i)], cudaEventDisableTiming));
   }
   cudaStream_t sl = c.s_load;
+  // graph mode: every item's DAG captured once (after an eager pipelined
+  // pass sized the workspaces) and replayed on alternating launch streams;
+  // the hand-offs between neighbours are external events: staging slot (the
+  // decode + expand of item i-2), recompute workspaces (item i-1's recompute
+  // end) and prefill workspaces (item i-1's prefill end)
+  static const bool graphs_env = [] {
+    const char* v = std::getenv("KRUL_BATCH_GRAPHS");
+    return !(v && v[0] == '0');
+  }();
+  const bool use_g = graphs_env && c.use_graphs;
+  std::vector<Ctx::BatchGraph*> bg(nn, nullptr);
+  bool all_cached = use_g;
+  if (use_g) {
+    for (int k = 0; k < 2; ++k) {
+      if (!c.b_launch[k]) KB_CUDA(cudaStreamCreateWithFlags(&c.b_launch[k], cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&c.b_dec[k], &c.b_comp[k], &c.b_new[k], &c.b_h2d[k]})
+        if (!*e) KB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    std::vector<Ctx::BatchGraph*> keep;
+    for (int i = 0; i < n; ++i) {
+      for (auto* x : c.bgraphs)
+        if (x->snap_serial == snaps[i]->serial && x->conv_serial == convs[i]->serial && x->L == Ls[i] &&
+            x->n_new == n_news[i] && x->slot == (i & 1) && x->buf_gen == g_buf_gen.load())
+          bg[size_t(i)] = x;
+      if (!bg[size_t(i)]) all_cached = false;
+    }
+    // drop cached graphs this batch does not use
+    for (auto* x : c.bgraphs) {
+      if (std::find(bg.begin(), bg.end(), x) != bg.end())
+        keep.push_back(x);
+      else
+        delete x;
+    }
+    c.bgraphs = keep;
+  }
+  if (all_cached) {
+    for (int i = 0; i < n; ++i) {
+      Ctx::BatchGraph& x = *bg[size_t(i)];
+      const int64_t nh = std::max<int64_t>(snaps[i]->p[0], 0);
+      int32_t* tq = static_cast<int32_t*>(x.tok.p);
+      if (nh) std::memcpy(tq, hists[i], size_t(nh) * 4);
+      std::memcpy(tq + nh, news[i], size_t(n_news[i]) * 4);
+      KB_CUDA(cudaGraphLaunch(x.exec, c.b_launch[i & 1]));
+      convs[i]->len = Ls[i] + n_news[i];
+    }
+    KB_CUDA(cudaDeviceSynchronize());
+    for (int i = 0; i < n; ++i) {
+      float ms = 0;
+      KB_CUDA(cudaEventElapsedTime(&ms, bg[size_t(i)]->t0, bg[size_t(i)]->t1));
+      if (ttft_ms) ttft_ms[i] = ms;
+      if (logits) std::memcpy(logits + size_t(i) * g.V, bg[size_t(i)]->logits.p, size_t(g.V) * 4);
+    }
+    float tot = 0;
+    KB_CUDA(cudaEventElapsedTime(&tot, bg[0]->t0, bg[size_t(n - 1)]->t1));
+    if (total_ms) *total_ms = tot;
+    for (int i = 0; i < n; ++i) {
+      cudaEventDestroy(t0[size_t(i)]);
+      cudaEventDestroy(t1[size_t(i)]);
+      cudaEventDestroy(done[size_t(i)]);
+    }
+    c.tl_pending = false;
+    c.kt.on = kt_was;
+    return;
+  }
   for (int i = 0; i < n; ++i) {
     const int slot = i & 1;
     if (i >= 2) KB_CUDA(cudaStreamWaitEvent(sl, done[size_t(i - 2)], 0));  // the slot's previous item decoded
@@ -641,6 +716,82 @@ void restore_batch(Ctx& c, int n, Conv* const* convs, Snapshot* const* snaps, co
     cudaEventDestroy(t0[size_t(i)]);
     cudaEventDestroy(t1[size_t(i)]);
     cudaEventDestroy(done[size_t(i)]);
+  }
+  // capture the items' graphs for the next call of this batch (the eager
+  // pass above sized every workspace)
+  if (use_g) {
+    for (int i = 0; i < n; ++i) {
+      if (bg[size_t(i)]) continue;
+      auto* x = new Ctx::BatchGraph;
+      c.bgraphs.push_back(x);
+      x->snap_serial = snaps[i]->serial;
+      x->conv_serial = convs[i]->serial;
+      x->L = Ls[i];
+      x->n_new = n_news[i];
+      x->slot = i & 1;
+      const int64_t nh = std::max<int64_t>(snaps[i]->p[0], 0);
+      x->tok.ensure(size_t(nh + n_news[i] + 1) * 4);
+      int32_t* dq = static_cast<int32_t*>(x->dtok.ensure(size_t(nh + n_news[i] + 1) * 4));
+      x->logits.ensure(size_t(g.V) * 4);
+      KB_CUDA(cudaEventCreate(&x->t0));
+      KB_CUDA(cudaEventCreate(&x->t1));
+      x->ev.resize(size_t(5 + 3 * g.N));
+      for (auto& m : x->ev) KB_CUDA(cudaEventCreateWithFlags(&m.dep, cudaEventDisableTiming));
+      const int slot = i & 1;
+      c.reset_events();
+      cudaStream_t sc = c.s_comp;
+      KB_CUDA(cudaStreamBeginCapture(sc, cudaStreamCaptureModeRelaxed));
+      try {
+        cudaEvent_t fork = c.event();
+        KB_CUDA(cudaEventRecord(fork, sc));
+        KB_CUDA(cudaStreamWaitEvent(sl, fork, 0));
+        KB_CUDA(cudaStreamWaitEvent(sl, c.b_dec[slot], cudaEventWaitExternal));
+        // the link carries one conversation at a time: copies after the
+        // previous item's (two copy streams would only share the link)
+        KB_CUDA(cudaStreamWaitEvent(sl, c.b_h2d[slot ^ 1], cudaEventWaitExternal));
+        KB_CUDA(record_timing(x->t0, sl));
+        KB_CUDA(cudaMemcpyAsync(dq, x->tok.p, size_t(nh + n_news[i]) * 4, cudaMemcpyHostToDevice, sl));
+        PipeItem it;
+        it.d_tok = dq;
+        it.d_new = dq + nh;
+        it.tok_ready = c.event();
+        KB_CUDA(cudaEventRecord(it.tok_ready, sl));
+        it.stg = stg_slot[slot];
+        it.cstg = cstg_slot[slot];
+        it.logits_host = static_cast<float*>(x->logits.p);
+        it.ev = x->ev.data();
+        it.wait_comp = c.b_comp[slot ^ 1];
+        it.rec_comp = c.b_comp[slot];
+        it.wait_new = c.b_new[slot ^ 1];
+        it.rec_new = c.b_new[slot];
+        double h2d = 0, eb = 0;
+        enqueue_restore(c, *convs[i], *snaps[i], Ls[i], nullptr, nullptr, n_news[i], nullptr, &h2d, &eb, &it);
+        KB_CUDA(cudaEventRecordWithFlags(c.b_dec[slot], c.s_exp, cudaEventRecordExternal));
+        KB_CUDA(cudaEventRecordWithFlags(c.b_h2d[slot], sl, cudaEventRecordExternal));
+        KB_CUDA(record_timing(x->t1, c.s_new));
+        for (cudaStream_t st : {sl, c.s_exp, c.s_new}) {  // join into the capture origin
+          cudaEvent_t j = c.event();
+          KB_CUDA(cudaEventRecord(j, st));
+          KB_CUDA(cudaStreamWaitEvent(sc, j, 0));
+        }
+      } catch (...) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(sc, &junk);
+        if (junk) cudaGraphDestroy(junk);
+        throw;
+      }
+      cudaGraph_t graph = nullptr;
+      KB_CUDA(cudaStreamEndCapture(sc, &graph));
+      const cudaError_t ie = cudaGraphInstantiate(&x->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        x->exec = nullptr;
+        fail(KRUL_E_CUDA, std::string("batch restore graph instantiation failed: ") + cudaGetErrorString(ie));
+      }
+    }
+    // the key's buffer generation once every new graph's own buffers exist
+    // (their allocations bump it too)
+    for (auto* x : c.bgraphs) x->buf_gen = g_buf_gen.load();
   }
   c.tl_pending = false;
   c.kt.on = kt_was;

@@ -227,6 +227,23 @@ struct Ctx {
   DevBuf staging;
   DevBuf cstaging;       // coded blob images (H2D target; decoded into `staging`)
   DevBuf staging2, cstaging2, batch_tok;  // restore_batch: the second staging slot, the batch's tokens
+  // restore_batch graph mode: one captured DAG per (snapshot, conversation,
+  // parity), launched on alternating streams with external-event hand-offs
+  struct BatchGraph {
+    uint64_t snap_serial = 0, conv_serial = 0, buf_gen = 0;
+    int64_t L = 0, n_new = 0;
+    int slot = 0;
+    cudaGraphExec_t exec = nullptr;
+    PinnedBuf tok, logits;
+    DevBuf dtok;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    std::vector<Mark> ev;  // dependency marks only (no timing events)
+    ~BatchGraph();
+  };
+  std::vector<BatchGraph*> bgraphs;
+  cudaEvent_t b_dec[2] = {nullptr, nullptr}, b_comp[2] = {nullptr, nullptr}, b_new[2] = {nullptr, nullptr},
+              b_h2d[2] = {nullptr, nullptr};
+  cudaStream_t b_launch[2] = {nullptr, nullptr};
   bool kv_coding = true; // exponent-code bf16 snapshots at compress (KRUL_KV_CODING=0: off)
   PinnedBuf tok_pin;     // pinned token staging (history | new input) for async / graph H2D
   PinnedBuf logits_pin;  // pinned logits landing buffer
