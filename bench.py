@@ -765,6 +765,13 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
     ms, by = est.fold_bench(20)
     hbm = PEAKS.get("hbm_gbs", 6547.2)
     gbs = by / (ms * 1e-3) / 1e9 if ms else None
+    # the fold's other roof: 2 f32 lane-ops (difference, square-accumulate)
+    # per pair, head and column on 128 f32 lanes / clk / SM (DESIGN.md §4 K1)
+    W = int(len(conv))
+    P = cfg.n_layers * (cfg.n_layers - 1) // 2
+    lane_ops = 2.0 * P * cfg.n_heads * W
+    fp32_peak = 128.0 * 148 * PEAKS.get("sm_max_mhz", 1965.0) * 1e6
+    fp32_frac = lane_ops / (ms * 1e-3) / fp32_peak if ms else None
     # finalize + selector (one CTA bitonic sort + greedy matching), timed on the host
     sums = est.sums()
     D = np.zeros((cfg.n_layers, cfg.n_layers))
@@ -779,9 +786,12 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
     for _ in range(reps):
         strat = K.select_strategy(ctx, D, layers, layers, 0.5, cfg.n_layers)
     sel_us = (time.perf_counter() - t0) / reps * 1e6
-    return {"fold": {"bound": "hbm", "kernel": "k_fold_direct (K1: f32 difference, FADD2/FFMA2) + k_fold_chunks",
+    return {"fold": {"bound": "hbm", "kernel": "k_fold_direct (K1: f32 difference, FADD2/FFMA2; one launch)",
                      "achieved": round(gbs, 1) if gbs else None, "unit": "GB/s", "peak": hbm,
                      "frac": round(gbs / hbm, 4) if gbs else None, "launches": n,
+                     "fp32_lane_ops": lane_ops, "fp32_peak_lane_ops_per_s": fp32_peak,
+                     "fp32_frac": round(fp32_frac, 4) if fp32_frac else None,
+                     "floor_us": round(1e6 * max(by / (hbm * 1e9), lane_ops / fp32_peak), 2),
                      "us_per_fold": round(1e3 * ms, 2),
                      "us_per_fold_incl_launch_gap": round(1e3 * ms_ev / max(n, 1), 2),
                      "width": int(len(conv)), "tracked_layers": cfg.n_layers},

@@ -412,13 +412,22 @@ int krul_ktime_roofline(krul_ctx* ctx, int tag, double peak_tflops, double peak_
                         double* ideal_ms);
 
 /* Device time of one decode fold (K1) on the last captured decode rows,
- * `iters` back to back into a scratch accumulator (estimator state untouched). */
+ * `iters` back to back in one captured graph, into scratch segment slots
+ * (estimator state untouched). */
 int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* bytes_per_fold);
 
 /* Kernel-tuning aid: times `iters` tcgen05 attention launches over conv's pages. */
 int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0,
                           int dbg, int target, int iters, float* ms_per_iter);
 /* Kernel-tuning aid: %globaltimer phase stamps of one attention launch, ts[cta * 8 + slot]. */
+// Debug: per-CTA %globaltimer stamps of the K1 decode fold ([cta][8]: entry,
+// setup done, chunk loop done; [7] = the SM id). on = 1 arms, on = 0
+// copies n_ts stamps into ts and disarms.
+int krul_debug_fold_timeline(int on, unsigned long long* ts, int64_t n_ts);
+// Debug: refold the rows of the last krul_est_fold_decode_host iters times
+// back to back on the device (one captured graph) -> ms per fold (the sums
+// keep accumulating).
+int krul_debug_fold_repeat(krul_est* est, int iters, float* ms_per_fold);
 int krul_debug_attn_timeline(krul_ctx* ctx, krul_conv* conv, int layer, int64_t rows, int64_t pos0, int target,
                              unsigned long long* ts, int64_t n_ts);
 /* Kernel-tuning aid: times `iters` device-resident bf16 GEMMs (not a product entry). */

@@ -40,9 +40,13 @@ struct Est {
   std::vector<int> layers;
   int H = 1;
   DevBuf d_layers, sums, partial, D, tmp, ident;
+  DevBuf seg;  // K1 decode fold: resident per-(head, segment, pair) f64 slots [H][seg_S][P]
+  int seg_S = 0;
   int64_t partial_cap = 0;
   bool prefill_done = false;
   int64_t prefill_rows = 0, decode_steps = 0;
+  int64_t host_W = 0, host_pitch = 0;  // rows of the last krul_est_fold_decode_host (in tmp)
+  int host_N = 0;
   int P() const { return int(layers.size() * (layers.size() - 1) / 2); }
 };
 }  // namespace kb
@@ -84,6 +88,11 @@ void ensure_partial(Est& e, int64_t chunks) {
     e.partial.ensure(size_t(need_n) * 8);
     e.partial_cap = need_n;
   }
+}
+// the K1 decode fold's resident segment slots -> sums (stream-ordered on s_est)
+void collect_segments(Est& e) {
+  launch_fold_collect(e.ctx->s_est, e.seg.as<double>(), e.seg_S, int(e.layers.size()), e.H, e.sums.as<double>());
+  KB_CUDA(cudaStreamSynchronize(e.ctx->s_est));
 }
 }  // namespace
 
@@ -338,6 +347,10 @@ int krul_est_create(krul_ctx* ctx, const int* ir, int n, krul_est** out) {
     const size_t ns = size_t(std::max(e->P(), 1)) * e->H;
     e->sums.ensure(ns * 8);
     KB_CUDA(kb_memset_sync(e->sums.p, 0, ns * 8));
+    e->seg_S = fold_seg_slots(e->H, ctx->c->sm_count > 0 ? ctx->c->sm_count : 148);
+    const size_t nseg = size_t(e->seg_S) * ns;
+    e->seg.ensure(nseg * 8);
+    KB_CUDA(kb_memset_sync(e->seg.p, 0, nseg * 8));
     *out = new krul_est{e};
   });
 }
@@ -369,14 +382,9 @@ static void fold_decode_dev(Est& e, const float* rows, int64_t W, int64_t pitch,
   Ctx& c = *e.ctx;
   const int n = int(e.layers.size());
   const int sms = c.sm_count > 0 ? c.sm_count : 148;
-  const int64_t need_p = fold_direct_partial_elems(std::max(n, 2), W, e.H, sms);
-  if (need_p > e.partial_cap) {
-    e.partial.ensure(size_t(need_p) * 8);
-    e.partial_cap = need_p;
-  }
   cudaEvent_t kt0 = kt_begin(c, c.s_est);
   launch_fold_direct(c.s_est, rows, int64_t(e.H) * pitch, pitch, W, e.H, e.d_layers.as<int>(), n,
-                     e.sums.as<double>(), e.partial.as<double>(), e.partial_cap, sms);
+                     e.seg.as<double>(), e.seg_S, sms);
   // algorithmic bytes: tracked rows read once + f64 accumulator RMW
   kt_end(c, c.s_est, kt0, KT_FOLD_DECODE, 0.0,
          double(e.layers.size()) * e.H * double(W) * 4.0 + double(e.P()) * e.H * 16.0);
@@ -408,16 +416,11 @@ static void fold_prefill_recompute(Est& e, Ctx& c) {
     for (int i = 0; i < n; ++i) ident[size_t(i)] = i;
     int* d_ident = static_cast<int*>(e.ident.ensure(size_t(n) * 4));
     KB_CUDA(kb_memcpy_sync(d_ident, ident.data(), size_t(n) * 4, cudaMemcpyHostToDevice));
-    const int64_t need_p = fold_direct_partial_elems(n, rows * wc, H, sms);
-    if (need_p > e.partial_cap) {
-      e.partial.ensure(size_t(need_p) * 8);
-      e.partial_cap = need_p;
-    }
     cudaEvent_t kt0 = kt_begin(c, c.s_est);
     for (int64_t c0 = 0; c0 < W; c0 += wc) {
       launch_prefill_probs(c, c.s_est, *conv, e.d_layers.as<int>(), n, rows, first_q, c0, int(wc), P);
       launch_fold_direct(c.s_est, P, int64_t(H) * rows * wc, rows * wc, rows * wc, H, d_ident, n,
-                         e.sums.as<double>(), e.partial.as<double>(), e.partial_cap, sms);
+                         e.seg.as<double>(), e.seg_S, sms);
     }
     kt_end(c, c.s_est, kt0, KT_FOLD_PREFILL, 0.0, double(n) * H * double(rows) * double(W) * 4.0);
     KB_CUDA(cudaStreamSynchronize(c.s_est));
@@ -481,6 +484,53 @@ int krul_est_fold_decode_host(krul_est* est, const float* rows, int N, int64_t W
     // non-blocking stream that does not order against the legacy stream
     KB_CUDA(cudaDeviceSynchronize());
     fold_decode_dev(e, d, W, pitch, N);
+    e.host_W = W;
+    e.host_pitch = pitch;
+    e.host_N = N;
+  });
+}
+// Debug: refold the rows of the last krul_est_fold_decode_host iters times
+// back to back (device-resident, CUDA events) -> ms per fold. The sums keep
+// accumulating: diagnostics only.
+int krul_debug_fold_repeat(krul_est* est, int iters, float* ms_per_fold) {
+  return guard([&] {
+    need(est, "est");
+    need(ms_per_fold, "ms_per_fold");
+    Est& e = *est->e;
+    Ctx& c = *e.ctx;
+    if (e.host_W <= 0) fail(KRUL_E_STATE_CORRUPTION, "no host rows folded yet");
+    KB_CUDA(cudaSetDevice(c.device));
+    const int n = int(e.layers.size());
+    const int sms = c.sm_count > 0 ? c.sm_count : 148;
+    const float* rows = e.tmp.as<float>();
+    iters = std::max(iters, 1);
+    // the folds captured as one graph: launch-gap free, like the restore DAG
+    launch_fold_direct(c.s_est, rows, int64_t(e.H) * e.host_pitch, e.host_pitch, e.host_W, e.H,
+                       e.d_layers.as<int>(), n, e.seg.as<double>(), e.seg_S, sms);  // warm (attributes)
+    KB_CUDA(cudaStreamSynchronize(c.s_est));
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    KB_CUDA(cudaStreamBeginCapture(c.s_est, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i)
+      launch_fold_direct(c.s_est, rows, int64_t(e.H) * e.host_pitch, e.host_pitch, e.host_W, e.H,
+                         e.d_layers.as<int>(), n, e.seg.as<double>(), e.seg_S, sms);
+    KB_CUDA(cudaStreamEndCapture(c.s_est, &g));
+    KB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaEvent_t a, b;
+    KB_CUDA(cudaEventCreate(&a));
+    KB_CUDA(cudaEventCreate(&b));
+    KB_CUDA(cudaGraphLaunch(ge, c.s_est));
+    KB_CUDA(cudaEventRecord(a, c.s_est));
+    KB_CUDA(cudaGraphLaunch(ge, c.s_est));
+    KB_CUDA(cudaEventRecord(b, c.s_est));
+    KB_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    KB_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    *ms_per_fold = ms / float(std::max(iters, 1));
   });
 }
 int krul_est_sums(krul_est* est, double* sums) {
@@ -488,6 +538,7 @@ int krul_est_sums(krul_est* est, double* sums) {
     need(est, "est");
     Est& e = *est->e;
     KB_CUDA(cudaSetDevice(e.ctx->device));
+    collect_segments(e);
     if (e.P() > 0) KB_CUDA(kb_memcpy_sync(sums, e.sums.p, size_t(e.P()) * e.H * 8, cudaMemcpyDeviceToHost));
   });
 }
@@ -500,6 +551,7 @@ int krul_est_finalize(krul_est* est, double* D) {
     if (n == 0) return;
     KB_CUDA(cudaSetDevice(e.ctx->device));
     double* dD = static_cast<double*>(e.D.ensure(size_t(n) * n * 8));
+    collect_segments(e);
     launch_finalize(e.ctx->s_est, e.sums.as<double>(), n, e.H, dD);
     KB_CUDA(cudaStreamSynchronize(e.ctx->s_est));
     KB_CUDA(kb_memcpy_sync(D, dD, size_t(n) * n * 8, cudaMemcpyDeviceToHost));
@@ -1460,35 +1512,64 @@ int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* by
     const int64_t W = c.dec_width, pitch = c.dec_pitch;
     const int n = int(e.layers.size());
     const int sms = c.sm_count > 0 ? c.sm_count : 148;
-    const int64_t need_p = fold_direct_partial_elems(std::max(n, 2), W, e.H, sms);
-    if (need_p > e.partial_cap) {
-      e.partial.ensure(size_t(need_p) * 8);
-      e.partial_cap = need_p;
-    }
-    DevBuf scratch;
-    double* sums = static_cast<double*>(scratch.ensure(size_t(std::max(e.P(), 1)) * e.H * 8));
+    DevBuf scratch;  // the bench folds into scratch slots: the estimator's sums stay untouched
+    const size_t nseg = size_t(e.seg_S) * std::max(e.P(), 1) * e.H;
+    double* seg = static_cast<double*>(scratch.ensure(nseg * 8));
+    KB_CUDA(kb_memset_sync(seg, 0, nseg * 8));
     const float* rows = c.dec_rows.as<float>();
     auto fold = [&] {
-      launch_fold_direct(c.s_est, rows, int64_t(e.H) * pitch, pitch, W, e.H, e.d_layers.as<int>(), n, sums,
-                         e.partial.as<double>(), e.partial_cap, sms);
+      launch_fold_direct(c.s_est, rows, int64_t(e.H) * pitch, pitch, W, e.H, e.d_layers.as<int>(), n, seg,
+                         e.seg_S, sms);
     };
     fold();  // warm
+    KB_CUDA(cudaStreamSynchronize(c.s_est));
+    // the folds as one captured graph (as in a captured decode loop): device
+    // time without host launch gaps
+    iters = std::max(iters, 1);
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    KB_CUDA(cudaStreamBeginCapture(c.s_est, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) fold();
+    KB_CUDA(cudaStreamEndCapture(c.s_est, &g));
+    KB_CUDA(cudaGraphInstantiate(&ge, g, 0));
     cudaEvent_t a, b;
     KB_CUDA(cudaEventCreate(&a));
     KB_CUDA(cudaEventCreate(&b));
+    KB_CUDA(cudaGraphLaunch(ge, c.s_est));
     KB_CUDA(cudaEventRecord(a, c.s_est));
-    for (int i = 0; i < iters; ++i) fold();
+    KB_CUDA(cudaGraphLaunch(ge, c.s_est));
     KB_CUDA(cudaEventRecord(b, c.s_est));
     KB_CUDA(cudaEventSynchronize(b));
     float ms = 0;
     KB_CUDA(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
     *ms_per_fold = ms / float(std::max(iters, 1));
     *bytes_per_fold = double(e.layers.size()) * e.H * double(W) * 4.0 + double(e.P()) * e.H * 16.0;
   });
 }
 
+// Debug: per-CTA %globaltimer stamps of the next decode folds ([cta][8] u64:
+// entry, after setup, after the chunk loop; [7] = SM id; a CTA with an
+// empty range stamps only entry). on = 1 arms a device
+// buffer, on = 0 copies it into ts (n_ts entries) and disarms.
+int krul_debug_fold_timeline(int on, unsigned long long* ts, int64_t n_ts) {
+  return guard([&] {
+    static DevBuf buf;
+    if (on) {
+      buf.ensure(size_t(std::max<int64_t>(n_ts, 8)) * 8);
+      KB_CUDA(cudaMemset(buf.p, 0, size_t(std::max<int64_t>(n_ts, 8)) * 8));
+      fold_set_timeline(static_cast<unsigned long long*>(buf.p));
+    } else {
+      need(ts, "ts");
+      KB_CUDA(cudaDeviceSynchronize());
+      KB_CUDA(cudaMemcpy(ts, buf.p, size_t(n_ts) * 8, cudaMemcpyDeviceToHost));
+      fold_set_timeline(nullptr);
+    }
+  });
+}
 
 // Restore scheduling mode: 1 (default) runs the new-input prefill on its own
 // stream, concurrent with the recompute; 0 serialises it behind the

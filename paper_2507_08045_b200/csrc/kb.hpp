@@ -422,10 +422,15 @@ void launch_finalize(cudaStream_t s, const double* sums, int n, int H, double* D
 void launch_prefill_probs(const Ctx& c, cudaStream_t s, const Conv& conv, const int* d_layers, int n,
                           int64_t rows, int64_t first_q, int64_t c0, int wc, float* out);
 // K1 decode fold (fold.cu): rows [layer][head][.] f32 with 16-byte aligned
-// strides; part = per-(chunk, pair, head) f64 scratch
-int64_t fold_direct_partial_elems(int n, int64_t W, int H, int sms);
+// strides (head stride >= the 16-byte-padded width); adds into seg, the
+// resident per-(head, segment, pair) f64 slots ([H][seg_S][P], zero at
+// creation, seg_S = fold_seg_slots(H, sms)); launch_fold_collect moves the
+// slots into sums[p][h] and zeroes them.
+int fold_seg_slots(int H, int sms);
+void fold_set_timeline(unsigned long long* d);  // debug: per-CTA %globaltimer stamps [cta][8]
 void launch_fold_direct(cudaStream_t s, const float* rows, int64_t layer_stride, int64_t head_stride, int64_t W,
-                        int H, const int* d_layers, int n, double* sums, double* part, int64_t part_cap, int sms);
+                        int H, const int* d_layers, int n, double* seg, int seg_S, int sms);
+void launch_fold_collect(cudaStream_t s, double* seg, int seg_S, int n, int H, double* sums);
 // selector: candidates sorted on device then greedily matched
 void launch_select(cudaStream_t s, const double* cand_d, const int* cand_i, const int* cand_j,
                    int n_cand, int quota, int* out_i, int* out_j, double* out_d, int* out_n);

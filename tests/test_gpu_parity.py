@@ -271,6 +271,27 @@ def test_estimator_folds_match_oracle(K, oracle):
         e2.finish()
 
 
+@pytest.mark.parametrize("n,H,W", [(40, 5, 3001), (80, 2, 515), (12, 200, 64), (32, 32, 8328), (2, 1, 3)])
+def test_estimator_decode_fold_shapes(K, oracle, n, H, W):
+    """K1 decode fold layouts: > 32 tracked layers (several unit rounds per
+    CTA), several heads per CTA, a CTA range crossing heads, row ends inside
+    a 64-column block and inside a 16-byte unit, the Llama-3-8B 8K shape."""
+    cfg = K.ModelConfig(n_layers=n, n_heads=H, head_dim=4, d_model=4 * H, vocab_size=5,
+                        dtype=K.KRUL_F32, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(n + H)
+    tracked = list(range(n))
+    est = K.StreamingEstimator(ctx, tracked)
+    acc = oracle.Accumulator(tracked, H)
+    for t in range(2):
+        rows = rng.dirichlet(np.ones(W + t), (n, H)).astype(np.float32)
+        est.fold_decode_rows(rows)
+        acc.fold_decode(rows)
+    got, want = est.sums(), acc.sums()
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() < 1e-6, (rel.max(), int(rel.argmax()), got[rel.argmax()], want[rel.argmax()])
+
+
 def test_estimator_on_engine_capture(K, oracle):
     kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
     ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)
