@@ -421,8 +421,8 @@ int krul_debug_attn_bench(krul_ctx* ctx, krul_conv* conv, int layer, int64_t row
                           int dbg, int target, int iters, float* ms_per_iter);
 /* Kernel-tuning aid: %globaltimer phase stamps of one attention launch, ts[cta * 8 + slot]. */
 // Debug: per-CTA %globaltimer stamps of the K1 decode fold ([cta][8]: entry,
-// setup done, chunk loop done; [7] = the SM id). on = 1 arms, on = 0
-// copies n_ts stamps into ts and disarms.
+// setup done, chunk loop done, chunks 0-3 in shared memory; [7] = the SM
+// id). on = 1 arms, on = 0 copies n_ts stamps into ts and disarms.
 int krul_debug_fold_timeline(int on, unsigned long long* ts, int64_t n_ts);
 // Debug: refold the rows of the last krul_est_fold_decode_host iters times
 // back to back on the device (one captured graph) -> ms per fold (the sums

@@ -473,7 +473,11 @@ int krul_est_fold_decode_host(krul_est* est, const float* rows, int N, int64_t W
     need(rows, "rows");
     Est& e = *est->e;
     KB_CUDA(cudaSetDevice(e.ctx->device));
-    const int64_t pitch = (W + 3) / 4 * 4;
+    static const int64_t pad = [] {  // diagnostics: extra row pitch (floats, multiple of 4)
+      const char* v = std::getenv("KRUL_FOLD_ROW_PAD");
+      return v ? int64_t(std::atoi(v)) / 4 * 4 : int64_t(0);
+    }();
+    const int64_t pitch = (W + 3) / 4 * 4 + pad;
     const size_t n = size_t(N) * e.H * size_t(pitch);
     float* d = static_cast<float*>(e.tmp.ensure(std::max<size_t>(n, 1) * 4));
     KB_CUDA(cudaDeviceSynchronize());
@@ -604,28 +608,35 @@ int krul_select(krul_ctx* ctx, const double* D, const int* dm_layers, int n, con
     Ctx& c = *ctx->c;
     KB_CUDA(cudaSetDevice(c.device));
     const int nc = int(cd.size());
-    DevBuf buf;
-    char* p = static_cast<char*>(buf.ensure(size_t(nc) * 16 + size_t(nc) * 16 + 64));
+    // one block each way: [d nc f64][i nc][j nc] in, [d nc f64][i nc][j nc][n] out,
+    // staged through ctx-owned pinned / device buffers (grown once)
+    const size_t in_b = size_t(nc) * 16, out_b = size_t(nc) * 16 + 16;
+    char* h = static_cast<char*>(c.sel_host.ensure(in_b + out_b));
+    char* p = static_cast<char*>(c.sel_dev.ensure(in_b + out_b));
+    std::memcpy(h, cd.data(), size_t(nc) * 8);
+    std::memcpy(h + size_t(nc) * 8, ci.data(), size_t(nc) * 4);
+    std::memcpy(h + size_t(nc) * 12, cj.data(), size_t(nc) * 4);
     double* d_cd = reinterpret_cast<double*>(p);
     int* d_ci = reinterpret_cast<int*>(d_cd + nc);
     int* d_cj = d_ci + nc;
-    double* d_od = reinterpret_cast<double*>(d_cj + nc);
+    double* d_od = reinterpret_cast<double*>(p + in_b);
     int* d_oi = reinterpret_cast<int*>(d_od + nc);
     int* d_oj = d_oi + nc;
     int* d_on = d_oj + nc;
-    KB_CUDA(kb_memcpy_sync(d_cd, cd.data(), size_t(nc) * 8, cudaMemcpyHostToDevice));
-    KB_CUDA(kb_memcpy_sync(d_ci, ci.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
-    KB_CUDA(kb_memcpy_sync(d_cj, cj.data(), size_t(nc) * 4, cudaMemcpyHostToDevice));
+    KB_CUDA(cudaMemcpyAsync(p, h, in_b, cudaMemcpyHostToDevice, c.s_est));
     launch_select(c.s_est, d_cd, d_ci, d_cj, nc, q, d_oi, d_oj, d_od, d_on);
+    KB_CUDA(cudaMemcpyAsync(h + in_b, p + in_b, out_b, cudaMemcpyDeviceToHost, c.s_est));
     KB_CUDA(cudaStreamSynchronize(c.s_est));
+    const char* o = h + in_b;
     int np = 0;
-    KB_CUDA(kb_memcpy_sync(&np, d_on, 4, cudaMemcpyDeviceToHost));
-    std::vector<int> oi(size_t(std::max(np, 1))), oj(oi.size());
-    std::vector<double> od(oi.size());
+    std::memcpy(&np, o + size_t(nc) * 16, 4);
+    if (np < 0 || np > nc) fail(KRUL_E_CUDA, "selector returned a bad pair count");
+    std::vector<double> od(size_t(std::max(np, 1)));
+    std::vector<int> oi(od.size()), oj(od.size());
     if (np) {
-      KB_CUDA(kb_memcpy_sync(oi.data(), d_oi, size_t(np) * 4, cudaMemcpyDeviceToHost));
-      KB_CUDA(kb_memcpy_sync(oj.data(), d_oj, size_t(np) * 4, cudaMemcpyDeviceToHost));
-      KB_CUDA(kb_memcpy_sync(od.data(), d_od, size_t(np) * 8, cudaMemcpyDeviceToHost));
+      std::memcpy(od.data(), o, size_t(np) * 8);
+      std::memcpy(oi.data(), o + size_t(nc) * 8, size_t(np) * 4);
+      std::memcpy(oj.data(), o + size_t(nc) * 12, size_t(np) * 4);
     }
     for (int k = 0; k < np; ++k) out[k] = krul_pair{oi[size_t(k)], oj[size_t(k)], od[size_t(k)]};
     *n_out = np;
@@ -1552,8 +1563,8 @@ int krul_est_fold_bench(krul_est* est, int iters, float* ms_per_fold, double* by
 }
 
 // Debug: per-CTA %globaltimer stamps of the next decode folds ([cta][8] u64:
-// entry, after setup, after the chunk loop; [7] = SM id; a CTA with an
-// empty range stamps only entry). on = 1 arms a device
+// entry, after setup, after the chunk loop, chunks 0-3 in shared memory;
+// [7] = SM id; a CTA with an empty range stamps only entry). on = 1 arms a device
 // buffer, on = 0 copies it into ts (n_ts entries) and disarms.
 int krul_debug_fold_timeline(int on, unsigned long long* ts, int64_t n_ts) {
   return guard([&] {

@@ -34,6 +34,7 @@ __device__ __forceinline__ uint32_t fold_smem_u32(const void* p) {
 }
 
 constexpr int kFoldWarps = 16;
+constexpr int kFoldStages = 3;
 constexpr int kFoldMaxUnits = 112;  // 8-layer blocks squared: <= 80 tracked layers (100 units)
 constexpr int kFoldMaxLayers = 80;
 
@@ -50,7 +51,8 @@ struct FoldDeal {
 };
 
 // Debug timeline (krul_debug_fold_timeline): per CTA, %globaltimer at
-// entry (0), after setup (1), after the chunk loop (2); slot 7 = %smid.
+// entry (0), after setup (1), after the chunk loop (2), when thread 0 has
+// chunk k (< 4) in shared memory (3 + k); slot 7 = %smid.
 __device__ unsigned long long* g_fold_ts = nullptr;
 __device__ __forceinline__ void fold_ts(int slot) {
   if (g_fold_ts && threadIdx.x == 0) {
@@ -179,11 +181,11 @@ struct FoldIt {
 // full mbarrier per stage; the last warp to finish a stage (a shared
 // counter) issues its refill, so no warp waits on another. Columns past W
 // are masked in the fold. Padded layers (n..n8) are zero rows written once.
-template <int PITCH, int kFoldStages>
+template <int PITCH>
 __global__ void __launch_bounds__(kFoldWarps * 32, 1)
     k_fold_direct(const float* __restrict__ rows, int64_t layer_stride, int64_t head_stride, int64_t W, int H,
                   const int* __restrict__ layers, int n, const __grid_constant__ FoldDeal deal,
-                  double* __restrict__ seg_acc, int seg_S, int pre, int dbg) {
+                  double* __restrict__ seg_acc, int seg_S, int dbg) {
   extern __shared__ __align__(128) float fbuf[];  // [kFoldStages][n8][PITCH]
   __shared__ __align__(8) uint64_t full[kFoldStages];
   __shared__ unsigned s_done[kFoldStages];  // warps done with the stage's current chunk
@@ -261,10 +263,8 @@ __global__ void __launch_bounds__(kFoldWarps * 32, 1)
   }();
   fold_ts(1);
   FoldIt ip{g0, h0, b0, 0};  // position of chunk k + kFoldStages (every warp tracks it)
-  FoldIt dp = ip;            // the first chunk issued late (see below)
   for (int k = 0; k < kFoldStages && k < nchunks; ++k) {
-    if (k == pre) dp = ip;
-    if (warp == 0 && k < pre) produce(ip, k);
+    if (warp == 0) produce(ip, k);
     advance(ip, len_of(ip));
   }
   float2 acc[32];
@@ -284,13 +284,10 @@ __global__ void __launch_bounds__(kFoldWarps * 32, 1)
     const int valid = cl < int64_t(len) * 64 ? int(cl) : len * 64;
     fold_mbar_wait(&full[st], ph);
     if (k < 4) fold_ts(3 + k);
-    if (k == 0 && warp == 0)  // chunks pre.. go out once chunk 0 is in: every CTA's first chunk lands first
-      for (int j = pre; j < kFoldStages && j < nchunks; ++j) {
-        produce(dp, j);
-        advance(dp, len_of(dp));
-      }
     const float* buf = fbuf + st * stage_elems;
     if (dbg & 1) {
+    } else if (dbg & 32) {  // diagnostics: same FP work, broadcast shared loads (one wavefront each)
+      fold_unit<kUnitOff, PITCH>(buf, valid, 0, 0, 0, acc);
     } else if (type == kUnitOff)
       fold_unit<kUnitOff, PITCH>(buf, valid, ra, rb, lane, acc);
     else if (type == kUnitDiag)
@@ -358,20 +355,17 @@ __global__ void k_fold_collect(double* __restrict__ seg, int S, int P, int H, do
   sums[int64_t(p) * H + h] += acc;
 }
 
-// Chunk width: kFoldStages stages of n8 rows in <= ~200 KB of shared
-// memory, at most 256 columns (KRUL_FOLD_PITCH=512/256/128 overrides).
 static int fold_env(const char* name) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : 0;
 }
-static int fold_stages() {
-  static const int st = fold_env("KRUL_FOLD_STAGES") == 4 ? 4 : 3;
-  return st;
-}
+// Chunk width: 512 columns (2 KB per row and bulk copy; 256 measured 1.3x
+// slower: half the bytes in flight per SM), halved until kFoldStages stages
+// of n8 rows fit in ~200 KB of shared memory (KRUL_FOLD_PITCH=256/128 caps).
 static int fold_pitch(int n8) {
   static const int env = fold_env("KRUL_FOLD_PITCH");
-  int pitch = env == 512 || env == 128 ? env : 256;
-  while (pitch > 128 && size_t(fold_stages()) * n8 * pitch * 4 > 200 * 1024) pitch /= 2;
+  int pitch = env == 256 || env == 128 ? env : 512;
+  while (pitch > 128 && size_t(kFoldStages) * n8 * pitch * 4 > 200 * 1024) pitch /= 2;
   return pitch;
 }
 
@@ -414,45 +408,29 @@ void launch_fold_direct(cudaStream_t s, const float* rows, int64_t layer_stride,
   const int grid = fold_grid(W, H, sms);
   if (fold_geom(n, W, H, grid).S > seg_S) fail(KRUL_E_CUDA, "fold segment slots too few");
   const FoldDeal deal = fold_deal(n);
-  const size_t smem = size_t(fold_stages()) * n8 * pitch * 4;
-  static const int pre = [] {  // chunks issued before the first one lands (KRUL_FOLD_PRE)
-    const int v = fold_env("KRUL_FOLD_PRE");
-    return v > 0 ? v : 99;
-  }();
-  static const int dbg = [] {  // diagnostics: 1 = skip the fold arithmetic, 2 = skip the row loads
+  const size_t smem = size_t(kFoldStages) * n8 * pitch * 4;
+  // diagnostics: 1 = skip the fold arithmetic, 2 = skip the row loads,
+  // 4 = skip the flushes, 32 = broadcast shared loads (same FP work)
+  static const int dbg = [] {
     const char* e = std::getenv("KRUL_FOLD_DBG");
     return e ? std::atoi(e) : 0;
   }();
-  auto go = [&](auto pitch_c, auto stages_c) {  // one static per variant (the kernels share one signature)
-    constexpr int PITCH = decltype(pitch_c)::value, ST = decltype(stages_c)::value;
+  auto go = [&](auto pitch_c) {  // one static per pitch (the kernels share one signature)
+    constexpr int PITCH = decltype(pitch_c)::value;
     static size_t smem_set = 0;
     if (smem > smem_set) {
-      KB_CUDA(cudaFuncSetAttribute(k_fold_direct<PITCH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      KB_CUDA(cudaFuncSetAttribute(k_fold_direct<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       smem_set = smem;
     }
-    k_fold_direct<PITCH, ST><<<unsigned(grid), kFoldWarps * 32, smem, s>>>(rows, layer_stride, head_stride, W, H,
-                                                                          d_layers, n, deal, seg, seg_S, pre, dbg);
+    k_fold_direct<PITCH><<<unsigned(grid), kFoldWarps * 32, smem, s>>>(rows, layer_stride, head_stride, W, H,
+                                                                      d_layers, n, deal, seg, seg_S, dbg);
   };
-  using I128 = std::integral_constant<int, 128>;
-  using I256 = std::integral_constant<int, 256>;
-  using I512 = std::integral_constant<int, 512>;
-  using S3 = std::integral_constant<int, 3>;
-  using S4 = std::integral_constant<int, 4>;
-  if (fold_stages() == 4) {
-    if (pitch == 512)
-      go(I512{}, S4{});
-    else if (pitch == 256)
-      go(I256{}, S4{});
-    else
-      go(I128{}, S4{});
-  } else {
-    if (pitch == 512)
-      go(I512{}, S3{});
-    else if (pitch == 256)
-      go(I256{}, S3{});
-    else
-      go(I128{}, S3{});
-  }
+  if (pitch == 512)
+    go(std::integral_constant<int, 512>{});
+  else if (pitch == 256)
+    go(std::integral_constant<int, 256>{});
+  else
+    go(std::integral_constant<int, 128>{});
   KB_LAUNCH();
 }
 

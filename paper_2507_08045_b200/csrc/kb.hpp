@@ -246,6 +246,8 @@ struct Ctx {
   cudaStream_t b_launch[2] = {nullptr, nullptr};
   bool kv_coding = true; // exponent-code bf16 snapshots at compress (KRUL_KV_CODING=0: off)
   PinnedBuf tok_pin;     // pinned token staging (history | new input) for async / graph H2D
+  DevBuf sel_dev;        // selector (K3) candidates + results, grown once
+  PinnedBuf sel_host;    // their pinned host image (one H2D, one D2H per call)
   PinnedBuf logits_pin;  // pinned logits landing buffer
   // CUDA graph of the last restore DAG (replayed when the key repeats)
   struct RestoreGraph {

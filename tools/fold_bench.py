@@ -10,11 +10,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2507_08045_b200 import native as K  # noqa: E402
 
-N, H, W = 32, 32, 8328
+N, H, W = 32, 32, int(os.environ.get("FOLD_W", 8328))
 cfg = K.ModelConfig(n_layers=N, n_heads=H, head_dim=4, d_model=4 * H, vocab_size=8,
                     dtype=K.KRUL_F32, max_tokens=64)
 ctx = K.Context(cfg, 0)
-rows = np.random.default_rng(0).dirichlet(np.ones(W), (N, H)).astype(np.float32)
+if os.environ.get("FOLD_DATA") == "softmax":  # peaked rows with tiny (subnormal) tails, like decode attention
+    z = np.random.default_rng(0).standard_normal((N, H, W)).astype(np.float32) * 12.0
+    z = np.exp(z - z.max(axis=-1, keepdims=True))
+    rows = (z / z.sum(axis=-1, keepdims=True)).astype(np.float32)
+    print("subnormal fraction", float(np.mean((rows > 0) & (rows < np.finfo(np.float32).tiny))),
+          "zero fraction", float(np.mean(rows == 0)))
+else:
+    rows = np.random.default_rng(0).dirichlet(np.ones(W), (N, H)).astype(np.float32)
 est = K.StreamingEstimator(ctx, list(range(N)))
 for _ in range(3):
     est.fold_decode_rows(rows)
