@@ -102,7 +102,9 @@ Snapshot* snapshot_compress(Ctx& c, Conv& conv, const krul_pair* pairs, int np, 
     const int64_t merge_from = pair ? p[b.owners[0]] : L;
     launch_compress(c, st, conv, deep, shallow, b.start, L, merge_from, stg + b.off);
   }
-  if (code && s->total) {
+  // a blob past the coded image's u32 offsets (> 4 GiB) keeps the snapshot raw
+  const bool fits = std::all_of(s->blobs.begin(), s->blobs.end(), [](const auto& b) { return ec_fits(b.bytes / 2); });
+  if (code && s->total && fits) {
     snapshot_encode(c, *s, stg, st);  // coded host store, one D2H of the coded image
   } else {
     s->host.ensure(std::max<size_t>(s->total, 256));
