@@ -21,5 +21,11 @@ cap dexp 'k_ec_decode_expand' 10 1 0.0
 cap logits 'k_logits' 0 1 0.0
 # the pyramid recompute's CTA-pair GEMMs
 cap gemm '^k_gemm_tc2$' 0 2 0.1
+# the K1 decode fold (32 layers x 32 heads x W 8328) alone: one --set full
+# capture, the per-CTA timeline and graph-replayed device time
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_fold_direct -c 1 \
+    -o $OUT/prof_fold_$TAG -f python tools/fold_bench.py > $OUT/prof_fold_$TAG.log 2>&1
+FOLD_TIMELINE=1 FOLD_LOOP=200 timeout 300 python tools/fold_bench.py > $OUT/fold_$TAG.txt 2>&1
+timeout 120 ./tools/exp/fp2_rate > $OUT/fp2_rate_$TAG.txt 2>&1
 bash tools/sanitize.sh $TAG
 echo done
