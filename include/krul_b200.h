@@ -182,6 +182,12 @@ int krul_est_fold_prefill_host(krul_est* est, const float* probs, int n_layers,
                                int64_t rows, int64_t width);
 int krul_est_fold_decode_host(krul_est* est, const float* rows, int n_layers,
                               int64_t width);
+/* Opt-in sampled token subset for the decode folds (north_star; not in the
+ * reference, so never used by the parity runs): fold every stride-th
+ * 64-column block of the attention row (phase = decode step mod stride, so
+ * each block is folded once per stride steps), scaled by W / sampled
+ * columns. stride 1 (default) folds every column exactly as the reference. */
+int krul_est_set_sampling(krul_est* est, int stride);
 int krul_est_sums(krul_est* est, double* sums); /* [pairs * n_heads] */
 int krul_est_finalize(krul_est* est, double* D); /* [n x n] */
 int krul_est_counts(krul_est* est, int64_t* prefill_rows, int64_t* decode_steps);

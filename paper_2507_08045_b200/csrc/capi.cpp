@@ -45,6 +45,7 @@ struct Est {
   int64_t partial_cap = 0;
   bool prefill_done = false;
   int64_t prefill_rows = 0, decode_steps = 0;
+  int sample_stride = 1;               // decode folds: every stride-th 64-column block (opt-in)
   int64_t host_W = 0, host_pitch = 0;  // rows of the last krul_est_fold_decode_host (in tmp)
   int host_N = 0;
   int P() const { return int(layers.size() * (layers.size() - 1) / 2); }
@@ -383,8 +384,11 @@ static void fold_decode_dev(Est& e, const float* rows, int64_t W, int64_t pitch,
   const int n = int(e.layers.size());
   const int sms = c.sm_count > 0 ? c.sm_count : 148;
   cudaEvent_t kt0 = kt_begin(c, c.s_est);
+  // the sampled token subset rotates its phase per step, so every block is
+  // folded once per `stride` steps
+  const int stride = e.sample_stride, phase = int(e.decode_steps % stride);
   launch_fold_direct(c.s_est, rows, int64_t(e.H) * pitch, pitch, W, e.H, e.d_layers.as<int>(), n,
-                     e.seg.as<double>(), e.seg_S, sms);
+                     e.seg.as<double>(), e.seg_S, sms, stride, phase);
   // algorithmic bytes: tracked rows read once + f64 accumulator RMW
   kt_end(c, c.s_est, kt0, KT_FOLD_DECODE, 0.0,
          double(e.layers.size()) * e.H * double(W) * 4.0 + double(e.P()) * e.H * 16.0);
@@ -535,6 +539,13 @@ int krul_debug_fold_repeat(krul_est* est, int iters, float* ms_per_fold) {
     cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
     *ms_per_fold = ms / float(std::max(iters, 1));
+  });
+}
+int krul_est_set_sampling(krul_est* est, int stride) {
+  return guard([&] {
+    need(est, "est");
+    if (stride < 1) fail(KRUL_E_CONFIG, "sampling stride must be >= 1");
+    est->e->sample_stride = stride;
   });
 }
 int krul_est_sums(krul_est* est, double* sums) {

@@ -160,9 +160,11 @@ __device__ __forceinline__ float warp_transpose_sum32(float (&v)[32], int lane) 
 struct FoldGeom {
   int cw, Q, S, rounds;
 };
-__host__ __device__ inline FoldGeom fold_geom(int n, int64_t W, int H, int grid) {
+// cw = column blocks per head in the fold's column space (all ceil(W / 64)
+// blocks, or the sampled ones)
+__host__ __device__ inline FoldGeom fold_geom(int n, int cw, int H, int grid) {
   FoldGeom g;
-  g.cw = int((W + 63) / 64);
+  g.cw = cw;
   const int64_t total = int64_t(H) * g.cw;
   g.Q = int((total + grid - 1) / grid);
   g.S = (g.cw + g.Q - 1) / g.Q + 1;
@@ -185,7 +187,8 @@ template <int PITCH>
 __global__ void __launch_bounds__(kFoldWarps * 32, 1)
     k_fold_direct(const float* __restrict__ rows, int64_t layer_stride, int64_t head_stride, int64_t W, int H,
                   const int* __restrict__ layers, int n, const __grid_constant__ FoldDeal deal,
-                  double* __restrict__ seg_acc, int seg_S, int dbg) {
+                  double* __restrict__ seg_acc, int seg_S, int cw, int stride, int phase, double scale,
+                  int dbg) {
   extern __shared__ __align__(128) float fbuf[];  // [kFoldStages][n8][PITCH]
   __shared__ __align__(8) uint64_t full[kFoldStages];
   __shared__ unsigned s_done[kFoldStages];  // warps done with the stage's current chunk
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, 1)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     g_fold_ts[blockIdx.x * 8 + 7] = smid;
   }
-  const FoldGeom g = fold_geom(n, W, H, gridDim.x);
+  const FoldGeom g = fold_geom(n, cw, H, gridDim.x);
   const int total = H * g.cw;
   const int g0 = min(total, int(blockIdx.x) * g.Q), g1 = min(total, g0 + g.Q);
   if (g1 <= g0) return;
@@ -232,29 +235,48 @@ __global__ void __launch_bounds__(kFoldWarps * 32, 1)
       it.b = b0;
     }
   };
+  // valid columns of the chunk `it` (only the row's last block is partial);
+  // block b of the column space is row block phase + b * stride
+  auto valid_of = [&](const FoldIt& it, int len) {
+    const int64_t last = int64_t(phase) + int64_t(it.b + len - 1) * stride;
+    return (len - 1) * 64 + int(min(int64_t(64), W - last * 64));
+  };
   // one warp: chunk `it` -> stage st
   auto produce = [&](const FoldIt& it, int st) {
     const int len = len_of(it);
-    const int64_t c0 = int64_t(it.b) * 64;
-    const int nc = len * 64;
-    const int valid = int(W - c0 < int64_t(nc) ? W - c0 : int64_t(nc));
-    // whole 16-byte units: past W this reads the row pitch's padding (host
-    // checks head_stride >= ceil4(W)), which the fold masks
-    const int bulk = (dbg & 2) ? 0 : (valid + 3) & ~3;
     float* dst = fbuf + st * stage_elems;
     __syncwarp();
     const uint32_t bar = fold_smem_u32(&full[st]);
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(n * bulk * 4))
-                   : "memory");
-    __syncwarp();
-    if (bulk > 0)  // one row per lane
-      for (int li = lane; li < n; li += 32)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                fold_smem_u32(dst + li * PITCH)),
-            "l"(s_row[li] + int64_t(it.h) * head_stride + c0), "r"(uint32_t(bulk * 4)), "r"(bar)
-            : "memory");
+    // whole 16-byte units: past W this reads the row pitch's padding (host
+    // checks head_stride >= ceil4(W)), which the fold masks
+    auto copy = [&](int li, int64_t c0, int cols, int soff) {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              fold_smem_u32(dst + li * PITCH + soff)),
+          "l"(s_row[li] + int64_t(it.h) * head_stride + c0), "r"(uint32_t(((cols + 3) & ~3) * 4)), "r"(bar)
+          : "memory");
+    };
+    if (stride == 1) {  // contiguous: one copy per row
+      const int64_t c0 = int64_t(it.b) * 64;
+      const int bulk = (dbg & 2) ? 0 : (valid_of(it, len) + 3) & ~3;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(n * bulk * 4))
+                     : "memory");
+      __syncwarp();
+      if (bulk > 0)  // one row per lane
+        for (int li = lane; li < n; li += 32) copy(li, c0, bulk, 0);
+    } else {  // sampled blocks: one copy per row and block
+      const int tail = (valid_of(it, len) - (len - 1) * 64 + 3) & ~3;
+      const uint32_t bytes = uint32_t(n) * uint32_t((len - 1) * 64 + tail) * 4u;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      __syncwarp();
+      for (int t = lane; t < n * len; t += 32) {
+        const int li = t / len, j = t - li * len;
+        const int64_t c0 = (int64_t(phase) + int64_t(it.b + j) * stride) * 64;
+        copy(li, c0, j == len - 1 ? tail : 64, j * 64);
+      }
+    }
   };
   const int nchunks = [&] {
     int c = 0;
@@ -280,8 +302,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, 1)
     const uint32_t u = q < deal.units ? deal.u[q] : 0xFFFFFFFFu;
     const int type = int(u >> 24), I = int((u >> 16) & 0xFF), J = int((u >> 8) & 0xFF), hh = int(u & 0xFF);
     const int ra = I * 8 + (type == kUnitOff ? 4 * hh : 0), rb = type == kUnitOff ? J * 8 : ra;
-    const int64_t cl = W - int64_t(it.b) * 64;
-    const int valid = cl < int64_t(len) * 64 ? int(cl) : len * 64;
+    const int valid = valid_of(it, len);
     fold_mbar_wait(&full[st], ph);
     if (k < 4) fold_ts(3 + k);
     const float* buf = fbuf + st * stage_elems;
@@ -333,7 +354,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32, 1)
         }
         if (a < bb && bb < n) {
           const int pp = a * n - a * (a + 1) / 2 + (bb - a - 1);
-          seg_acc[(int64_t(h) * seg_S + seg) * P + pp] += double(sum);
+          seg_acc[(int64_t(h) * seg_S + seg) * P + pp] += double(sum) * scale;
         }
       }
     }
@@ -383,8 +404,8 @@ static FoldDeal fold_deal(int n) {
   return d;
 }
 
-static int fold_grid(int64_t W, int H, int sms) {
-  return int(std::max<int64_t>(1, std::min<int64_t>(sms, int64_t(H) * ((W + 63) / 64))));
+static int fold_grid(int cw, int H, int sms) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(sms, int64_t(H) * cw)));
 }
 
 int fold_seg_slots(int H, int sms) { return sms / std::max(H, 1) + 2; }
@@ -397,16 +418,26 @@ void launch_fold_collect(cudaStream_t s, double* seg, int S, int n, int H, doubl
 }
 
 void launch_fold_direct(cudaStream_t s, const float* rows, int64_t layer_stride, int64_t head_stride, int64_t W,
-                        int H, const int* d_layers, int n, double* seg, int seg_S, int sms) {
+                        int H, const int* d_layers, int n, double* seg, int seg_S, int sms, int stride, int phase) {
   if (n < 2 || W <= 0) return;
+  if (stride < 1 || phase < 0 || phase >= stride) fail(KRUL_E_CONFIG, "fold sampling: need stride >= 1, 0 <= phase < stride");
+  // sampled token subset (opt-in): row blocks phase, phase + stride, ...;
+  // each sampled sum is scaled by W / sampled columns (an estimate of the
+  // full-width sum; stride 1 folds every column with scale 1 exactly)
+  const int64_t cw_all = (W + 63) / 64;
+  if (phase >= cw_all) return;
+  const int cw = int((cw_all - 1 - phase) / stride + 1);
+  const int64_t last = phase + int64_t(cw - 1) * stride;
+  const int64_t sampled_cols = int64_t(cw - 1) * 64 + std::min<int64_t>(64, W - last * 64);
+  const double scale = stride == 1 ? 1.0 : double(W) / double(sampled_cols);
   if (n > kFoldMaxLayers) fail(KRUL_E_CONFIG, "too many tracked layers for the estimator fold (max 80)");
   const int n8 = (n + 7) & ~7;
   if (((reinterpret_cast<uintptr_t>(rows) | uintptr_t(layer_stride * 4) | uintptr_t(head_stride * 4)) & 15) != 0)
     fail(KRUL_E_CUDA, "decode fold rows must be 16-byte aligned with 16-byte row pitch");
   if (head_stride < (W + 3) / 4 * 4) fail(KRUL_E_CUDA, "decode fold rows: head stride below the 16-byte-padded width");
   const int pitch = fold_pitch(n8);
-  const int grid = fold_grid(W, H, sms);
-  if (fold_geom(n, W, H, grid).S > seg_S) fail(KRUL_E_CUDA, "fold segment slots too few");
+  const int grid = fold_grid(cw, H, sms);
+  if (fold_geom(n, cw, H, grid).S > seg_S) fail(KRUL_E_CUDA, "fold segment slots too few");
   const FoldDeal deal = fold_deal(n);
   const size_t smem = size_t(kFoldStages) * n8 * pitch * 4;
   // diagnostics: 1 = skip the fold arithmetic, 2 = skip the row loads,
@@ -423,7 +454,8 @@ void launch_fold_direct(cudaStream_t s, const float* rows, int64_t layer_stride,
       smem_set = smem;
     }
     k_fold_direct<PITCH><<<unsigned(grid), kFoldWarps * 32, smem, s>>>(rows, layer_stride, head_stride, W, H,
-                                                                      d_layers, n, deal, seg, seg_S, dbg);
+                                                                      d_layers, n, deal, seg, seg_S, cw, stride, phase,
+                                                                      scale, dbg);
   };
   if (pitch == 512)
     go(std::integral_constant<int, 512>{});

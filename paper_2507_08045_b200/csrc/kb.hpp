@@ -430,8 +430,11 @@ void launch_prefill_probs(const Ctx& c, cudaStream_t s, const Conv& conv, const 
 // slots into sums[p][h] and zeroes them.
 int fold_seg_slots(int H, int sms);
 void fold_set_timeline(unsigned long long* d);  // debug: per-CTA %globaltimer stamps [cta][8]
+// stride > 1: the sampled token subset (opt-in, krul_est_set_sampling):
+// 64-column blocks phase, phase + stride, ... folded, scaled by W / sampled
 void launch_fold_direct(cudaStream_t s, const float* rows, int64_t layer_stride, int64_t head_stride, int64_t W,
-                        int H, const int* d_layers, int n, double* seg, int seg_S, int sms);
+                        int H, const int* d_layers, int n, double* seg, int seg_S, int sms, int stride = 1,
+                        int phase = 0);
 void launch_fold_collect(cudaStream_t s, double* seg, int seg_S, int n, int H, double* sums);
 // selector: candidates sorted on device then greedily matched
 void launch_select(cudaStream_t s, const double* cand_d, const int* cand_i, const int* cand_j,

@@ -486,6 +486,12 @@ class StreamingEstimator:
         N, H, R, W = p.shape
         _check(lib().krul_est_fold_prefill_host(self.h, _p(p), N, C.c_int64(R), C.c_int64(W)))
 
+    def set_sampling(self, stride: int):
+        """Opt-in sampled token subset for the decode folds (every stride-th
+        64-column block, rotating per step, scaled to the full width); 1 =
+        every column, the reference's fold."""
+        _check(lib().krul_est_set_sampling(self.h, int(stride)))
+
     def fold_decode_rows(self, rows):
         r = np.ascontiguousarray(rows, np.float32)
         N, H, W = r.shape

@@ -292,6 +292,42 @@ def test_estimator_decode_fold_shapes(K, oracle, n, H, W):
     assert rel.max() < 1e-6, (rel.max(), int(rel.argmax()), got[rel.argmax()], want[rel.argmax()])
 
 
+@pytest.mark.parametrize("stride,W", [(3, 1000), (2, 8328), (5, 130)])
+def test_estimator_sampled_token_subset(K, stride, W):
+    """Opt-in sampled decode folds (not a parity mode): step t folds the
+    64-column blocks b with b % stride == t % stride, each pair-head sum
+    scaled by W / sampled columns. Checked against the same sampled sum in
+    numpy (f32 difference, f64 square-sum), rel <= 1e-6."""
+    n, H = 12, 4
+    cfg = K.ModelConfig(n_layers=n, n_heads=H, head_dim=4, d_model=4 * H, vocab_size=5,
+                        dtype=K.KRUL_F32, max_tokens=64)
+    ctx = K.Context(cfg, 0)
+    rng = np.random.default_rng(stride * 7 + W)
+    est = K.StreamingEstimator(ctx, list(range(n)))
+    est.set_sampling(stride)
+    want = np.zeros((n * (n - 1) // 2, H))
+    for t in range(stride + 1):
+        w = W + t
+        rows = rng.dirichlet(np.ones(w), (n, H)).astype(np.float32)
+        est.fold_decode_rows(rows)
+        blocks = [np.arange(b * 64, min(w, b * 64 + 64)) for b in range((w + 63) // 64) if b % stride == t % stride]
+        if not blocks:  # this step's phase has no block in a row this short: nothing is folded
+            continue
+        cols = np.concatenate(blocks)
+        scale = w / len(cols)
+        p = 0
+        for a in range(n):
+            for b in range(a + 1, n):
+                d = (rows[a][:, cols] - rows[b][:, cols]).astype(np.float64)  # f32 difference, widened
+                want[p] += scale * (d * d).sum(axis=1)
+                p += 1
+    got = est.sums().reshape(-1, H)
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() < 1e-6, rel.max()
+    with pytest.raises(K.ConfigError):
+        est.set_sampling(0)
+
+
 def test_estimator_on_engine_capture(K, oracle):
     kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
     ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_F32, **kw)

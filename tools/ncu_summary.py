@@ -23,6 +23,8 @@ KEYS = [
     ("launch__registers_per_thread", "regs/thread"),
     ("launch__shared_mem_per_block", "smem/block"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe cycles active %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
 ]
 
 
