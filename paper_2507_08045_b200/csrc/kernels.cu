@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256) k_attn_decode1(const bf16* __restrict__ q
   const int64_t k0 = int64_t(blockIdx.x) * kDecChunk;
   const int nk = int(W - k0 < kDecChunk ? W - k0 : kDecChunk);
   __shared__ float qs[kDecMaxG][HD];
-  __shared__ float ps[kDecMaxG][kDecChunk];
+  __shared__ __align__(16) float ps[kDecMaxG][kDecChunk];
   __shared__ float red[kDecMaxG][8];
   __shared__ float o2[kDecMaxG][HD];
   for (int i = threadIdx.x; i < G * HD; i += blockDim.x) qs[i / HD][i % HD] = __bfloat162float(q[(h0 + i / HD) * HD + i % HD]) * scale;
@@ -367,12 +367,22 @@ __global__ void __launch_bounds__(256) k_attn_decode1(const bf16* __restrict__ q
     const uint4 x = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(pv.page(k)) +
                                                          pv.v_off(g, k, d)));
     const uint32_t u[4] = {x.x, x.y, x.z, x.w};
+    float t[8];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[e]));
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[e]));
+      t[2 * e] = f.x;
+      t[2 * e + 1] = f.y;
+    }
+    // the 8 probabilities of each head as two broadcast 16-byte shared loads
 #pragma unroll
-      for (int hh = 0; hh < kDecMaxG; ++hh)
-        if (hh < G) acc[hh] += ps[hh][i + 2 * e] * t.x + ps[hh][i + 2 * e + 1] * t.y;
+    for (int hh = 0; hh < kDecMaxG; ++hh) {
+      if (hh < G) {
+        const float4 p0 = *reinterpret_cast<const float4*>(&ps[hh][i]);
+        const float4 p1 = *reinterpret_cast<const float4*>(&ps[hh][i + 4]);
+        acc[hh] += p0.x * t[0] + p0.y * t[1] + p0.z * t[2] + p0.w * t[3] + p1.x * t[4] + p1.y * t[5] +
+                   p1.z * t[6] + p1.w * t[7];
+      }
     }
   }
   for (; i < i1; ++i) {
