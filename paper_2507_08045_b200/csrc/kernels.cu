@@ -436,13 +436,25 @@ __global__ void __launch_bounds__(256) k_attn_decode2(const float* __restrict__ 
   __syncthreads();
   m = sh_ml[0];
   l = sh_ml[1];
-  if (blockIdx.y == 0 && threadIdx.x < HD) {
+  if (blockIdx.y == 0) {  // context row: the two thread halves take alternate chunks, loads batched
+    __shared__ float oh[HD];
+    const int d = threadIdx.x & (HD - 1), hf = threadIdx.x >> 7;
     float o = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const float* pp = part + (int64_t(c) * H + h) * (HD + 2);
-      o += pp[threadIdx.x] * expf(pp[HD] - m);
+    for (int c0 = hf; c0 < nchunks; c0 += 16) {
+      float pv[8], ev[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + 2 * u;
+        const float* pp = part + (int64_t(c) * H + h) * (HD + 2);
+        pv[u] = c < nchunks ? pp[d] : 0.f;
+        ev[u] = c < nchunks ? pp[HD] : -FLT_MAX;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o += pv[u] * expf(ev[u] - m);
     }
-    out[int64_t(h) * HD + threadIdx.x] = __float2bfloat16_rn(o / l);
+    if (hf == 1) oh[d] = o;
+    __syncthreads();
+    if (hf == 0) out[int64_t(h) * HD + d] = __float2bfloat16_rn((o + oh[d]) / l);
   }
   if (probs) {
     const int64_t per = (W + gridDim.y - 1) / gridDim.y;
