@@ -744,7 +744,7 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
     # per-step times, the two modes interleaved, medians: the eager decode
     # step is host-launch-bound and a shared host adds bursty noise
     tpot = {False: [], True: []}
-    for i in range(24):
+    for i in range(48):
         with_est = bool(i & 1)
         t0 = time.perf_counter()
         ctx.decode_step(conv, int(rng.integers(0, cfg.vocab_size)))
@@ -798,7 +798,7 @@ def estimator_leg(K, ctx, conv, cfg, spec, steps=8):
             "tpot": {"decode_step_ms": round(tpot[False], 3),
                      "decode_step_with_estimator_ms": round(tpot[True], 3),
                      "estimator_overhead": round(tpot[True] / tpot[False] - 1.0, 4),
-                     "note": "median wall clock of 12 synchronous decode steps per mode (eager launches, "
+                     "note": "median wall clock of 24 synchronous decode steps per mode (eager launches, "
                              "modes interleaved) at the restored context length, all layers tracked"},
             "select": {"bound": "latency", "kernel": "k_select (K3) incl. D upload + result read",
                        "us_per_call": round(sel_us, 1), "pairs_selected": len(strat.pairs),
