@@ -22,12 +22,12 @@ def K():
     return native
 
 
-def make_pair(K, O, dtype, **kw):
+def make_pair(K, O, dtype, max_tokens=1024, **kw):
     base = dict(n_layers=3, n_heads=2, head_dim=4, d_model=8, vocab_size=17, ffn_mult=2.0, seed=5)
     base.update(kw)
     ocfg = O.ModelConfig(**base)
     om = O.Model(ocfg)
-    cfg = K.ModelConfig(**base, dtype=dtype, max_tokens=1024)
+    cfg = K.ModelConfig(**base, dtype=dtype, max_tokens=max_tokens)
     ctx = K.Context(cfg, 0)
     ctx.upload_weights(om.weights())
     return ocfg, om, cfg, ctx
@@ -909,6 +909,29 @@ def test_decode_attention_split_keys_matches_simt(K, oracle):
             assert np.abs(rows[0] - rr[0]).max() < 1e-5  # layer 0: identical inputs
             assert rel_fro(rows, rr) < 2e-2              # deeper: bf16 hidden-state drift
             np.testing.assert_allclose(rows.reshape(-1, rows.shape[-1]).sum(axis=-1), 1.0, atol=1e-4)
+
+
+@pytest.mark.parametrize("L", [63, 700, 2049])
+def test_decode_attention_split_keys_matches_oracle(K, oracle, L):
+    """The bf16 split-key decode (k_attn_decode1/2, GQA 4 heads per KV head,
+    hd 128, SwiGLU) against the oracle's decode_step (engine.cpp:406-446)
+    directly: logits and every layer's captured probability row after the
+    same prefill, three steps (bf16 tolerance rel-Fro <= 3e-2; rows sum to 1)."""
+    kw = dict(n_layers=2, n_heads=8, n_kv_heads=2, head_dim=128, d_model=1024, vocab_size=512,
+              ffn_mult=3.5, ffn_kind=1, rope_theta=500000.0, seed=3)
+    ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, max_tokens=L + 16, **kw)
+    toks = oracle.tokens(L, 9, 512)
+    conv = ctx.conversation(L + 16)
+    ctx.prefill(conv, toks)
+    okv = om.prefill(toks).take_kv()
+    for t in range(3):
+        lg = ctx.decode_step(conv, 7 + t)
+        rows = ctx.captured_decode()
+        olg, orows = om.decode(okv, 7 + t)
+        assert rel_fro(lg, olg) < 3e-2, (L, t)
+        assert rows.shape == orows.shape, (rows.shape, orows.shape)
+        assert rel_fro(rows, orows) < 3e-2, (L, t)
+        np.testing.assert_allclose(rows.reshape(-1, rows.shape[-1]).sum(axis=-1), 1.0, atol=1e-4)
 
 
 def test_calibrate_rc_measured_contract(K, oracle):
