@@ -50,8 +50,9 @@ except Exception:
 NCU_TRAFFIC = {
     "gemm": (276_462_080, 1078 * 4096 * 2 + 28672 * 4096 * 2 + 1078 * 14336 * 2,
              "profiles/r01c/SUMMARY.md (FFN1 pair GEMM, M=1078 N=28672 K=4096)"),
-    "gemm_stream": (241502208, 28672 * 4096 * 2 + 128 * 4096 * 2 + 128 * 14336 * 2,
-                    "profiles/r01d/ncu_gstream.md (new-input FFN1, M=128 N=28672 K=4096, SwiGLU epilogue)"),
+    "gemm_stream": (236031744 + 4214016, 28672 * 4096 * 2 + 128 * 4096 * 2 + 128 * 14336 * 2,
+                    "profiles/r02/ncu_gstream.md (new-input FFN1, M=128 N=28672 K=4096, SwiGLU epilogue, "
+                    "k_gemm_tc<256,4,4> cluster split-K, dram read + write)"),
 }
 
 METRIC = ("restoration TTFT p50 (ms) @8K history; conversations restored/sec at 1/2/4/8 GPU")
