@@ -975,15 +975,110 @@ __device__ __forceinline__ void expand_tile(const T* blob, int64_t blob_start, i
     }
   }
 }
+// TMA-staged full page (bf16, every page but a ragged head / tail): the
+// blob's K rows [64][hd] and V rows [64][hd] arrive in shared memory by two
+// bulk copies (cp.async.bulk, one mbarrier); the K block leaves by one bulk
+// store to the page's contiguous K block; V is transposed in shared memory
+// (lane = one 32-bit column pair, conflict-free reads) into a [hd][64 + 8]
+// tile whose rows leave as hd bulk stores of 128 B (the page's V^T block).
+// Returns false when the tile does not qualify (the caller takes the
+// vector path): partial page, or a blob source not 16-byte aligned.
+constexpr int kExVtPitch = kPageTokens + 8;  // bf16 elements; 144 B rows (16-byte aligned, 2-way stores)
+__device__ __forceinline__ uint32_t ex_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ bool expand_tile_tma(const bf16* blob, int64_t blob_start, int64_t L,
+                                                const PageView& pv, int64_t from, int64_t ti,
+                                                unsigned char* sm, uint32_t& phase) {
+  const int hd = pv.hd, Hkv = pv.Hkv;
+  const int g = blockIdx.y;
+  const int64_t p0 = (from / kPageTokens + ti) * kPageTokens;
+  if (p0 < from || p0 + kPageTokens > L || (hd % 8) != 0) return false;
+  const int64_t rows_blob = L - blob_start;
+  const int64_t krow0 = p0 - blob_start;
+  const bf16* ksrc = blob + (int64_t(g) * rows_blob + krow0) * hd;
+  const bf16* vsrc = blob + (int64_t(Hkv + g) * rows_blob + krow0) * hd;
+  if (((reinterpret_cast<uintptr_t>(ksrc) | reinterpret_cast<uintptr_t>(vsrc)) & 15) != 0) return false;
+  const uint32_t bytes = uint32_t(kPageTokens) * hd * 2;
+  bf16* kbuf = reinterpret_cast<bf16*>(sm);
+  bf16* vbuf = kbuf + kPageTokens * hd;
+  bf16* vt = vbuf + kPageTokens * hd;  // [hd][kExVtPitch]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vt + hd * kExVtPitch);
+  bf16* page = reinterpret_cast<bf16*>(pv.page(p0));
+  bf16* kdst = page + pv.k_off(g, p0, 0);
+  bf16* vdst = page + pv.v_off(g, p0, 0);  // [hd][64] contiguous
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ex_smem_u32(bar)),
+                 "r"(2 * bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(ex_smem_u32(kbuf)), "l"(ksrc), "r"(bytes), "r"(ex_smem_u32(bar)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(ex_smem_u32(vbuf)), "l"(vsrc), "r"(bytes), "r"(ex_smem_u32(bar)) : "memory");
+  }
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "EXW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra EXD_%=;\n\t"
+      "bra EXW_%=;\n"
+      "EXD_%=:\n\t}" ::"r"(ex_smem_u32(bar)), "r"(phase) : "memory");
+  phase ^= 1u;
+  if (threadIdx.x == 0)  // K: the staged block is the page's K block
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(kdst), "r"(ex_smem_u32(kbuf)), "r"(bytes) : "memory");
+  // V^T: work item = (column pair, 8-row group); a warp's 32 lanes read 32
+  // consecutive 32-bit words of one row -> 32 distinct banks
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vbuf);
+  const int cp = hd / 2;
+  for (int i = threadIdx.x; i < cp * (kPageTokens / 8); i += blockDim.x) {
+    const int c2 = i % cp, r8 = (i / cp) * 8;
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[j] = vw[(r8 + j) * cp + c2];
+    uint4 lo, hi;
+    lo.x = (w[0] & 0xffffu) | (w[1] << 16); lo.y = (w[2] & 0xffffu) | (w[3] << 16);
+    lo.z = (w[4] & 0xffffu) | (w[5] << 16); lo.w = (w[6] & 0xffffu) | (w[7] << 16);
+    hi.x = (w[0] >> 16) | (w[1] & 0xffff0000u); hi.y = (w[2] >> 16) | (w[3] & 0xffff0000u);
+    hi.z = (w[4] >> 16) | (w[5] & 0xffff0000u); hi.w = (w[6] >> 16) | (w[7] & 0xffff0000u);
+    *reinterpret_cast<uint4*>(vt + (2 * c2) * kExVtPitch + r8) = lo;
+    *reinterpret_cast<uint4*>(vt + (2 * c2 + 1) * kExVtPitch + r8) = hi;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  for (int t = threadIdx.x; t < hd; t += blockDim.x)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(vdst + int64_t(t) * kPageTokens), "r"(ex_smem_u32(vt + t * kExVtPitch)),
+                 "r"(uint32_t(kPageTokens * 2)) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before smem reuse / exit
+  return true;
+}
+__host__ __device__ inline size_t expand_tma_smem(int hd) {
+  return size_t(2) * kPageTokens * hd * 2 + size_t(hd) * kExVtPitch * 2 + 16;
+}
+
 // One CTA per (page tile, kv head), or a CTA-capped grid-stride loop over
 // the tiles (KRUL_EXPAND_CTAS) so the scatter leaves SMs to the recompute.
 template <class T>
 __global__ void k_expand(const T* blob, int64_t blob_start, int64_t L, PageView pv, int64_t from,
                          int64_t tiles) {
-  extern __shared__ unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   T* tile = reinterpret_cast<T*>(smraw);  // [kPageTokens][hd + pad]
+  uint32_t phase = 0;
+  if constexpr (sizeof(T) == 2) {
+    if (threadIdx.x == 0) {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + expand_tma_smem(pv.hd) - 16);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ex_smem_u32(bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   for (int64_t ti = blockIdx.x; ti < tiles; ti += gridDim.x) {
-    expand_tile(blob, blob_start, L, pv, from, ti, tile);
+    bool done = false;
+    if constexpr (sizeof(T) == 2)
+      done = expand_tile_tma(reinterpret_cast<const bf16*>(blob), blob_start, L, pv, from, ti, smraw, phase);
+    if (!done) expand_tile(blob, blob_start, L, pv, from, ti, tile);
     __syncthreads();
   }
 }
@@ -1164,8 +1259,9 @@ void launch_expand_impl(const Ctx& c, cudaStream_t s, const void* blob, int64_t 
     return v ? std::atoi(v) : 0;
   }();
   if (cap > 0) grid.x = unsigned(std::min<int64_t>(tiles, std::max(1, cap / int(c.cfg.Hkv))));
-  const size_t smem = size_t(kPageTokens) * (c.cfg.hd + 2) * c.esz + 16;
+  size_t smem = size_t(kPageTokens) * (c.cfg.hd + 2) * c.esz + 16;
   if (c.cfg.dtype == KRUL_BF16) {
+    smem = std::max(smem, expand_tma_smem(c.cfg.hd));
     KB_CUDA(cudaFuncSetAttribute(k_expand<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     k_expand<bf16><<<grid, 256, smem, s>>>((const bf16*)blob, blob_start, L, pv, from, tiles);

@@ -735,12 +735,16 @@ def test_kvcode_device_matches_host(K, n):
     assert np.array_equal(dec, x)
 
 
-def test_coded_store_restores_bit_exact(K, oracle, monkeypatch):
+@pytest.mark.parametrize("hd", [64, 128])
+def test_coded_store_restores_bit_exact(K, oracle, monkeypatch, hd):
     """The coded store (H2D of the coded image + device decode) restores the
     same bits as the raw store: identical logits, KV, blob values and
-    container bytes; the load stream moves fewer bytes."""
+    container bytes; the load stream moves fewer bytes. At hd = 128 the two
+    arms share no kernel: the raw store goes through the TMA-staged k_expand
+    (bulk copies in, bulk stores out; ragged head / tail pages on the
+    vector path), the coded one through the fused k_ec_decode_expand."""
     monkeypatch.setenv("KRUL_KV_POOL_CONVS", "6")
-    kw = dict(n_layers=4, n_heads=4, head_dim=64, d_model=256, vocab_size=256, ffn_mult=4.0, seed=7)
+    kw = dict(n_layers=4, n_heads=4, head_dim=hd, d_model=4 * hd, vocab_size=256, ffn_mult=4.0, seed=7)
     ocfg, om, cfg, ctx = make_pair(K, oracle, K.KRUL_BF16, **kw)
     hist = oracle.tokens(700, 11, 256)
     new = oracle.tokens(64, 12, 256)
