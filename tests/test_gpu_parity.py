@@ -778,6 +778,22 @@ def test_coded_store_restores_bit_exact(K, oracle, monkeypatch, hd):
     assert raw.coding() == cod.coding()
 
 
+def test_expand_cta_capped_loop_bit_exact():
+    """KRUL_EXPAND_CTAS caps the k_expand grid, so each CTA walks several
+    page tiles through the TMA-staged path (the mbarrier phase flips per
+    tile, shared memory reused behind the bulk stores). The cap is read once
+    per process: the hd-128 raw-vs-coded test runs again in a child."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, KRUL_EXPAND_CTAS="8")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"{__file__}::test_coded_store_restores_bit_exact[128]"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "1 passed" in r.stdout
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_fused_recompute_matches_separate_stream(K, oracle, dtype, monkeypatch):
     """The fused DAG (recompute rows inside the new-input prefill's layer
